@@ -1,0 +1,132 @@
+/*
+ * ewald_b200.h -- C-ABI of the B200-native classical Ewald library
+ * (libewaldb200.so).  Plain pointers and sizes only; no torch types.
+ *
+ * Every entry point replaces one reference interface of the Python package
+ * ewaldmd (paths are relative to /root/reference/pkg/src/ewaldmd):
+ *
+ *   ewb_set_system        EwaldParams / coulomb_short_range_kernel consts
+ *                         (ewald.py:40-72, 243-259)
+ *   ewb_set_kspace        ReciprocalSpace.__init__ (ewald.py:150-168)
+ *   ewb_compute_rho_hat   compute_rho_hat           (ewald.py:457-464)
+ *   ewb_long_range        long_range_energy_forces  (ewald.py:467-479)
+ *   ewb_short_range       PairLoop(coulomb_short_range) over build_cell_list
+ *                         (ewald.py:639-643, engine.py:283-324,
+ *                          celllist.py:75-108)
+ *   ewb_self_energy       self_energy               (ewald.py:482-484)
+ *   ewb_evaluate          EwaldSolver.evaluate      (ewald.py:629-655)
+ *
+ * Host-pointer entry points copy inputs host->device and results back; they
+ * follow the reference's argument meaning exactly: pos is (N,3) C-order
+ * xyz-interleaved float64, q is (N,), force is (N,3) and is ACCUMULATED
+ * (+=, ewald.py:603-605), rho is the GlobalAccumulator layout: K real parts
+ * followed by K imaginary parts, rho(k) = sum_j q_j exp(-i k.r_j), K in the
+ * caller's m_int order (ewald.py:170-173, 303-305).
+ *
+ * ewb_dev_* entry points take DEVICE pointers and run on the stream set by
+ * ewb_set_stream; they are the stages a multi-GPU driver composes around its
+ * collectives (particle-sharded S(k) partials -> all-reduce -> force gather).
+ *
+ * All functions return an ewb_status; ewb_last_error() gives the message.
+ * A handle is not thread-safe (same contract as the reference engine,
+ * SPEC.md:181).
+ */
+#ifndef EWALD_B200_H
+#define EWALD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ewb_handle ewb_handle;
+
+typedef enum {
+    EWB_OK = 0,
+    EWB_EINVAL = 1,      /* ValueError                       */
+    EWB_ECOINCIDENT = 2, /* CoincidentParticlesError (r^2==0) */
+    EWB_ECUTOFF = 3,     /* CutoffTooLargeError (r_c > L/2)  */
+    EWB_EUNWRAPPED = 4,  /* ValueError: positions not in [0,L) */
+    EWB_ECUDA = 5,       /* RuntimeError: CUDA failure        */
+    EWB_EKSPACE = 7,     /* KSpaceEmptyError                  */
+    EWB_ESTATE = 8       /* RuntimeError: call order violated */
+} ewb_status;
+
+/* library / handle lifetime */
+int ewb_version(void);
+int ewb_create(int device, ewb_handle **out);
+void ewb_destroy(ewb_handle *h);
+const char *ewb_last_error(const ewb_handle *h);
+/* stream used by every later call (0 = the handle's own stream) */
+int ewb_set_stream(ewb_handle *h, uintptr_t stream);
+/* tuning knob: maximum k-column segment length (1..32; default 28) */
+int ewb_set_max_segment(ewb_handle *h, int mcap);
+
+/* EwaldParams: box edge L, screening alpha (A^-2, erfc(sqrt(alpha) r)),
+ * real-space cutoff.  rc2 is r_cutoff**2 as the caller computed it, so the
+ * cutoff predicate r2 < rc2 is bit-identical to the reference's. */
+int ewb_set_system(ewb_handle *h, double L, double alpha, double r_cutoff,
+                   double rc2);
+
+/* ReciprocalSpace: m_int (K,3) int64 in caller order, coeff (K,) C_k. */
+int ewb_set_kspace(ewb_handle *h, const int64_t *m_int, int64_t K,
+                   const double *coeff);
+/* plan summary: [K, n_items, M, n_rows, n_tiles, max_table] */
+int ewb_kspace_info(const ewb_handle *h, int64_t *info6);
+
+/* ---- host-pointer entry points (reference-facing) ---- */
+int ewb_compute_rho_hat(ewb_handle *h, const double *pos, const double *q,
+                        int64_t n, double *rho_out);
+int ewb_long_range(ewb_handle *h, const double *pos, const double *q,
+                   int64_t n, const double *rho, double *force_inout,
+                   double *u_lr);
+int ewb_short_range(ewb_handle *h, const double *pos, const double *q,
+                    int64_t n, double *force_inout, double *u_sr);
+int ewb_self_energy(ewb_handle *h, const double *q, int64_t n,
+                    double *u_self);
+/* energies[3] = u_sr, u_lr, u_self; timings[4] = t_cell, t_sr, t_alg1,
+ * t_alg2 in seconds (device events); rho_out may be NULL. */
+int ewb_evaluate(ewb_handle *h, const double *pos, const double *q,
+                 int64_t n, double *force_inout, double *rho_out,
+                 double *energies, double *timings);
+
+/* ---- device-pointer stages (multi-GPU driver, device-resident bench) ---- */
+/* Load particles (device pos (N,3), q (N,)); validates wrapping. */
+int ewb_dev_load(ewb_handle *h, const double *d_pos, const double *d_q,
+                 int64_t n);
+/* Number of doubles of the slot-layout S(k) buffer (2 * M * n_items). */
+int64_t ewb_dev_slot_doubles(const ewb_handle *h);
+/* S(k) partial over particles [i0, i1) into d_slots (slot layout). */
+int ewb_dev_rho_partial(ewb_handle *h, int64_t i0, int64_t i1,
+                        double *d_slots);
+/* From complete slot-layout S(k): rho_out (device, 2K, may be NULL),
+ * internal C*S for the force gather, and u_lr = sum_k C_k |S_k|^2. */
+int ewb_dev_kspace_finalize(ewb_handle *h, const double *d_slots,
+                            double *d_rho_out, double *u_lr);
+/* Reciprocal forces of particles [i0, i1), added into d_force (N,3). */
+int ewb_dev_recip_forces(ewb_handle *h, int64_t i0, int64_t i1,
+                         double *d_force);
+/* Real-space forces of the particles whose home cell lies in z-slab
+ * part/nparts, added into d_force (N,3); u_sr of those particles. */
+int ewb_dev_real_space(ewb_handle *h, int part, int nparts, double *d_force,
+                       double *u_sr);
+/* Self energy -sqrt(alpha/pi) * sum q^2 over all loaded particles. */
+int ewb_dev_self_energy(ewb_handle *h, double *u_self);
+/* Whole evaluation on device-resident data (single GPU); force +=. */
+int ewb_dev_evaluate(ewb_handle *h, const double *d_pos, const double *d_q,
+                     int64_t n, double *d_force, double *d_rho_out,
+                     double *energies, double *timings);
+/* Kernels launched by this handle since creation (evidence counter). */
+int64_t ewb_launch_count(const ewb_handle *h);
+
+/* ---- harness helper (csrc/workloads.c, separate library) ----
+ * int ewb_gen_hardcore_gas(int64_t n, double L, double min_sep,
+ *                          uint64_t seed, int64_t max_attempts,
+ *                          double *pos_out, int64_t *attempts_out);
+ */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EWALD_B200_H */

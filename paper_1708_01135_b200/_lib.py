@@ -1,0 +1,258 @@
+"""ctypes binding of libewaldb200.so (the C-ABI in include/ewald_b200.h).
+
+There is no fallback: if the shared library is missing or no CUDA device is
+usable, every entry point raises.  Status codes map onto the reference's
+exception classes (core.py:14-55).
+"""
+
+import ctypes
+import os
+
+import numpy as np
+
+from .core import (
+    CoincidentParticlesError,
+    CutoffTooLargeError,
+    KSpaceEmptyError,
+)
+
+LIB_NAME = "libewaldb200.so"
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+
+EWB_OK = 0
+EWB_EINVAL = 1
+EWB_ECOINCIDENT = 2
+EWB_ECUTOFF = 3
+EWB_EUNWRAPPED = 4
+EWB_ECUDA = 5
+EWB_EKSPACE = 7
+EWB_ESTATE = 8
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_D = ctypes.c_double
+_INT = ctypes.c_int
+
+#: every symbol include/ewald_b200.h declares, with (restype, argtypes)
+SIGNATURES = {
+    "ewb_version": (_INT, []),
+    "ewb_create": (_INT, [_INT, ctypes.POINTER(_P)]),
+    "ewb_destroy": (None, [_P]),
+    "ewb_last_error": (ctypes.c_char_p, [_P]),
+    "ewb_set_stream": (_INT, [_P, ctypes.c_size_t]),
+    "ewb_set_max_segment": (_INT, [_P, _INT]),
+    "ewb_set_system": (_INT, [_P, _D, _D, _D, _D]),
+    "ewb_set_kspace": (_INT, [_P, _P, _I64, _P]),
+    "ewb_kspace_info": (_INT, [_P, _P]),
+    "ewb_compute_rho_hat": (_INT, [_P, _P, _P, _I64, _P]),
+    "ewb_long_range": (_INT, [_P, _P, _P, _I64, _P, _P, _P]),
+    "ewb_short_range": (_INT, [_P, _P, _P, _I64, _P, _P]),
+    "ewb_self_energy": (_INT, [_P, _P, _I64, _P]),
+    "ewb_evaluate": (_INT, [_P, _P, _P, _I64, _P, _P, _P, _P]),
+    "ewb_dev_load": (_INT, [_P, _P, _P, _I64]),
+    "ewb_dev_slot_doubles": (_I64, [_P]),
+    "ewb_dev_rho_partial": (_INT, [_P, _I64, _I64, _P]),
+    "ewb_dev_kspace_finalize": (_INT, [_P, _P, _P, _P]),
+    "ewb_dev_recip_forces": (_INT, [_P, _I64, _I64, _P]),
+    "ewb_dev_real_space": (_INT, [_P, _INT, _INT, _P, _P]),
+    "ewb_dev_self_energy": (_INT, [_P, _P]),
+    "ewb_dev_evaluate": (_INT, [_P, _P, _P, _I64, _P, _P, _P, _P]),
+    "ewb_launch_count": (_I64, [_P]),
+}
+
+_LIB = None
+
+
+def load_library():
+    """Load the CUDA library; raise ImportError (loudly) if it is absent."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} not found: the CUDA extension is not built "
+            f"(run __graft_entry__.build()); there is no CPU fallback")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _LIB = lib
+    return lib
+
+
+def _ptr(a):
+    return None if a is None else ctypes.c_void_p(a.ctypes.data)
+
+
+class DeviceError(RuntimeError):
+    """CUDA failure or misuse of the device library."""
+
+
+def raise_for(status, message, lib=None):
+    if status == EWB_OK:
+        return
+    if status == EWB_ECOINCIDENT:
+        raise CoincidentParticlesError(message)
+    if status == EWB_ECUTOFF:
+        raise CutoffTooLargeError(message)
+    if status == EWB_EKSPACE:
+        raise KSpaceEmptyError(message)
+    if status in (EWB_EINVAL, EWB_EUNWRAPPED):
+        raise ValueError(message)
+    raise DeviceError(f"libewaldb200 status {status}: {message}")
+
+
+def default_device():
+    return int(os.environ.get("EWALDB200_DEVICE",
+                              os.environ.get("LOCAL_RANK", "0")))
+
+
+def f64c(a, shape=None):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if shape is not None and a.shape != shape:
+        a = a.reshape(shape)
+    return a
+
+
+class Handle:
+    """One device context: box/parameters, k-space plan, device buffers."""
+
+    def __init__(self, device=None):
+        self.lib = load_library()
+        self.device = default_device() if device is None else int(device)
+        h = ctypes.c_void_p()
+        st = self.lib.ewb_create(self.device, ctypes.byref(h))
+        if st != EWB_OK:
+            raise DeviceError(
+                f"ewb_create(device={self.device}) failed with status {st}: "
+                f"no usable CUDA device (this package has no CPU path)")
+        self.h = h
+        self.system = None
+        self.kspace_key = None
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            try:
+                self.lib.ewb_destroy(h)
+            except Exception:
+                pass
+            self.h = None
+
+    def _check(self, st):
+        if st != EWB_OK:
+            msg = self.lib.ewb_last_error(self.h)
+            raise_for(st, msg.decode() if msg else "", self.lib)
+
+    # configuration -------------------------------------------------------
+    def set_system(self, L, alpha, r_cutoff):
+        key = (float(L), float(alpha), float(r_cutoff))
+        if key != self.system:
+            rc = float(r_cutoff)
+            self._check(self.lib.ewb_set_system(self.h, key[0], key[1], rc,
+                                                rc**2))
+            self.system = key
+
+    def set_kspace(self, m_int, coeff, key=None):
+        if key is not None and key == self.kspace_key:
+            return
+        m = np.ascontiguousarray(m_int, dtype=np.int64).reshape(-1, 3)
+        c = f64c(coeff)
+        if c.shape[0] != m.shape[0]:
+            raise ValueError("coeff and m_int lengths differ")
+        self._check(self.lib.ewb_set_kspace(self.h, _ptr(m), m.shape[0],
+                                            _ptr(c)))
+        self.kspace_key = key
+
+    def set_max_segment(self, mcap):
+        self._check(self.lib.ewb_set_max_segment(self.h, int(mcap)))
+        self.kspace_key = None
+
+    def kspace_info(self):
+        info = np.zeros(6, dtype=np.int64)
+        self._check(self.lib.ewb_kspace_info(self.h, _ptr(info)))
+        return dict(zip(("K", "n_items", "M", "n_rows", "n_tiles",
+                         "max_table"), info.tolist()))
+
+    def set_stream(self, stream_ptr):
+        self._check(self.lib.ewb_set_stream(self.h, int(stream_ptr)))
+
+    def launch_count(self):
+        return int(self.lib.ewb_launch_count(self.h))
+
+    # host-pointer entry points --------------------------------------------
+    def compute_rho_hat(self, pos, q, rho_out):
+        n = q.shape[0]
+        self._check(self.lib.ewb_compute_rho_hat(self.h, _ptr(pos), _ptr(q),
+                                                 n, _ptr(rho_out)))
+
+    def long_range(self, pos, q, rho, force):
+        u = ctypes.c_double(0.0)
+        self._check(self.lib.ewb_long_range(self.h, _ptr(pos), _ptr(q),
+                                            q.shape[0], _ptr(rho),
+                                            _ptr(force), ctypes.byref(u)))
+        return u.value
+
+    def short_range(self, pos, q, force):
+        u = ctypes.c_double(0.0)
+        self._check(self.lib.ewb_short_range(self.h, _ptr(pos), _ptr(q),
+                                             q.shape[0], _ptr(force),
+                                             ctypes.byref(u)))
+        return u.value
+
+    def self_energy(self, q):
+        u = ctypes.c_double(0.0)
+        self._check(self.lib.ewb_self_energy(self.h, _ptr(q), q.shape[0],
+                                             ctypes.byref(u)))
+        return u.value
+
+    def evaluate(self, pos, q, force, rho_out=None):
+        en = np.zeros(3)
+        tm = np.zeros(4)
+        self._check(self.lib.ewb_evaluate(self.h, _ptr(pos), _ptr(q),
+                                          q.shape[0], _ptr(force),
+                                          _ptr(rho_out), _ptr(en), _ptr(tm)))
+        return en, tm
+
+    # device-pointer stages (integers are raw device addresses) -------------
+    def dev_load(self, d_pos, d_q, n):
+        self._check(self.lib.ewb_dev_load(self.h, d_pos, d_q, int(n)))
+
+    def dev_slot_doubles(self):
+        return int(self.lib.ewb_dev_slot_doubles(self.h))
+
+    def dev_rho_partial(self, i0, i1, d_slots):
+        self._check(self.lib.ewb_dev_rho_partial(self.h, int(i0), int(i1),
+                                                 d_slots))
+
+    def dev_kspace_finalize(self, d_slots, d_rho_out=None):
+        u = ctypes.c_double(0.0)
+        self._check(self.lib.ewb_dev_kspace_finalize(
+            self.h, d_slots, d_rho_out, ctypes.byref(u)))
+        return u.value
+
+    def dev_recip_forces(self, i0, i1, d_force):
+        self._check(self.lib.ewb_dev_recip_forces(self.h, int(i0), int(i1),
+                                                  d_force))
+
+    def dev_real_space(self, part, nparts, d_force):
+        u = ctypes.c_double(0.0)
+        self._check(self.lib.ewb_dev_real_space(self.h, int(part),
+                                                int(nparts), d_force,
+                                                ctypes.byref(u)))
+        return u.value
+
+    def dev_self_energy(self):
+        u = ctypes.c_double(0.0)
+        self._check(self.lib.ewb_dev_self_energy(self.h, ctypes.byref(u)))
+        return u.value
+
+    def dev_evaluate(self, d_pos, d_q, n, d_force, d_rho_out=None,
+                     timings=True):
+        en = np.zeros(3)
+        tm = np.zeros(4)
+        self._check(self.lib.ewb_dev_evaluate(
+            self.h, d_pos, d_q, int(n), d_force, d_rho_out, _ptr(en),
+            _ptr(tm) if timings else None))
+        return en, tm

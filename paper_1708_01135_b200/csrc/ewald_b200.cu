@@ -1,0 +1,1689 @@
+// ewald_b200.cu -- B200-native (sm_100a) classical Ewald energy + forces.
+//
+// Hot path of arXiv 1708.01135 as restated by the reference package ewaldmd
+// (/root/reference/pkg/src/ewaldmd).  See include/ewald_b200.h for the C-ABI
+// and DESIGN.md for the data layout and rooflines.  Kernels:
+//
+//   k_prep            fractional coordinates t = r/L, per-axis base phases
+//                     e^{-i 2 pi t}, wrap check                (O(N), HBM)
+//   k1_structure_factor  Alg. 1 (ewald.py:281-305): S(k) = sum_j q_j e^{-ik.r_j}
+//                     thread = one k-column segment (registers hold M
+//                     accumulators), particles streamed through shared-memory
+//                     phase tables; phases along m_z by the three-term
+//                     recurrence A_{m+1} = 2cos(theta_z) A_m - A_{m-1}
+//                     (4 FP64 instructions per particle.k pair)
+//   k2_finalize       reduce particle-chunk partials, scatter rho_hat to the
+//                     caller's k order, C_k*S_k for the gather, u_lr=sum C|S|^2
+//   k3_force_gather   Alg. 2 (ewald.py:308-349): thread = particle, k-slots
+//                     broadcast from shared memory; F_i = q_i 4pi/L sum_k m_k
+//                     Im(e^{ik.r_i} C_k S_k) with the m_z weight folded into a
+//                     running-sum identity (5 FP64 instructions per pair)
+//   k4/k5*            counting-sort binning into reference-sized cells
+//                     (celllist.py:75-108), deterministic in-cell order
+//   k6_real_space     ordered-pair erfc loop (ewald.py:208-221,
+//                     engine.py:102-159) with per-lane compaction queues so
+//                     erfc/exp run warp-converged; cutoff predicate
+//                     bit-identical to the reference (no FMA contraction)
+//   k7_sum_q2         self energy (ewald.py:482-484)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "ewald_b200.h"
+
+#define EWB_VERSION 100
+
+namespace {
+
+constexpr int ERR_UNWRAPPED = 1;
+constexpr int ERR_COINCIDENT = 2;
+
+constexpr int MAXM = 32;          // longest k-column segment (template range)
+constexpr int K1_THREADS = 128;   // k-items per structure-factor block
+constexpr int K1_PMAX = 32;       // particles per shared-memory phase chunk
+constexpr int TAB_SEG = 8;        // phase-table entries per build task
+constexpr int K3_THREADS = 128;
+constexpr int K3_PPT = 2;         // particles per thread in the gather
+constexpr int K3_CH = 32;         // k-items per shared-memory chunk
+constexpr int K6_WARPS = 4;
+constexpr int QCAP = 64;          // per-lane pair queue (power of two)
+constexpr int SORT_CAP = 4096;    // in-cell deterministic sort capacity
+constexpr int RED_THREADS = 256;
+
+// tab_desc flags
+constexpr int TF_QSCALE = 1;
+constexpr int TF_LINK = 2;
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic block reduction; result valid in thread 0.
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double *sh) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NT / 32; ++i) r += sh[i];
+  }
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// k_prep: per-particle derived data, O(N)
+__global__ void k_prep(const double *__restrict__ pos, const double *__restrict__ q, int64_t n,
+                       double L, double4 *__restrict__ frac, double2 *__restrict__ base,
+                       double4 *__restrict__ xyzq, int *__restrict__ err) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double x = pos[3 * i], y = pos[3 * i + 1], z = pos[3 * i + 2], qi = q[i];
+  if (!(x >= 0.0 && x < L && y >= 0.0 && y < L && z >= 0.0 && z < L)) atomicOr(err, ERR_UNWRAPPED);
+  const double tx = x / L, ty = y / L, tz = z / L;
+  frac[i] = make_double4(tx, ty, tz, qi);
+  xyzq[i] = make_double4(x, y, z, qi);
+  double s, c;
+  sincospi(2.0 * tx, &s, &c);
+  base[3 * i] = make_double2(c, -s);
+  sincospi(2.0 * ty, &s, &c);
+  base[3 * i + 1] = make_double2(c, -s);
+  sincospi(2.0 * tz, &s, &c);
+  base[3 * i + 2] = make_double2(c, -s);
+}
+
+// ---------------------------------------------------------------------------
+// K1: structure factor.  Block = (k-tile of K1_THREADS items, particle chunk).
+template <int M>
+__global__ void __launch_bounds__(K1_THREADS)
+    k1_structure_factor(const double4 *__restrict__ frac, const double2 *__restrict__ base,
+                        int64_t p_begin, int64_t p_end, int64_t ppb, int pchunk,
+                        const int2 *__restrict__ item_tab, int n_items,
+                        const int4 *__restrict__ tab_desc, const int *__restrict__ tile_off,
+                        const int *__restrict__ tile_ts, double2 *__restrict__ spart) {
+  extern __shared__ double2 tab[];
+  const int tile = blockIdx.x;
+  const int item = tile * K1_THREADS + threadIdx.x;
+  const bool valid = item < n_items;
+  const int2 it = item_tab[valid ? item : n_items - 1];
+  const int TS = tile_ts[tile];
+  const int4 *desc = tab_desc + tile_off[tile];
+  const int eidx = TS - 1;
+
+  double2 acc[M];
+#pragma unroll
+  for (int m = 0; m < M; ++m) acc[m] = make_double2(0.0, 0.0);
+
+  const int64_t c_begin = p_begin + (int64_t)blockIdx.y * ppb;
+  const int64_t c_end = min(p_end, c_begin + ppb);
+  const int ntask_p = (TS + TAB_SEG - 1) / TAB_SEG;
+
+  for (int64_t c0 = c_begin; c0 < c_end; c0 += pchunk) {
+    const int np = (int)min((int64_t)pchunk, c_end - c0);
+    __syncthreads();
+    // build the per-particle phase tables of this tile: rows
+    // q e^{-i(mx th_x + s th_z)}, columns e^{-i my th_y}, and e^{-i th_z}
+    for (int task = threadIdx.x; task < np * ntask_p; task += K1_THREADS) {
+      const int p = task / ntask_p;
+      const int e0 = (task - p * ntask_p) * TAB_SEG;
+      const int e1 = min(TS, e0 + TAB_SEG);
+      const double4 f = frac[c0 + p];
+      double2 prev = make_double2(1.0, 0.0);
+      for (int e = e0; e < e1; ++e) {
+        const int4 d = __ldg(desc + e);
+        double2 v;
+        if (e == e0 || !(d.w & TF_LINK)) {
+          const double arg = (double)d.x * f.x + (double)d.y * f.y + (double)d.z * f.z;
+          double sn, cs;
+          sincospi(2.0 * arg, &sn, &cs);
+          v = make_double2(cs, -sn);
+          if (d.w & TF_QSCALE) {
+            v.x *= f.w;
+            v.y *= f.w;
+          }
+        } else {
+          v = cmul(prev, base[3 * (c0 + p) + ((d.w >> 2) & 3)]);
+        }
+        tab[p * TS + e] = v;
+        prev = v;
+      }
+    }
+    __syncthreads();
+    int p = 0;
+    for (; p + 1 < np; p += 2) {
+      const double2 *t0 = tab + p * TS;
+      const double2 *t1 = t0 + TS;
+      const double2 e0 = t0[eidx], e1 = t1[eidx];
+      const double2 b0 = cmul(t0[it.x], t0[it.y]);
+      const double2 d0 = cmul(t1[it.x], t1[it.y]);
+      const double c0z = e0.x + e0.x, c1z = e1.x + e1.x;
+      acc[0].x += b0.x + d0.x;
+      acc[0].y += b0.y + d0.y;
+      if (M > 1) {
+        double2 bp = b0, dp = d0;
+        double2 bc = cmul(b0, e0), dc = cmul(d0, e1);
+        acc[1].x += bc.x + dc.x;
+        acc[1].y += bc.y + dc.y;
+#pragma unroll
+        for (int m = 2; m < M; ++m) {
+          const double2 bn = make_double2(fma(c0z, bc.x, -bp.x), fma(c0z, bc.y, -bp.y));
+          const double2 dn = make_double2(fma(c1z, dc.x, -dp.x), fma(c1z, dc.y, -dp.y));
+          acc[m].x += bn.x + dn.x;
+          acc[m].y += bn.y + dn.y;
+          bp = bc;
+          bc = bn;
+          dp = dc;
+          dc = dn;
+        }
+      }
+    }
+    if (p < np) {
+      const double2 *t0 = tab + p * TS;
+      const double2 e0 = t0[eidx];
+      const double2 b0 = cmul(t0[it.x], t0[it.y]);
+      const double c0z = e0.x + e0.x;
+      acc[0].x += b0.x;
+      acc[0].y += b0.y;
+      if (M > 1) {
+        double2 bp = b0, bc = cmul(b0, e0);
+        acc[1].x += bc.x;
+        acc[1].y += bc.y;
+#pragma unroll
+        for (int m = 2; m < M; ++m) {
+          const double2 bn = make_double2(fma(c0z, bc.x, -bp.x), fma(c0z, bc.y, -bp.y));
+          acc[m].x += bn.x;
+          acc[m].y += bn.y;
+          bp = bc;
+          bc = bn;
+        }
+      }
+    }
+  }
+  if (valid) {
+    double2 *out = spart + (size_t)blockIdx.y * M * n_items + item;
+#pragma unroll
+    for (int m = 0; m < M; ++m) out[(size_t)m * n_items] = acc[m];
+  }
+}
+
+// K2: reduce particle-chunk partials; optionally finalize (rho scatter,
+// C*S for the gather, energy partials).
+__global__ void __launch_bounds__(RED_THREADS)
+    k2_finalize(const double2 *__restrict__ spart, int n_part, int64_t n_slots,
+                const int *__restrict__ slot_k, const double *__restrict__ slot_coeff, int64_t K,
+                double *__restrict__ rho_out, double2 *__restrict__ s_out,
+                double2 *__restrict__ sp, double *__restrict__ epart, int finalize) {
+  __shared__ double sh[RED_THREADS / 32];
+  const int64_t s = blockIdx.x * (int64_t)RED_THREADS + threadIdx.x;
+  double e = 0.0;
+  if (s < n_slots) {
+    double2 S = make_double2(0.0, 0.0);
+    for (int pc = 0; pc < n_part; ++pc) {
+      const double2 v = spart[(size_t)pc * n_slots + s];
+      S.x += v.x;
+      S.y += v.y;
+    }
+    if (s_out) s_out[s] = S;
+    if (finalize) {
+      const int k = slot_k[s];
+      if (k >= 0) {
+        if (rho_out) {
+          rho_out[k] = S.x;
+          rho_out[K + k] = S.y;
+        }
+        const double C = slot_coeff[s];
+        sp[s] = make_double2(C * S.x, C * S.y);
+        e = C * (S.x * S.x + S.y * S.y);
+      } else {
+        sp[s] = make_double2(0.0, 0.0);
+      }
+    }
+  }
+  if (finalize) {
+    const double b = block_sum<RED_THREADS>(e, sh);
+    if (threadIdx.x == 0) epart[blockIdx.x] = b;
+  }
+}
+
+// Deterministic single-block sum of an array into out[0].
+__global__ void __launch_bounds__(1024) k_sum(const double *__restrict__ v, int64_t n,
+                                               double scale, double *__restrict__ out) {
+  __shared__ double sh[32];
+  double a = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += 1024) a += v[i];
+  const double r = block_sum<1024>(a, sh);
+  if (threadIdx.x == 0) *out = scale * r;
+}
+
+// ---------------------------------------------------------------------------
+// K3: reciprocal force gather.  Block = (K3_THREADS*K3_PPT particles, k-split).
+__device__ __forceinline__ double2 phase_plus(int mx, int my, int s, double tx, double ty,
+                                              double tz) {
+  const double arg = (double)mx * tx + (double)my * ty + (double)s * tz;
+  double sn, cs;
+  sincospi(2.0 * arg, &sn, &cs);
+  return make_double2(cs, sn);
+}
+
+template <int M, bool ENERGY>
+__global__ void __launch_bounds__(K3_THREADS)
+    k3_force_gather(const double4 *__restrict__ frac, const double2 *__restrict__ base,
+                    int64_t p_begin, int64_t p_end, const int4 *__restrict__ rows,
+                    const int *__restrict__ ks_rows, const int *__restrict__ item_my,
+                    const int *__restrict__ item_row, const double2 *__restrict__ sp, int n_items,
+                    double *__restrict__ fpart, double *__restrict__ upart) {
+  __shared__ double2 s_sp[K3_CH * M];
+  __shared__ int s_my[K3_CH];
+  __shared__ int s_row[K3_CH];
+  const int64_t n_local = p_end - p_begin;
+  const int ks = blockIdx.y;
+  const int r_begin = ks_rows[ks], r_end = ks_rows[ks + 1];
+
+  int64_t pi[K3_PPT];
+  double tx[K3_PPT], ty[K3_PPT], tz[K3_PPT], c2z[K3_PPT];
+  double2 ey[K3_PPT], ez[K3_PPT], P[K3_PPT];
+  double Fx[K3_PPT], Fy[K3_PPT], Fz[K3_PPT], U[K3_PPT], SG[K3_PPT], SY[K3_PPT], SH[K3_PPT];
+#pragma unroll
+  for (int q = 0; q < K3_PPT; ++q) {
+    pi[q] = (int64_t)blockIdx.x * (K3_THREADS * K3_PPT) + q * K3_THREADS + threadIdx.x;
+    const int64_t g = p_begin + (pi[q] < n_local ? pi[q] : 0);
+    const double4 f = frac[g];
+    tx[q] = f.x;
+    ty[q] = f.y;
+    tz[q] = f.z;
+    const double2 by = base[3 * g + 1], bz = base[3 * g + 2];
+    ey[q] = make_double2(by.x, -by.y);
+    ez[q] = make_double2(bz.x, -bz.y);
+    c2z[q] = bz.x + bz.x;
+    Fx[q] = Fy[q] = Fz[q] = U[q] = SG[q] = SY[q] = SH[q] = 0.0;
+    P[q] = make_double2(1.0, 0.0);
+  }
+
+  int cur_row = -1, pmy = 0, cmx = 0, cs = 0;
+  if (r_begin < r_end) {
+    const int i_first = rows[r_begin].z;
+    const int4 rl = rows[r_end - 1];
+    const int i_last = rl.z + rl.w;
+    for (int c0 = i_first; c0 < i_last; c0 += K3_CH) {
+      const int nc = min(K3_CH, i_last - c0);
+      __syncthreads();
+      for (int t = threadIdx.x; t < nc * M; t += K3_THREADS) {
+        const int m = t / nc, itc = t - m * nc;
+        s_sp[itc * M + m] = sp[(size_t)m * n_items + c0 + itc];
+      }
+      for (int t = threadIdx.x; t < nc; t += K3_THREADS) {
+        s_my[t] = item_my[c0 + t];
+        s_row[t] = item_row[c0 + t];
+      }
+      __syncthreads();
+      for (int itc = 0; itc < nc; ++itc) {
+        const int row = s_row[itc], my = s_my[itc];
+        if (row != cur_row) {
+          if (cur_row >= 0) {
+#pragma unroll
+            for (int q = 0; q < K3_PPT; ++q) {
+              Fx[q] = fma((double)cmx, SG[q], Fx[q]);
+              Fy[q] += SY[q];
+              Fz[q] += fma((double)(cs + M), SG[q], -SH[q]);
+              SG[q] = SY[q] = SH[q] = 0.0;
+            }
+          }
+          const int4 r = rows[row];
+          cmx = r.x;
+          cs = r.y;
+          cur_row = row;
+#pragma unroll
+          for (int q = 0; q < K3_PPT; ++q) P[q] = phase_plus(cmx, my, cs, tx[q], ty[q], tz[q]);
+        } else if (my != pmy + 1) {
+#pragma unroll
+          for (int q = 0; q < K3_PPT; ++q) P[q] = phase_plus(cmx, my, cs, tx[q], ty[q], tz[q]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < K3_PPT; ++q) P[q] = cmul(P[q], ey[q]);
+        }
+        pmy = my;
+        const double2 *spi = s_sp + itc * M;
+        double2 Ap[K3_PPT], Ac[K3_PPT];
+        double G[K3_PPT], H[K3_PPT];
+        {
+          const double2 s0 = spi[0];
+#pragma unroll
+          for (int q = 0; q < K3_PPT; ++q) {
+            Ap[q] = P[q];
+            G[q] = fma(Ap[q].x, s0.y, Ap[q].y * s0.x);
+            H[q] = G[q];
+            if (ENERGY) U[q] = fma(Ap[q].x, s0.x, fma(-Ap[q].y, s0.y, U[q]));
+          }
+        }
+        if (M > 1) {
+          const double2 s1 = spi[1];
+#pragma unroll
+          for (int q = 0; q < K3_PPT; ++q) {
+            Ac[q] = cmul(P[q], ez[q]);
+            G[q] = fma(Ac[q].x, s1.y, fma(Ac[q].y, s1.x, G[q]));
+            H[q] += G[q];
+            if (ENERGY) U[q] = fma(Ac[q].x, s1.x, fma(-Ac[q].y, s1.y, U[q]));
+          }
+#pragma unroll
+          for (int m = 2; m < M; ++m) {
+            const double2 sm = spi[m];
+#pragma unroll
+            for (int q = 0; q < K3_PPT; ++q) {
+              const double2 An = make_double2(fma(c2z[q], Ac[q].x, -Ap[q].x),
+                                              fma(c2z[q], Ac[q].y, -Ap[q].y));
+              Ap[q] = Ac[q];
+              Ac[q] = An;
+              G[q] = fma(An.x, sm.y, fma(An.y, sm.x, G[q]));
+              H[q] += G[q];
+              if (ENERGY) U[q] = fma(An.x, sm.x, fma(-An.y, sm.y, U[q]));
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < K3_PPT; ++q) {
+          SG[q] += G[q];
+          SY[q] = fma((double)my, G[q], SY[q]);
+          SH[q] += H[q];
+        }
+      }
+    }
+    if (cur_row >= 0) {
+#pragma unroll
+      for (int q = 0; q < K3_PPT; ++q) {
+        Fx[q] = fma((double)cmx, SG[q], Fx[q]);
+        Fy[q] += SY[q];
+        Fz[q] += fma((double)(cs + M), SG[q], -SH[q]);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < K3_PPT; ++q) {
+    if (pi[q] < n_local) {
+      double *fp = fpart + (size_t)ks * 3 * n_local;
+      fp[pi[q]] = Fx[q];
+      fp[n_local + pi[q]] = Fy[q];
+      fp[2 * n_local + pi[q]] = Fz[q];
+      if (ENERGY) upart[(size_t)ks * n_local + pi[q]] = U[q];
+    }
+  }
+}
+
+// Combine k-split partial forces: force[i] += (4 pi / L) q_i sum_ks F.
+__global__ void __launch_bounds__(RED_THREADS)
+    k3_combine(const double *__restrict__ fpart, const double *__restrict__ upart, int n_ks,
+               int64_t p_begin, int64_t n_local, const double4 *__restrict__ frac, double scale,
+               double *__restrict__ force, double *__restrict__ eblk, int energy) {
+  __shared__ double sh[RED_THREADS / 32];
+  const int64_t i = blockIdx.x * (int64_t)RED_THREADS + threadIdx.x;
+  double e = 0.0;
+  if (i < n_local) {
+    double fx = 0.0, fy = 0.0, fz = 0.0, u = 0.0;
+    for (int ks = 0; ks < n_ks; ++ks) {
+      const double *fp = fpart + (size_t)ks * 3 * n_local;
+      fx += fp[i];
+      fy += fp[n_local + i];
+      fz += fp[2 * n_local + i];
+      if (energy) u += upart[(size_t)ks * n_local + i];
+    }
+    const int64_t g = p_begin + i;
+    const double qi = frac[g].w;
+    const double sq = scale * qi;
+    force[3 * g] += sq * fx;
+    force[3 * g + 1] += sq * fy;
+    force[3 * g + 2] += sq * fz;
+    e = qi * u;
+  }
+  if (energy) {
+    const double b = block_sum<RED_THREADS>(e, sh);
+    if (threadIdx.x == 0) eblk[blockIdx.x] = b;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Real space: counting-sort binning (celllist.py:75-108)
+__global__ void k4_bin_count(const double4 *__restrict__ xyzq, int64_t n, double edge, int cpd,
+                             int *__restrict__ cell_of, int *__restrict__ slot,
+                             int *__restrict__ count) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double4 p = xyzq[i];
+  int c = 0;
+  if (cpd > 1) {
+    const double v[3] = {p.x, p.y, p.z};
+    int id[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double f = floor(v[a] / edge);
+      int k = (f >= 0.0) ? (f < (double)cpd ? (int)f : cpd - 1) : 0;  // NaN -> 0
+      id[a] = k;
+    }
+    c = id[0] + cpd * (id[1] + cpd * id[2]);
+  }
+  cell_of[i] = c;
+  slot[i] = atomicAdd(count + c, 1);
+}
+
+// Single-block exclusive scans of cell counts (start) and 32-groups (gstart).
+__global__ void __launch_bounds__(1024) k_scan_cells(const int *__restrict__ count, int n_cells,
+                                                     int *__restrict__ start,
+                                                     int *__restrict__ gstart) {
+  __shared__ int wa[32], wb[32];
+  __shared__ int carry_a, carry_b;
+  if (threadIdx.x == 0) carry_a = carry_b = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int base = 0; base < n_cells; base += 1024) {
+    const int c = base + threadIdx.x;
+    const int a = c < n_cells ? count[c] : 0;
+    const int b = (a + 31) >> 5;
+    int ia = a, ib = b;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int ta = __shfl_up_sync(0xffffffffu, ia, o);
+      const int tb = __shfl_up_sync(0xffffffffu, ib, o);
+      if (lane >= o) {
+        ia += ta;
+        ib += tb;
+      }
+    }
+    if (lane == 31) {
+      wa[w] = ia;
+      wb[w] = ib;
+    }
+    __syncthreads();
+    if (w == 0) {
+      int xa = wa[lane], xb = wb[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int ta = __shfl_up_sync(0xffffffffu, xa, o);
+        const int tb = __shfl_up_sync(0xffffffffu, xb, o);
+        if (lane >= o) {
+          xa += ta;
+          xb += tb;
+        }
+      }
+      wa[lane] = xa;
+      wb[lane] = xb;
+    }
+    __syncthreads();
+    const int pa = (w ? wa[w - 1] : 0) + ia - a + carry_a;
+    const int pb = (w ? wb[w - 1] : 0) + ib - b + carry_b;
+    if (c < n_cells) {
+      start[c] = pa;
+      gstart[c] = pb;
+    }
+    __syncthreads();
+    if (threadIdx.x == 1023) {
+      carry_a = pa + a;
+      carry_b = pb + b;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    start[n_cells] = carry_a;
+    gstart[n_cells] = carry_b;
+  }
+}
+
+__global__ void k5_scatter(const int *__restrict__ cell_of, const int *__restrict__ slot, int64_t n,
+                           const int *__restrict__ start, int *__restrict__ order_tmp) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  order_tmp[start[cell_of[i]] + slot[i]] = (int)i;
+}
+
+// Restore a deterministic (ascending original index = stable) order in cells.
+__global__ void __launch_bounds__(256) k5_cell_sort(const int *__restrict__ start,
+                                                    const int *__restrict__ order_tmp,
+                                                    int *__restrict__ order) {
+  __shared__ int mem[SORT_CAP];
+  const int c = blockIdx.x;
+  const int s = start[c], e = start[c + 1], cnt = e - s;
+  if (cnt > SORT_CAP) {
+    for (int t = threadIdx.x; t < cnt; t += 256) order[s + t] = order_tmp[s + t];
+    return;
+  }
+  for (int t = threadIdx.x; t < cnt; t += 256) mem[t] = order_tmp[s + t];
+  __syncthreads();
+  for (int t = threadIdx.x; t < cnt; t += 256) {
+    const int v = mem[t];
+    int r = 0;
+    for (int u = 0; u < cnt; ++u) r += mem[u] < v;
+    order[s + r] = v;
+  }
+}
+
+__global__ void k_iota(int *__restrict__ v, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) v[i] = (int)i;
+}
+
+__global__ void k5_gather(const int *__restrict__ order, const double4 *__restrict__ xyzq,
+                          int64_t n, double4 *__restrict__ sorted) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  sorted[p] = xyzq[order[p]];
+}
+
+// K6: ordered-pair real-space kernel.  One warp = up to 32 centre particles of
+// one home cell (lanes), candidates broadcast from shared memory; accepted
+// pairs go to a per-lane queue and are evaluated in converged rounds.
+struct RSParams {
+  double L, hl, rc2, sa, al, tsap;
+  int cpd, fold;
+  int c_lo, c_hi;
+  int64_t n;
+};
+
+__device__ __forceinline__ void rs_shift(int c, int s, int cpd, double L, double &sx, double &sy,
+                                         double &sz, int &nc) {
+  const int cx = c % cpd, cy = (c / cpd) % cpd, cz = c / (cpd * cpd);
+  int nx = cx + (s % 3) - 1, ny = cy + (s / 3) % 3 - 1, nz = cz + s / 9 - 1;
+  sx = sy = sz = 0.0;
+  if (nx < 0) {
+    nx += cpd;
+    sx = L;
+  } else if (nx >= cpd) {
+    nx -= cpd;
+    sx = -L;
+  }
+  if (ny < 0) {
+    ny += cpd;
+    sy = L;
+  } else if (ny >= cpd) {
+    ny -= cpd;
+    sy = -L;
+  }
+  if (nz < 0) {
+    nz += cpd;
+    sz = L;
+  } else if (nz >= cpd) {
+    nz -= cpd;
+    sz = -L;
+  }
+  nc = nx + cpd * (ny + cpd * nz);
+}
+
+// dx exactly as the reference: fl(xi - xj) then one fold by +-L
+// (engine.py:117-131); with a stencil the fold is the cell-pair shift, which
+// equals the reference's fold for every pair inside the cutoff.
+template <bool FOLD>
+__device__ __forceinline__ double rs_disp(double xi, double xj, double shift, double hl, double L) {
+  double d = __dsub_rn(xi, xj);
+  if (FOLD) {
+    if (d >= hl)
+      d = __dsub_rn(d, L);
+    else if (d < -hl)
+      d = __dadd_rn(d, L);
+  } else {
+    d = __dadd_rn(d, shift);
+  }
+  return d;
+}
+
+__device__ __forceinline__ double rs_r2(double dx, double dy, double dz) {
+  return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+}
+
+template <bool FOLD>
+__global__ void __launch_bounds__(K6_WARPS * 32)
+    k6_real_space(const double4 *__restrict__ sorted, const int *__restrict__ order,
+                  const int *__restrict__ cell_start, const int *__restrict__ gstart, RSParams P,
+                  double *__restrict__ force, double *__restrict__ eblk, int *__restrict__ err) {
+  __shared__ uint32_t qbuf[K6_WARPS][QCAP][32];
+  __shared__ double4 stage[K6_WARPS][32];
+  __shared__ double sh[K6_WARPS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int u_lo = gstart[P.c_lo], u_hi = gstart[P.c_hi];
+  const int u = u_lo + blockIdx.x * K6_WARPS + warp;
+  double ue = 0.0;
+  if (u < u_hi) {
+    int lo = P.c_lo, hi = P.c_hi - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (gstart[mid] <= u)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    const int c = lo;
+    const int cs = cell_start[c], ce = cell_start[c + 1];
+    const int i = cs + 32 * (u - gstart[c]) + lane;
+    const bool valid = i < ce;
+    const double4 pi = sorted[valid ? i : cs];
+    double fx = 0.0, fy = 0.0, fz = 0.0;
+    int head = 0, tail = 0;
+    bool coincident = false;
+
+    auto eval_one = [&]() {
+      const uint32_t code = qbuf[warp][head & (QCAP - 1)][lane];
+      ++head;
+      const int j = (int)(code & 0x7FFFFFFu);
+      const int s = (int)(code >> 27);
+      const double4 pj = sorted[j];
+      double sx = 0.0, sy = 0.0, sz = 0.0;
+      if (!FOLD) {
+        int nc;
+        rs_shift(c, s, P.cpd, P.L, sx, sy, sz, nc);
+      }
+      const double dx = rs_disp<FOLD>(pi.x, pj.x, sx, P.hl, P.L);
+      const double dy = rs_disp<FOLD>(pi.y, pj.y, sy, P.hl, P.L);
+      const double dz = rs_disp<FOLD>(pi.z, pj.z, sz, P.hl, P.L);
+      const double r2 = rs_r2(dx, dy, dz);
+      if (r2 == 0.0) {
+        coincident = true;
+        return;
+      }
+      const double qq = pi.w * pj.w;
+      const double r = sqrt(r2);
+      const double sc = erfc(P.sa * r) / r;
+      ue += 0.5 * qq * sc;
+      const double g = qq * (sc + P.tsap * exp(-P.al * r2)) / r2;
+      fx = fma(g, dx, fx);
+      fy = fma(g, dy, fy);
+      fz = fma(g, dz, fz);
+    };
+
+    const int nst = FOLD ? 1 : 27;
+    for (int s = 0; s < nst; ++s) {
+      int jb, je;
+      double sx = 0.0, sy = 0.0, sz = 0.0;
+      if (FOLD) {
+        jb = 0;
+        je = (int)P.n;
+      } else {
+        int nc;
+        rs_shift(c, s, P.cpd, P.L, sx, sy, sz, nc);
+        jb = cell_start[nc];
+        je = cell_start[nc + 1];
+      }
+      for (int j0 = jb; j0 < je; j0 += 32) {
+        const int nb = min(32, je - j0);
+        __syncwarp();
+        if (lane < nb) stage[warp][lane] = sorted[j0 + lane];
+        __syncwarp();
+        for (int t = 0; t < nb; ++t) {
+          const double4 pj = stage[warp][t];
+          const double dx = rs_disp<FOLD>(pi.x, pj.x, sx, P.hl, P.L);
+          const double dy = rs_disp<FOLD>(pi.y, pj.y, sy, P.hl, P.L);
+          const double dz = rs_disp<FOLD>(pi.z, pj.z, sz, P.hl, P.L);
+          const double r2 = rs_r2(dx, dy, dz);
+          const int j = j0 + t;
+          if (valid && r2 < P.rc2 && j != i) {
+            qbuf[warp][tail & (QCAP - 1)][lane] = (uint32_t)j | ((uint32_t)s << 27);
+            ++tail;
+          }
+        }
+        while (__all_sync(0xffffffffu, !valid || tail - head > 0)) eval_one();
+        while (__any_sync(0xffffffffu, tail - head > QCAP - 32)) {
+          if (tail - head > 0) eval_one();
+        }
+      }
+    }
+    while (__any_sync(0xffffffffu, tail > head)) {
+      if (tail > head) eval_one();
+    }
+    if (coincident) atomicOr(err, ERR_COINCIDENT);
+    if (valid) {
+      const int o = order[i];
+      force[3 * (int64_t)o] += fx;
+      force[3 * (int64_t)o + 1] += fy;
+      force[3 * (int64_t)o + 2] += fz;
+    }
+  }
+  ue = warp_sum(ue);
+  if (lane == 0) sh[warp] = ue;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int w = 0; w < K6_WARPS; ++w) b += sh[w];
+    eblk[blockIdx.x] = b;
+  }
+}
+
+// K7: sum q^2 (self energy) partials.
+__global__ void __launch_bounds__(RED_THREADS) k7_sum_q2(const double4 *__restrict__ frac, int64_t n,
+                                                         double *__restrict__ eblk) {
+  __shared__ double sh[RED_THREADS / 32];
+  double a = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)RED_THREADS + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * RED_THREADS) {
+    const double q = frac[i].w;
+    a = fma(q, q, a);
+  }
+  const double b = block_sum<RED_THREADS>(a, sh);
+  if (threadIdx.x == 0) eblk[blockIdx.x] = b;
+}
+
+// ---------------------------------------------------------------------------
+// template dispatch tables
+#define EWB_M_CASES(X)                                                                           \
+  X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) X(17) \
+      X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30) X(31) X(32)
+
+typedef void (*k1_fn)(const double4 *, const double2 *, int64_t, int64_t, int64_t, int,
+                      const int2 *, int, const int4 *, const int *, const int *, double2 *);
+typedef void (*k3_fn)(const double4 *, const double2 *, int64_t, int64_t, const int4 *,
+                      const int *, const int *, const int *, const double2 *, int, double *,
+                      double *);
+
+k1_fn k1_table(int M) {
+  switch (M) {
+#define X(m) \
+  case m:    \
+    return k1_structure_factor<m>;
+    EWB_M_CASES(X)
+#undef X
+  }
+  return nullptr;
+}
+
+k3_fn k3_table(int M, bool energy) {
+  switch (M) {
+#define X(m) \
+  case m:    \
+    return energy ? k3_force_gather<m, true> : k3_force_gather<m, false>;
+    EWB_M_CASES(X)
+#undef X
+  }
+  return nullptr;
+}
+
+// ---------------------------------------------------------------------------
+// host side
+struct DBuf {
+  void *p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaSuccess) cap = bytes;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  template <class T>
+  T *as() const {
+    return reinterpret_cast<T *>(p);
+  }
+};
+
+struct Plan {
+  int64_t K = 0;
+  int M = 0, n_items = 0, n_rows = 0, n_tiles = 0, ts_max = 0, pchunk = K1_PMAX;
+  std::vector<int> row_item_prefix;  // n_rows+1
+  DBuf item_tab, item_my, item_row, rows, tab_desc, tile_off, tile_ts, slot_k, slot_coeff;
+  DBuf ks_rows;
+  int ks_cached = -1;
+  void release() {
+    for (DBuf *b : {&item_tab, &item_my, &item_row, &rows, &tab_desc, &tile_off, &tile_ts,
+                    &slot_k, &slot_coeff, &ks_rows})
+      b->release();
+  }
+};
+
+}  // namespace
+
+struct ewb_handle {
+  int device = 0;
+  int n_sm = 148;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[6] = {};
+  std::string err;
+  int mcap = 28;
+  int64_t launches = 0;
+  // system
+  bool have_system = false;
+  double L = 0, alpha = 0, rc = 0, rc2 = 0;
+  // k-space
+  bool have_kspace = false;
+  Plan plan;
+  // particles
+  int64_t n = 0;
+  bool loaded = false;
+  DBuf pos, q, force, rho;                   // host-API staging (caller layout)
+  DBuf frac, base, xyzq;                     // derived
+  DBuf spart, sslot, sp, fpart, upart, eblk, eblk2, energy, errflag;
+  DBuf cell_of, slot, count, start, gstart, order_tmp, order, sorted;
+  int occ_k1[MAXM + 1] = {};
+  int occ_k3[MAXM + 1][2] = {};
+  bool k1_attr[MAXM + 1] = {};
+
+  int fail(int code, const std::string &msg) {
+    err = msg;
+    return code;
+  }
+};
+
+namespace {
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return h->fail(EWB_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));      \
+  } while (0)
+
+#define CKL()                                                                                 \
+  do {                                                                                        \
+    ++h->launches;                                                                            \
+    cudaError_t e_ = cudaGetLastError();                                                      \
+    if (e_ != cudaSuccess)                                                                    \
+      return h->fail(EWB_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e_));    \
+  } while (0)
+
+inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+// number of blocks along the split axis minimising ceil(tiles*s/slots)/s
+int best_split(int64_t tiles, int64_t slots, int max_split) {
+  int best = 1;
+  double best_cost = 1e300;
+  for (int s = 1; s <= max_split; ++s) {
+    const double waves = std::ceil((double)(tiles * s) / (double)slots);
+    const double cost = waves / s;
+    if (cost < best_cost * (1.0 - 1e-9)) {
+      best_cost = cost;
+      best = s;
+    }
+  }
+  return best;
+}
+
+template <class T>
+int upload(ewb_handle *h, DBuf &b, const std::vector<T> &v) {
+  CK(b.ensure(v.size() * sizeof(T)));
+  if (!v.empty()) CK(cudaMemcpy(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return EWB_OK;
+}
+
+// Host planning of the k-space work decomposition.
+int build_plan(ewb_handle *h, const int64_t *m, int64_t K, const double *coeff) {
+  Plan &P = h->plan;
+  if (K <= 0) return h->fail(EWB_EKSPACE, "empty reciprocal-space table");
+  for (int64_t i = 0; i < 3 * K; ++i)
+    if (m[i] > 1000000 || m[i] < -1000000)
+      return h->fail(EWB_EINVAL, "m_int entries must satisfy |m| <= 1e6");
+  std::vector<int64_t> idx(K);
+  std::iota(idx.begin(), idx.end(), 0);
+  std::sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) {
+    for (int c = 0; c < 3; ++c)
+      if (m[3 * a + c] != m[3 * b + c]) return m[3 * a + c] < m[3 * b + c];
+    return a < b;
+  });
+  struct Item {
+    int mx, my, s, len;
+    int64_t off;
+  };
+  std::vector<Item> items;
+  const int mcap = std::max(1, std::min(MAXM, h->mcap));
+  int64_t a = 0;
+  while (a < K) {
+    const int64_t i0 = idx[a];
+    int64_t b = a + 1;
+    while (b < K) {
+      const int64_t ib = idx[b], ip = idx[b - 1];
+      if (m[3 * ib] != m[3 * i0] || m[3 * ib + 1] != m[3 * i0 + 1] ||
+          m[3 * ib + 2] != m[3 * ip + 2] + 1)
+        break;
+      ++b;
+    }
+    const int64_t len = b - a;
+    const int64_t nseg = (len + mcap - 1) / mcap;
+    const int64_t base_len = len / nseg, rem = len % nseg;
+    int64_t off = a;
+    for (int64_t sg = 0; sg < nseg; ++sg) {
+      const int sl = (int)(base_len + (sg < rem ? 1 : 0));
+      items.push_back(Item{(int)m[3 * i0], (int)m[3 * i0 + 1], (int)m[3 * idx[off] + 2], sl, off});
+      off += sl;
+    }
+    a = b;
+  }
+  std::sort(items.begin(), items.end(), [](const Item &x, const Item &y) {
+    if (x.s != y.s) return x.s < y.s;
+    if (x.mx != y.mx) return x.mx < y.mx;
+    return x.my < y.my;
+  });
+  const int n_items = (int)items.size();
+  int M = 0;
+  for (auto &it : items) M = std::max(M, it.len);
+
+  // rows: maximal runs of equal (s, mx)
+  std::vector<int> item_row(n_items), item_my(n_items);
+  std::vector<int4> rows;
+  for (int i = 0; i < n_items; ++i) {
+    if (i == 0 || items[i].s != items[i - 1].s || items[i].mx != items[i - 1].mx)
+      rows.push_back(make_int4(items[i].mx, items[i].s, i, 0));
+    rows.back().w++;
+    item_row[i] = (int)rows.size() - 1;
+    item_my[i] = items[i].my;
+  }
+  const int n_rows = (int)rows.size();
+  P.row_item_prefix.assign(n_rows + 1, 0);
+  for (int r = 0; r < n_rows; ++r) P.row_item_prefix[r + 1] = P.row_item_prefix[r] + rows[r].w;
+
+  // slots (slot-major layout: slot = m * n_items + item)
+  const size_t n_slots = (size_t)M * n_items;
+  std::vector<int> slot_k(n_slots, -1);
+  std::vector<double> slot_coeff(n_slots, 0.0);
+  for (int i = 0; i < n_items; ++i)
+    for (int mm = 0; mm < items[i].len; ++mm) {
+      const int64_t k = idx[items[i].off + mm];
+      slot_k[(size_t)mm * n_items + i] = (int)k;
+      slot_coeff[(size_t)mm * n_items + i] = coeff ? coeff[k] : 0.0;
+    }
+
+  // K1 tiles and their phase-table descriptors
+  const int n_tiles = (n_items + K1_THREADS - 1) / K1_THREADS;
+  std::vector<int2> item_tab(n_items);
+  std::vector<int4> desc;
+  std::vector<int> tile_off(n_tiles), tile_ts(n_tiles);
+  int ts_max = 0;
+  for (int t = 0; t < n_tiles; ++t) {
+    const int i0 = t * K1_THREADS, i1 = std::min(n_items, i0 + K1_THREADS);
+    const int r_lo = item_row[i0], r_hi = item_row[i1 - 1];
+    int my_lo = items[i0].my, my_hi = items[i0].my;
+    for (int i = i0; i < i1; ++i) {
+      my_lo = std::min(my_lo, items[i].my);
+      my_hi = std::max(my_hi, items[i].my);
+    }
+    const int n_r = r_hi - r_lo + 1, n_y = my_hi - my_lo + 1;
+    const int TS = n_r + n_y + 1;
+    if (TS > 8192) return h->fail(EWB_EINVAL, "k-table too sparse for the tile planner");
+    tile_off[t] = (int)desc.size();
+    tile_ts[t] = TS;
+    ts_max = std::max(ts_max, TS);
+    for (int r = r_lo; r <= r_hi; ++r) {
+      int fl = TF_QSCALE;
+      if (r > r_lo && rows[r].y == rows[r - 1].y && rows[r].x == rows[r - 1].x + 1)
+        fl |= TF_LINK | (0 << 2);
+      desc.push_back(make_int4(rows[r].x, 0, rows[r].y, fl));
+    }
+    for (int y = my_lo; y <= my_hi; ++y)
+      desc.push_back(make_int4(0, y, 0, y > my_lo ? (TF_LINK | (1 << 2)) : 0));
+    desc.push_back(make_int4(0, 0, 1, 0));
+    for (int i = i0; i < i1; ++i) item_tab[i] = make_int2(item_row[i] - r_lo, n_r + items[i].my - my_lo);
+  }
+
+  P.K = K;
+  P.M = M;
+  P.n_items = n_items;
+  P.n_rows = n_rows;
+  P.n_tiles = n_tiles;
+  P.ts_max = ts_max;
+  P.pchunk = std::max(1, std::min(K1_PMAX, (160 * 1024) / (16 * ts_max)));
+  P.ks_cached = -1;
+  int rc;
+  if ((rc = upload(h, P.item_tab, item_tab))) return rc;
+  if ((rc = upload(h, P.item_my, item_my))) return rc;
+  if ((rc = upload(h, P.item_row, item_row))) return rc;
+  if ((rc = upload(h, P.rows, rows))) return rc;
+  if ((rc = upload(h, P.tab_desc, desc))) return rc;
+  if ((rc = upload(h, P.tile_off, tile_off))) return rc;
+  if ((rc = upload(h, P.tile_ts, tile_ts))) return rc;
+  if ((rc = upload(h, P.slot_k, slot_k))) return rc;
+  if ((rc = upload(h, P.slot_coeff, slot_coeff))) return rc;
+  return EWB_OK;
+}
+
+int ensure_ks(ewb_handle *h, int n_ks) {
+  Plan &P = h->plan;
+  if (P.ks_cached == n_ks) return EWB_OK;
+  std::vector<int> b(n_ks + 1);
+  b[0] = 0;
+  b[n_ks] = P.n_rows;
+  for (int q = 1; q < n_ks; ++q) {
+    const int64_t target = (int64_t)q * P.n_items / n_ks;
+    int r = (int)(std::lower_bound(P.row_item_prefix.begin(), P.row_item_prefix.end(), target) -
+                  P.row_item_prefix.begin());
+    b[q] = std::max(b[q - 1], std::min(r, P.n_rows));
+  }
+  int rc = upload(h, P.ks_rows, b);
+  if (rc) return rc;
+  P.ks_cached = n_ks;
+  return EWB_OK;
+}
+
+int require_state(ewb_handle *h, bool need_kspace, bool need_loaded) {
+  if (!h) return EWB_EINVAL;
+  if (!h->have_system) return h->fail(EWB_ESTATE, "ewb_set_system not called");
+  if (need_kspace && !h->have_kspace) return h->fail(EWB_ESTATE, "ewb_set_kspace not called");
+  if (need_loaded && !h->loaded) return h->fail(EWB_ESTATE, "no particles loaded");
+  return EWB_OK;
+}
+
+// ---- stages (all asynchronous on h->stream) ----
+int stage_load(ewb_handle *h, const double *d_pos, const double *d_q, int64_t n) {
+  if (n < 1) return h->fail(EWB_EINVAL, "particle count must be >= 1");
+  if (n >= (int64_t)1 << 27) return h->fail(EWB_EINVAL, "particle count must be < 2^27");
+  CK(h->frac.ensure(n * sizeof(double4)));
+  CK(h->xyzq.ensure(n * sizeof(double4)));
+  CK(h->base.ensure(n * 3 * sizeof(double2)));
+  CK(h->errflag.ensure(sizeof(int)));
+  CK(cudaMemsetAsync(h->errflag.p, 0, sizeof(int), h->stream));
+  k_prep<<<blocks_for(n, 256), 256, 0, h->stream>>>(d_pos, d_q, n, h->L, h->frac.as<double4>(),
+                                                    h->base.as<double2>(), h->xyzq.as<double4>(),
+                                                    h->errflag.as<int>());
+  CKL();
+  h->n = n;
+  h->loaded = true;
+  return EWB_OK;
+}
+
+int occupancy_k1(ewb_handle *h, int M, size_t smem, int *occ_out) {
+  if (!h->k1_attr[M]) {
+    CK(cudaFuncSetAttribute((const void *)k1_table(M), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            200 * 1024));
+    h->k1_attr[M] = true;
+  }
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)k1_table(M), K1_THREADS,
+                                                   smem));
+  *occ_out = std::max(1, occ);
+  return EWB_OK;
+}
+
+// S(k) over particles [i0, i1): partials over particle chunks reduced into
+// d_slots (if non-null) or left in h->spart with *n_part set.
+int stage_rho(ewb_handle *h, int64_t i0, int64_t i1, int *n_part_out) {
+  Plan &P = h->plan;
+  const int M = P.M;
+  const size_t smem = (size_t)P.pchunk * P.ts_max * sizeof(double2);
+  int occ = 1;
+  int rc = occupancy_k1(h, M, smem, &occ);
+  if (rc) return rc;
+  const int64_t n = std::max<int64_t>(0, i1 - i0);
+  const int64_t max_pc = std::max<int64_t>(1, std::min<int64_t>(4096, (n + 31) / 32));
+  int n_pc = best_split(P.n_tiles, (int64_t)h->n_sm * occ, (int)max_pc);
+  int64_t ppb = (n + n_pc - 1) / std::max(1, n_pc);
+  ppb = std::max<int64_t>(1, ppb);
+  n_pc = (int)std::max<int64_t>(1, (n + ppb - 1) / ppb);
+  const size_t n_slots = (size_t)M * P.n_items;
+  CK(h->spart.ensure((size_t)n_pc * n_slots * sizeof(double2)));
+  dim3 grid(P.n_tiles, n_pc);
+  k1_table(M)<<<grid, K1_THREADS, smem, h->stream>>>(
+      h->frac.as<double4>(), h->base.as<double2>(), i0, std::max(i0, i1), ppb, P.pchunk,
+      P.item_tab.as<int2>(), P.n_items, P.tab_desc.as<int4>(), P.tile_off.as<int>(),
+      P.tile_ts.as<int>(), h->spart.as<double2>());
+  CKL();
+  *n_part_out = n_pc;
+  return EWB_OK;
+}
+
+// finalize from n_part partial slot buffers in `src`
+int stage_finalize(ewb_handle *h, const double2 *src, int n_part, double *d_rho_out,
+                   double *d_u_out) {
+  Plan &P = h->plan;
+  const int64_t n_slots = (int64_t)P.M * P.n_items;
+  const unsigned nb = blocks_for(n_slots, RED_THREADS);
+  CK(h->sp.ensure(n_slots * sizeof(double2)));
+  CK(h->eblk.ensure(nb * sizeof(double)));
+  k2_finalize<<<nb, RED_THREADS, 0, h->stream>>>(src, n_part, n_slots, P.slot_k.as<int>(),
+                                                 P.slot_coeff.as<double>(), P.K, d_rho_out,
+                                                 nullptr, h->sp.as<double2>(),
+                                                 h->eblk.as<double>(), 1);
+  CKL();
+  k_sum<<<1, 1024, 0, h->stream>>>(h->eblk.as<double>(), nb, 1.0, d_u_out);
+  CKL();
+  return EWB_OK;
+}
+
+int stage_recip_forces(ewb_handle *h, int64_t i0, int64_t i1, double *d_force, bool energy,
+                       double *d_u_out) {
+  Plan &P = h->plan;
+  const int64_t n_local = std::max<int64_t>(0, i1 - i0);
+  if (n_local == 0) {
+    if (energy) CK(cudaMemsetAsync(d_u_out, 0, sizeof(double), h->stream));
+    return EWB_OK;
+  }
+  const int M = P.M;
+  k3_fn fn = k3_table(M, energy);
+  int &occ = h->occ_k3[M][energy ? 1 : 0];
+  if (occ == 0) {
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)fn, K3_THREADS, 0));
+    occ = std::max(1, occ);
+  }
+  const int64_t ptiles = (n_local + K3_THREADS * K3_PPT - 1) / (K3_THREADS * K3_PPT);
+  const int max_ks = std::max(1, std::min(P.n_rows, 64));
+  const int n_ks = best_split(ptiles, (int64_t)h->n_sm * occ, max_ks);
+  int rc = ensure_ks(h, n_ks);
+  if (rc) return rc;
+  CK(h->fpart.ensure((size_t)n_ks * 3 * n_local * sizeof(double)));
+  if (energy) CK(h->upart.ensure((size_t)n_ks * n_local * sizeof(double)));
+  dim3 grid((unsigned)ptiles, n_ks);
+  fn<<<grid, K3_THREADS, 0, h->stream>>>(h->frac.as<double4>(), h->base.as<double2>(), i0, i1,
+                                         P.rows.as<int4>(), P.ks_rows.as<int>(),
+                                         P.item_my.as<int>(), P.item_row.as<int>(),
+                                         h->sp.as<double2>(), P.n_items, h->fpart.as<double>(),
+                                         energy ? h->upart.as<double>() : nullptr);
+  CKL();
+  const unsigned nb = blocks_for(n_local, RED_THREADS);
+  if (energy) CK(h->eblk2.ensure(nb * sizeof(double)));
+  k3_combine<<<nb, RED_THREADS, 0, h->stream>>>(
+      h->fpart.as<double>(), energy ? h->upart.as<double>() : nullptr, n_ks, i0, n_local,
+      h->frac.as<double4>(), 4.0 * M_PI / h->L, d_force, energy ? h->eblk2.as<double>() : nullptr,
+      energy ? 1 : 0);
+  CKL();
+  if (energy) {
+    k_sum<<<1, 1024, 0, h->stream>>>(h->eblk2.as<double>(), nb, 1.0, d_u_out);
+    CKL();
+  }
+  return EWB_OK;
+}
+
+// Cell list + real space for z-slab part/nparts; u_sr into d_u_out.
+int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, double *d_u_out,
+                     cudaEvent_t ev_cell) {
+  const int64_t n = h->n;
+  if (!(h->rc > 0.0)) return h->fail(EWB_EINVAL, "cutoff must be positive");
+  if (h->rc > 0.5 * h->L)
+    return h->fail(EWB_ECUTOFF, "cutoff " + std::to_string(h->rc) + " exceeds L/2 = " +
+                                    std::to_string(0.5 * h->L) + " (minimum-image bound)");
+  // reference binning: cpd = floor(L / r_c), edge = L / cpd (celllist.py:96-98);
+  // with cpd < 3 the 27-stencil folds onto every cell and the reference scans
+  // all particles with a per-pair fold (engine.py:111-134) -- FOLD mode here.
+  int cpd = (int)std::floor(h->L / h->rc);
+  if (cpd < 1) cpd = 1;
+  if (cpd > 128) cpd = 128;  // edge stays >= r_c; bounds the cell arrays
+  const bool fold = cpd < 3;
+  const int cpd_eff = fold ? 1 : cpd;
+  const int n_cells = cpd_eff * cpd_eff * cpd_eff;
+  const double edge = h->L / cpd;
+  CK(h->cell_of.ensure(n * sizeof(int)));
+  CK(h->slot.ensure(n * sizeof(int)));
+  CK(h->count.ensure((n_cells + 1) * sizeof(int)));
+  CK(h->start.ensure((n_cells + 1) * sizeof(int)));
+  CK(h->gstart.ensure((n_cells + 1) * sizeof(int)));
+  CK(h->order_tmp.ensure(n * sizeof(int)));
+  CK(h->order.ensure(n * sizeof(int)));
+  CK(h->sorted.ensure(n * sizeof(double4)));
+  CK(cudaMemsetAsync(h->count.p, 0, (n_cells + 1) * sizeof(int), h->stream));
+  k4_bin_count<<<blocks_for(n, 256), 256, 0, h->stream>>>(h->xyzq.as<double4>(), n, edge, cpd_eff,
+                                                          h->cell_of.as<int>(), h->slot.as<int>(),
+                                                          h->count.as<int>());
+  CKL();
+  k_scan_cells<<<1, 1024, 0, h->stream>>>(h->count.as<int>(), n_cells, h->start.as<int>(),
+                                          h->gstart.as<int>());
+  CKL();
+  if (fold) {
+    k_iota<<<blocks_for(n, 256), 256, 0, h->stream>>>(h->order.as<int>(), n);
+    CKL();
+  } else {
+    k5_scatter<<<blocks_for(n, 256), 256, 0, h->stream>>>(h->cell_of.as<int>(), h->slot.as<int>(),
+                                                          n, h->start.as<int>(),
+                                                          h->order_tmp.as<int>());
+    CKL();
+    k5_cell_sort<<<n_cells, 256, 0, h->stream>>>(h->start.as<int>(), h->order_tmp.as<int>(),
+                                                 h->order.as<int>());
+    CKL();
+  }
+  k5_gather<<<blocks_for(n, 256), 256, 0, h->stream>>>(h->order.as<int>(), h->xyzq.as<double4>(),
+                                                       n, h->sorted.as<double4>());
+  CKL();
+  if (ev_cell) CK(cudaEventRecord(ev_cell, h->stream));
+
+  RSParams rp;
+  rp.L = h->L;
+  rp.hl = 0.5 * h->L;
+  rp.rc2 = h->rc2;
+  rp.sa = std::sqrt(h->alpha);
+  rp.al = h->alpha;
+  rp.tsap = 2.0 * std::sqrt(h->alpha / M_PI);
+  rp.cpd = cpd_eff;
+  rp.fold = fold;
+  rp.n = n;
+  const int zl = (int)((int64_t)cpd_eff * part / nparts), zh = (int)((int64_t)cpd_eff * (part + 1) / nparts);
+  rp.c_lo = zl * cpd_eff * cpd_eff;
+  rp.c_hi = zh * cpd_eff * cpd_eff;
+  const int64_t cells_slab = rp.c_hi - rp.c_lo;
+  const int64_t units_max = n / 32 + cells_slab + 1;
+  const unsigned nb = (unsigned)std::max<int64_t>(1, (units_max + K6_WARPS - 1) / K6_WARPS);
+  CK(h->eblk.ensure(nb * sizeof(double)));
+  if (cells_slab <= 0) {
+    CK(cudaMemsetAsync(d_u_out, 0, sizeof(double), h->stream));
+    return EWB_OK;
+  }
+  if (fold)
+    k6_real_space<true><<<nb, K6_WARPS * 32, 0, h->stream>>>(
+        h->sorted.as<double4>(), h->order.as<int>(), h->start.as<int>(), h->gstart.as<int>(), rp,
+        d_force, h->eblk.as<double>(), h->errflag.as<int>());
+  else
+    k6_real_space<false><<<nb, K6_WARPS * 32, 0, h->stream>>>(
+        h->sorted.as<double4>(), h->order.as<int>(), h->start.as<int>(), h->gstart.as<int>(), rp,
+        d_force, h->eblk.as<double>(), h->errflag.as<int>());
+  CKL();
+  k_sum<<<1, 1024, 0, h->stream>>>(h->eblk.as<double>(), nb, 1.0, d_u_out);
+  CKL();
+  return EWB_OK;
+}
+
+int stage_self(ewb_handle *h, double *d_u_out) {
+  const unsigned nb = (unsigned)std::min<int64_t>(1024, blocks_for(h->n, RED_THREADS));
+  CK(h->eblk2.ensure(std::max<size_t>(nb, 1) * sizeof(double)));
+  k7_sum_q2<<<nb, RED_THREADS, 0, h->stream>>>(h->frac.as<double4>(), h->n, h->eblk2.as<double>());
+  CKL();
+  k_sum<<<1, 1024, 0, h->stream>>>(h->eblk2.as<double>(), nb, -std::sqrt(h->alpha / M_PI), d_u_out);
+  CKL();
+  return EWB_OK;
+}
+
+int check_errflag(ewb_handle *h, int mask) {
+  int e = 0;
+  CK(cudaMemcpyAsync(&e, h->errflag.p, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  e &= mask;
+  if (e & ERR_UNWRAPPED)
+    return h->fail(EWB_EUNWRAPPED, "positions must be wrapped into [0, L) before binning");
+  if (e & ERR_COINCIDENT)
+    return h->fail(EWB_ECOINCIDENT, "coincident particles in Coulomb kernel");
+  return EWB_OK;
+}
+
+int h2d_particles(ewb_handle *h, const double *pos, const double *q, int64_t n) {
+  if (!pos || !q) return h->fail(EWB_EINVAL, "null particle arrays");
+  CK(h->pos.ensure(n * 3 * sizeof(double)));
+  CK(h->q.ensure(n * sizeof(double)));
+  CK(cudaMemcpyAsync(h->pos.p, pos, n * 3 * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  CK(cudaMemcpyAsync(h->q.p, q, n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  return stage_load(h, h->pos.as<double>(), h->q.as<double>(), n);
+}
+
+int h2d_force(ewb_handle *h, const double *force, int64_t n) {
+  CK(h->force.ensure(n * 3 * sizeof(double)));
+  CK(cudaMemcpyAsync(h->force.p, force, n * 3 * sizeof(double), cudaMemcpyHostToDevice,
+                     h->stream));
+  return EWB_OK;
+}
+
+// full single-GPU pipeline on loaded particles; energies stay on device
+int pipeline(ewb_handle *h, double *d_force, double *d_rho_out, bool timed) {
+  int rc;
+  CK(h->energy.ensure(8 * sizeof(double)));
+  double *en = h->energy.as<double>();
+  if (timed) CK(cudaEventRecord(h->ev[0], h->stream));
+  if ((rc = stage_real_space(h, 0, 1, d_force, en + 0, timed ? h->ev[1] : nullptr))) return rc;
+  if (timed) CK(cudaEventRecord(h->ev[2], h->stream));
+  int n_part = 0;
+  if ((rc = stage_rho(h, 0, h->n, &n_part))) return rc;
+  if ((rc = stage_finalize(h, h->spart.as<double2>(), n_part, d_rho_out, en + 1))) return rc;
+  if (timed) CK(cudaEventRecord(h->ev[3], h->stream));
+  if ((rc = stage_recip_forces(h, 0, h->n, d_force, false, nullptr))) return rc;
+  if (timed) CK(cudaEventRecord(h->ev[4], h->stream));
+  if ((rc = stage_self(h, en + 2))) return rc;
+  return EWB_OK;
+}
+
+__global__ void k_rho_to_slots(const double *__restrict__ rho, int64_t K,
+                               const int *__restrict__ slot_k, int64_t n_slots,
+                               double2 *__restrict__ out) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= n_slots) return;
+  const int k = slot_k[s];
+  out[s] = k >= 0 ? make_double2(rho[k], rho[K + k]) : make_double2(0.0, 0.0);
+}
+
+// rho (caller order, h->rho) -> slot layout (h->sslot)
+int stage_rho_to_slots(ewb_handle *h) {
+  const int64_t n_slots = (int64_t)h->plan.M * h->plan.n_items;
+  k_rho_to_slots<<<blocks_for(n_slots, 256), 256, 0, h->stream>>>(
+      h->rho.as<double>(), h->plan.K, h->plan.slot_k.as<int>(), n_slots, h->sslot.as<double2>());
+  CKL();
+  return EWB_OK;
+}
+
+int read_timings(ewb_handle *h, double *timings) {
+  if (!timings) return EWB_OK;
+  float a = 0, b = 0, c = 0, d = 0;
+  CK(cudaEventElapsedTime(&a, h->ev[0], h->ev[1]));
+  CK(cudaEventElapsedTime(&b, h->ev[0], h->ev[2]));
+  CK(cudaEventElapsedTime(&c, h->ev[2], h->ev[3]));
+  CK(cudaEventElapsedTime(&d, h->ev[3], h->ev[4]));
+  timings[0] = a * 1e-3;
+  timings[1] = b * 1e-3;
+  timings[2] = c * 1e-3;
+  timings[3] = d * 1e-3;
+  return EWB_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+extern "C" {
+
+int ewb_version(void) { return EWB_VERSION; }
+
+int ewb_create(int device, ewb_handle **out) {
+  if (!out) return EWB_EINVAL;
+  *out = nullptr;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) return EWB_ECUDA;
+  if (device < 0 || device >= ndev) return EWB_EINVAL;
+  if (cudaSetDevice(device) != cudaSuccess) return EWB_ECUDA;
+  ewb_handle *h = new ewb_handle();
+  h->device = device;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) h->n_sm = prop.multiProcessorCount;
+  if (cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete h;
+    return EWB_ECUDA;
+  }
+  h->stream = h->own_stream;
+  for (auto &ev : h->ev)
+    if (cudaEventCreate(&ev) != cudaSuccess) {
+      delete h;
+      return EWB_ECUDA;
+    }
+  *out = h;
+  return EWB_OK;
+}
+
+void ewb_destroy(ewb_handle *h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  for (DBuf *b : {&h->pos, &h->q, &h->force, &h->rho, &h->frac, &h->base, &h->xyzq, &h->spart,
+                  &h->sslot, &h->sp, &h->fpart, &h->upart, &h->eblk, &h->eblk2, &h->energy,
+                  &h->errflag, &h->cell_of, &h->slot, &h->count, &h->start, &h->gstart,
+                  &h->order_tmp, &h->order, &h->sorted})
+    b->release();
+  h->plan.release();
+  for (auto &ev : h->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (h->own_stream) cudaStreamDestroy(h->own_stream);
+  delete h;
+}
+
+const char *ewb_last_error(const ewb_handle *h) { return h ? h->err.c_str() : "null handle"; }
+
+int ewb_set_stream(ewb_handle *h, uintptr_t stream) {
+  if (!h) return EWB_EINVAL;
+  h->stream = stream ? reinterpret_cast<cudaStream_t>(stream) : h->own_stream;
+  return EWB_OK;
+}
+
+int ewb_set_max_segment(ewb_handle *h, int mcap) {
+  if (!h) return EWB_EINVAL;
+  if (mcap < 1 || mcap > MAXM) return h->fail(EWB_EINVAL, "segment length must be in [1, 32]");
+  h->mcap = mcap;
+  return EWB_OK;
+}
+
+int ewb_set_system(ewb_handle *h, double L, double alpha, double r_cutoff, double rc2) {
+  if (!h) return EWB_EINVAL;
+  if (!(L > 0.0) || !std::isfinite(L)) return h->fail(EWB_EINVAL, "box edge length must be positive");
+  if (!(alpha > 0.0) || !std::isfinite(alpha)) return h->fail(EWB_EINVAL, "alpha must be positive");
+  h->L = L;
+  h->alpha = alpha;
+  h->rc = r_cutoff;
+  h->rc2 = rc2;
+  h->have_system = true;
+  return EWB_OK;
+}
+
+int ewb_set_kspace(ewb_handle *h, const int64_t *m_int, int64_t K, const double *coeff) {
+  if (!h) return EWB_EINVAL;
+  if (!m_int && K > 0) return h->fail(EWB_EINVAL, "null m_int");
+  CK(cudaSetDevice(h->device));
+  int rc = build_plan(h, m_int, K, coeff);
+  if (rc) return rc;
+  h->have_kspace = true;
+  return EWB_OK;
+}
+
+int ewb_kspace_info(const ewb_handle *h, int64_t *info6) {
+  if (!h || !info6) return EWB_EINVAL;
+  info6[0] = h->plan.K;
+  info6[1] = h->plan.n_items;
+  info6[2] = h->plan.M;
+  info6[3] = h->plan.n_rows;
+  info6[4] = h->plan.n_tiles;
+  info6[5] = h->plan.ts_max;
+  return EWB_OK;
+}
+
+int ewb_compute_rho_hat(ewb_handle *h, const double *pos, const double *q, int64_t n,
+                        double *rho_out) {
+  int rc = require_state(h, true, false);
+  if (rc) return rc;
+  CK(cudaSetDevice(h->device));
+  if ((rc = h2d_particles(h, pos, q, n))) return rc;
+  CK(h->rho.ensure(2 * h->plan.K * sizeof(double)));
+  CK(h->energy.ensure(8 * sizeof(double)));
+  int n_part = 0;
+  if ((rc = stage_rho(h, 0, n, &n_part))) return rc;
+  if ((rc = stage_finalize(h, h->spart.as<double2>(), n_part, h->rho.as<double>(),
+                           h->energy.as<double>() + 1)))
+    return rc;
+  CK(cudaMemcpyAsync(rho_out, h->rho.p, 2 * h->plan.K * sizeof(double), cudaMemcpyDeviceToHost,
+                     h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return EWB_OK;
+}
+
+int ewb_long_range(ewb_handle *h, const double *pos, const double *q, int64_t n, const double *rho,
+                   double *force_inout, double *u_lr) {
+  int rc = require_state(h, true, false);
+  if (rc) return rc;
+  CK(cudaSetDevice(h->device));
+  if ((rc = h2d_particles(h, pos, q, n))) return rc;
+  if ((rc = h2d_force(h, force_inout, n))) return rc;
+  // rho given by the caller (any values): scatter it into slot layout
+  const int64_t K = h->plan.K;
+  const int64_t n_slots = (int64_t)h->plan.M * h->plan.n_items;
+  CK(h->rho.ensure(2 * K * sizeof(double)));
+  CK(h->sslot.ensure(n_slots * sizeof(double2)));
+  CK(h->energy.ensure(8 * sizeof(double)));
+  CK(cudaMemcpyAsync(h->rho.p, rho, 2 * K * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  if ((rc = stage_rho_to_slots(h))) return rc;
+  if ((rc = stage_finalize(h, h->sslot.as<double2>(), 1, nullptr, h->energy.as<double>() + 7)))
+    return rc;
+  if ((rc = stage_recip_forces(h, 0, n, h->force.as<double>(), true, h->energy.as<double>() + 1)))
+    return rc;
+  double u = 0.0;
+  CK(cudaMemcpyAsync(&u, h->energy.as<double>() + 1, sizeof(double), cudaMemcpyDeviceToHost,
+                     h->stream));
+  CK(cudaMemcpyAsync(force_inout, h->force.p, n * 3 * sizeof(double), cudaMemcpyDeviceToHost,
+                     h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  if (u_lr) *u_lr = u;
+  return EWB_OK;
+}
+
+int ewb_short_range(ewb_handle *h, const double *pos, const double *q, int64_t n,
+                    double *force_inout, double *u_sr) {
+  int rc = require_state(h, false, false);
+  if (rc) return rc;
+  CK(cudaSetDevice(h->device));
+  if (!(h->rc > 0.0)) return h->fail(EWB_EINVAL, "cutoff must be positive");
+  if (h->rc > 0.5 * h->L)
+    return h->fail(EWB_ECUTOFF, "cutoff exceeds L/2 (minimum-image bound)");
+  if ((rc = h2d_particles(h, pos, q, n))) return rc;
+  if ((rc = check_errflag(h, ERR_UNWRAPPED))) return rc;
+  if ((rc = h2d_force(h, force_inout, n))) return rc;
+  CK(h->energy.ensure(8 * sizeof(double)));
+  if ((rc = stage_real_space(h, 0, 1, h->force.as<double>(), h->energy.as<double>(), nullptr)))
+    return rc;
+  double u = 0.0;
+  CK(cudaMemcpyAsync(&u, h->energy.as<double>(), sizeof(double), cudaMemcpyDeviceToHost,
+                     h->stream));
+  if ((rc = check_errflag(h, ERR_COINCIDENT))) return rc;
+  CK(cudaMemcpy(force_inout, h->force.p, n * 3 * sizeof(double), cudaMemcpyDeviceToHost));
+  if (u_sr) *u_sr = u;
+  return EWB_OK;
+}
+
+int ewb_self_energy(ewb_handle *h, const double *q, int64_t n, double *u_self) {
+  int rc = require_state(h, false, false);
+  if (rc) return rc;
+  CK(cudaSetDevice(h->device));
+  if (n < 1) return h->fail(EWB_EINVAL, "particle count must be >= 1");
+  CK(h->q.ensure(n * sizeof(double)));
+  CK(h->pos.ensure(n * 3 * sizeof(double)));
+  CK(cudaMemcpyAsync(h->q.p, q, n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  CK(cudaMemsetAsync(h->pos.p, 0, n * 3 * sizeof(double), h->stream));
+  if ((rc = stage_load(h, h->pos.as<double>(), h->q.as<double>(), n))) return rc;
+  CK(h->energy.ensure(8 * sizeof(double)));
+  if ((rc = stage_self(h, h->energy.as<double>() + 2))) return rc;
+  double u = 0.0;
+  CK(cudaMemcpyAsync(&u, h->energy.as<double>() + 2, sizeof(double), cudaMemcpyDeviceToHost,
+                     h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  if (u_self) *u_self = u;
+  return EWB_OK;
+}
+
+int ewb_evaluate(ewb_handle *h, const double *pos, const double *q, int64_t n,
+                 double *force_inout, double *rho_out, double *energies, double *timings) {
+  int rc = require_state(h, true, false);
+  if (rc) return rc;
+  CK(cudaSetDevice(h->device));
+  if (!(h->rc > 0.0)) return h->fail(EWB_EINVAL, "cutoff must be positive");
+  if (h->rc > 0.5 * h->L)
+    return h->fail(EWB_ECUTOFF, "cutoff exceeds L/2 (minimum-image bound)");
+  if ((rc = h2d_particles(h, pos, q, n))) return rc;
+  if ((rc = h2d_force(h, force_inout, n))) return rc;
+  if (rho_out) CK(h->rho.ensure(2 * h->plan.K * sizeof(double)));
+  if ((rc = pipeline(h, h->force.as<double>(), rho_out ? h->rho.as<double>() : nullptr, true)))
+    return rc;
+  double en[3];
+  CK(cudaMemcpyAsync(en, h->energy.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  if ((rc = check_errflag(h, ERR_UNWRAPPED | ERR_COINCIDENT))) return rc;
+  CK(cudaMemcpy(force_inout, h->force.p, n * 3 * sizeof(double), cudaMemcpyDeviceToHost));
+  if (rho_out)
+    CK(cudaMemcpy(rho_out, h->rho.p, 2 * h->plan.K * sizeof(double), cudaMemcpyDeviceToHost));
+  if (energies) std::memcpy(energies, en, sizeof en);
+  return read_timings(h, timings);
+}
+
+// ---- device-pointer stages ----
+int ewb_dev_load(ewb_handle *h, const double *d_pos, const double *d_q, int64_t n) {
+  int rc = require_state(h, false, false);
+  if (rc) return rc;
+  CK(cudaSetDevice(h->device));
+  return stage_load(h, d_pos, d_q, n);
+}
+
+int64_t ewb_dev_slot_doubles(const ewb_handle *h) {
+  if (!h || !h->have_kspace) return -1;
+  return 2 * (int64_t)h->plan.M * h->plan.n_items;
+}
+
+int ewb_dev_rho_partial(ewb_handle *h, int64_t i0, int64_t i1, double *d_slots) {
+  int rc = require_state(h, true, true);
+  if (rc) return rc;
+  if (i0 < 0 || i1 > h->n || i0 > i1) return h->fail(EWB_EINVAL, "bad particle range");
+  CK(cudaSetDevice(h->device));
+  const int64_t n_slots = (int64_t)h->plan.M * h->plan.n_items;
+  if (i1 == i0) {
+    CK(cudaMemsetAsync(d_slots, 0, n_slots * sizeof(double2), h->stream));
+    return EWB_OK;
+  }
+  int n_part = 0;
+  if ((rc = stage_rho(h, i0, i1, &n_part))) return rc;
+  const unsigned nb = blocks_for(n_slots, RED_THREADS);
+  k2_finalize<<<nb, RED_THREADS, 0, h->stream>>>(h->spart.as<double2>(), n_part, n_slots, nullptr,
+                                                 nullptr, h->plan.K, nullptr,
+                                                 reinterpret_cast<double2 *>(d_slots), nullptr,
+                                                 nullptr, 0);
+  CKL();
+  return EWB_OK;
+}
+
+int ewb_dev_kspace_finalize(ewb_handle *h, const double *d_slots, double *d_rho_out, double *u_lr) {
+  int rc = require_state(h, true, false);
+  if (rc) return rc;
+  CK(cudaSetDevice(h->device));
+  CK(h->energy.ensure(8 * sizeof(double)));
+  if ((rc = stage_finalize(h, reinterpret_cast<const double2 *>(d_slots), 1, d_rho_out,
+                           h->energy.as<double>() + 1)))
+    return rc;
+  if (u_lr) {
+    CK(cudaMemcpyAsync(u_lr, h->energy.as<double>() + 1, sizeof(double), cudaMemcpyDeviceToHost,
+                       h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+  }
+  return EWB_OK;
+}
+
+int ewb_dev_recip_forces(ewb_handle *h, int64_t i0, int64_t i1, double *d_force) {
+  int rc = require_state(h, true, true);
+  if (rc) return rc;
+  if (i0 < 0 || i1 > h->n || i0 > i1) return h->fail(EWB_EINVAL, "bad particle range");
+  CK(cudaSetDevice(h->device));
+  return stage_recip_forces(h, i0, i1, d_force, false, nullptr);
+}
+
+int ewb_dev_real_space(ewb_handle *h, int part, int nparts, double *d_force, double *u_sr) {
+  int rc = require_state(h, false, true);
+  if (rc) return rc;
+  if (nparts < 1 || part < 0 || part >= nparts) return h->fail(EWB_EINVAL, "bad slab index");
+  CK(cudaSetDevice(h->device));
+  if ((rc = check_errflag(h, ERR_UNWRAPPED))) return rc;
+  CK(h->energy.ensure(8 * sizeof(double)));
+  if ((rc = stage_real_space(h, part, nparts, d_force, h->energy.as<double>(), nullptr))) return rc;
+  double u = 0.0;
+  CK(cudaMemcpyAsync(&u, h->energy.as<double>(), sizeof(double), cudaMemcpyDeviceToHost,
+                     h->stream));
+  if ((rc = check_errflag(h, ERR_COINCIDENT))) return rc;
+  if (u_sr) *u_sr = u;
+  return EWB_OK;
+}
+
+int ewb_dev_self_energy(ewb_handle *h, double *u_self) {
+  int rc = require_state(h, false, true);
+  if (rc) return rc;
+  CK(cudaSetDevice(h->device));
+  CK(h->energy.ensure(8 * sizeof(double)));
+  if ((rc = stage_self(h, h->energy.as<double>() + 2))) return rc;
+  double u = 0.0;
+  CK(cudaMemcpyAsync(&u, h->energy.as<double>() + 2, sizeof(double), cudaMemcpyDeviceToHost,
+                     h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  if (u_self) *u_self = u;
+  return EWB_OK;
+}
+
+int ewb_dev_evaluate(ewb_handle *h, const double *d_pos, const double *d_q, int64_t n,
+                     double *d_force, double *d_rho_out, double *energies, double *timings) {
+  int rc = require_state(h, true, false);
+  if (rc) return rc;
+  CK(cudaSetDevice(h->device));
+  if (!(h->rc > 0.0)) return h->fail(EWB_EINVAL, "cutoff must be positive");
+  if (h->rc > 0.5 * h->L)
+    return h->fail(EWB_ECUTOFF, "cutoff exceeds L/2 (minimum-image bound)");
+  if ((rc = stage_load(h, d_pos, d_q, n))) return rc;
+  if ((rc = pipeline(h, d_force, d_rho_out, timings != nullptr))) return rc;
+  double en[3];
+  CK(cudaMemcpyAsync(en, h->energy.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  if ((rc = check_errflag(h, ERR_UNWRAPPED | ERR_COINCIDENT))) return rc;
+  if (energies) std::memcpy(energies, en, sizeof en);
+  return read_timings(h, timings);
+}
+
+int64_t ewb_launch_count(const ewb_handle *h) { return h ? h->launches : -1; }
+
+}  // extern "C"
+

@@ -1,0 +1,312 @@
+"""Ewald energy/force entry points -- drop-in for the reference ``ewald.py``.
+
+Same names, argument order, return values, in-place side effects and
+exceptions as ``/root/reference/pkg/src/ewaldmd/ewald.py``; every number is
+computed by the sm_100a kernels behind the C-ABI (``_lib.py``).  There is
+no CPU path: a missing library or device raises.
+
+Reference interfaces mirrored (file:line in the reference package):
+
+* ``EwaldParams`` (ewald.py:40-72), ``BALANCE_CONSTANT`` (:80),
+  ``choose_parameters`` (:83-136) -- host scalar set-up, reproduced exactly.
+* ``ReciprocalSpace`` (:139-173), ``enumerate_kvectors`` (:176-202) --
+  the k-table and C_k; the table is handed to the device planner unchanged.
+* ``compute_rho_hat`` (:457-464) -> ``ewb_compute_rho_hat``.
+* ``long_range_energy_forces`` (:467-479) -> ``ewb_long_range``.
+* ``self_energy`` (:482-484) -> ``ewb_self_energy``.
+* ``EwaldEnergies`` (:582-596), ``EwaldSolver`` (:599-655),
+  ``total_coulomb`` (:658-665) -> ``ewb_evaluate``.
+
+``workers`` is accepted for signature compatibility and ignored: one
+process drives one GPU; multi-GPU sharding lives in ``distributed.py``.
+``cell_list`` is accepted and ignored: the device builds its own.
+"""
+
+import math
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .core import (
+    BoxTooSmallError,
+    GlobalAccumulator,
+    KSpaceEmptyError,
+    require_neutral,
+)
+
+
+@dataclass(frozen=True)
+class EwaldParams:
+    """Splitting parameter alpha (A^-2) and cutoffs for one tolerance."""
+
+    alpha: float
+    r_cutoff: float
+    k_cutoff: float
+    tolerance: float
+
+    def truncation_errors(self):
+        real = math.erfc(math.sqrt(self.alpha) * self.r_cutoff) / self.r_cutoff
+        recip = math.exp(-self.k_cutoff**2 / (4.0 * self.alpha))
+        return float(real), float(recip)
+
+    def validate(self):
+        real, recip = self.truncation_errors()
+        if real > self.tolerance * (1.0 + 1e-12):
+            raise ValueError(
+                f"real-space truncation {real:.3e} exceeds tolerance "
+                f"{self.tolerance:.3e}")
+        if recip > self.tolerance * (1.0 + 1e-12):
+            raise ValueError(
+                f"reciprocal truncation {recip:.3e} exceeds tolerance "
+                f"{self.tolerance:.3e}")
+
+
+#: Work-balance constant in alpha = C * (n/V^2)^(1/3) (ewald.py:75-80).
+BALANCE_CONSTANT = 2.0 * math.pi
+
+
+def choose_parameters(n, box, epsilon, alpha=None, r_cutoff=None):
+    """Select (alpha, r_c, k_c) meeting the tolerance (ewald.py:83-136)."""
+    n = int(n)
+    if n < 2:
+        raise ValueError(f"need at least two particles, got {n}")
+    if not 1e-12 < epsilon < 1.0:
+        raise ValueError(f"tolerance must lie in (1e-12, 1), got {epsilon}")
+    if alpha is not None and r_cutoff is not None:
+        raise ValueError("override either alpha or r_cutoff, not both")
+    L = box.edge_length
+    s = math.sqrt(-math.log(epsilon))
+    if alpha is not None:
+        alpha = float(alpha)
+        if alpha <= 0.0:
+            raise ValueError(f"alpha must be positive, got {alpha}")
+        r_c = s / math.sqrt(alpha)
+    else:
+        if r_cutoff is not None:
+            r_c = float(r_cutoff)
+            if r_c <= 0.0:
+                raise ValueError(f"r_cutoff must be positive, got {r_c}")
+            if r_c > box.max_cutoff():
+                r_c = box.max_cutoff()
+        else:
+            alpha = BALANCE_CONSTANT * (n / box.volume**2) ** (1.0 / 3.0)
+            r_c = s / math.sqrt(alpha)
+            if r_c > box.max_cutoff():
+                r_c = box.max_cutoff()
+        alpha = (s / r_c) ** 2
+    k_c = 2.0 * s * math.sqrt(alpha)
+    params = EwaldParams(alpha=alpha, r_cutoff=r_c, k_cutoff=k_c,
+                         tolerance=float(epsilon))
+    try:
+        params.validate()
+    except ValueError as err:
+        raise BoxTooSmallError(
+            f"no parameters meet tolerance {epsilon:.1e} in a box of edge "
+            f"{L} A: {err}") from err
+    return params
+
+
+class ReciprocalSpace:
+    """Half-space k-vector table, coefficients C_k and rho_hat storage.
+
+    Attributes match the reference (ewald.py:150-173).  ``m_int`` may be any
+    (K,3) integer table (sphere, cube, ...); the device plans its own work
+    decomposition from it and writes rho back in this order.
+    """
+
+    def __init__(self, box, params, m_int):
+        L = box.edge_length
+        m_int = np.asarray(m_int)
+        self.box = box
+        self.params = params
+        self.m_int = m_int
+        self.n_stored = m_int.shape[0]
+        self.count = 2 * self.n_stored
+        self.kvec = (2.0 * math.pi / L) * m_int.astype(float)
+        k2 = np.einsum("ij,ij->i", self.kvec, self.kvec)
+        self.coeff = (4.0 * math.pi / (box.volume * k2)) * np.exp(
+            -k2 / (4.0 * params.alpha))
+        self.m_abs = np.abs(m_int).astype(np.int64)
+        self.m_sign = np.where(m_int < 0, -1.0, 1.0)
+        self.mmax = int(self.m_abs.max())
+        self.rho = GlobalAccumulator(2 * self.n_stored)
+        self.dims = np.array([self.n_stored, self.mmax], dtype=np.int64)
+        self.phase_step = np.array([2.0 * math.pi / L])
+
+    @property
+    def rho_complex(self):
+        nk = self.n_stored
+        return self.rho.values[:nk] + 1j * self.rho.values[nk:]
+
+
+def enumerate_kvectors(box, params):
+    """Sphere table 0 < |k| < k_c, lexicographic half (ewald.py:176-202)."""
+    L = box.edge_length
+    bound = params.k_cutoff * L / (2.0 * math.pi)
+    mmax = int(math.floor(bound))
+    if mmax < 1:
+        raise KSpaceEmptyError(
+            f"k_cutoff {params.k_cutoff:.4g} admits no reciprocal vector for "
+            f"box edge {L} (need k_cutoff > 2*pi/L = {2.0 * math.pi / L:.4g})")
+    rng = np.arange(-mmax, mmax + 1)
+    mx, my, mz = np.meshgrid(rng, rng, rng, indexing="ij")
+    m = np.stack([mx.ravel(), my.ravel(), mz.ravel()], axis=1)
+    m2 = np.einsum("ij,ij->i", m, m)
+    below = (m2 > 0) & (m2 < bound * bound)
+    z, y, x = m[:, 2], m[:, 1], m[:, 0]
+    half = (z > 0) | ((z == 0) & (y > 0)) | ((z == 0) & (y == 0) & (x > 0))
+    m = m[below & half]
+    if m.shape[0] == 0:
+        raise KSpaceEmptyError(
+            f"k_cutoff {params.k_cutoff:.4g} admits no reciprocal vector")
+    return ReciprocalSpace(box, params, m.astype(np.int64))
+
+
+# ---------------------------------------------------------------------------
+# device handles: one per ReciprocalSpace (k-space plan) or per solver
+
+_RS_HANDLES = weakref.WeakKeyDictionary()
+
+
+def _kspace_key(rs):
+    return (id(rs), rs.n_stored)
+
+
+def _handle_for(rs, box=None, params=None):
+    """Device handle carrying rs's k-table (created once per table)."""
+    try:
+        h = _RS_HANDLES.get(rs)
+    except TypeError:
+        h = None
+    if h is None:
+        h = _lib.Handle()
+        try:
+            _RS_HANDLES[rs] = h
+        except TypeError:
+            pass
+    box = rs.box if box is None else box
+    params = rs.params if params is None else params
+    h.set_system(box.edge_length, params.alpha, params.r_cutoff)
+    h.set_kspace(rs.m_int, rs.coeff, key=_kspace_key(rs))
+    return h
+
+
+def _particles(ps):
+    pos = _lib.f64c(ps.position, (ps.count, 3))
+    q = _lib.f64c(ps.charge, (ps.count,))
+    return pos, q
+
+
+def _force_buffer(ps):
+    f = ps.force
+    if (isinstance(f, np.ndarray) and f.dtype == np.float64
+            and f.flags.c_contiguous and f.shape == (ps.count, 3)):
+        return f, False
+    return np.ascontiguousarray(f, dtype=np.float64).reshape(ps.count, 3), True
+
+
+def compute_rho_hat(ps, rs, workers=None):
+    """Fill rs.rho with rho_hat(k) = sum_j q_j exp(-i k.r_j) (Alg. 1)."""
+    h = _handle_for(rs)
+    pos, q = _particles(ps)
+    out = np.empty(2 * rs.n_stored)
+    h.compute_rho_hat(pos, q, out)
+    rs.rho.values[:] = out
+    return rs
+
+
+def long_range_energy_forces(ps, rs, workers=None):
+    """Accumulate reciprocal forces into ps.force; return u_lr (Alg. 2).
+
+    Uses the caller's rs.rho as given (ewald.py:467-479), so u_lr is
+    sum_i q_i sum_k C_k Re(e^{ik.r_i} rho_k) even for a foreign rho.
+    """
+    h = _handle_for(rs)
+    pos, q = _particles(ps)
+    f, copied = _force_buffer(ps)
+    rho = _lib.f64c(rs.rho.values)
+    u = h.long_range(pos, q, rho, f)
+    if copied:
+        ps.force[:] = f
+    return u
+
+
+_SELF_HANDLE = None
+
+
+def self_energy(ps, params):
+    """Gaussian-screen self-interaction, -sqrt(alpha/pi) * sum q_i^2."""
+    global _SELF_HANDLE
+    if _SELF_HANDLE is None:
+        _SELF_HANDLE = _lib.Handle()
+    _SELF_HANDLE.set_system(ps.box.edge_length, params.alpha,
+                            params.r_cutoff)
+    q = _lib.f64c(ps.charge, (ps.count,))
+    return _SELF_HANDLE.self_energy(q)
+
+
+@dataclass
+class EwaldEnergies:
+    """Energy breakdown and per-component device times of one evaluation."""
+
+    u_sr: float
+    u_lr: float
+    u_self: float
+    t_cell: float = 0.0
+    t_sr: float = 0.0
+    t_alg1: float = 0.0
+    t_alg2: float = 0.0
+
+    @property
+    def total(self):
+        return self.u_sr + self.u_lr + self.u_self
+
+
+class EwaldSolver:
+    """Reusable Coulomb evaluator for one box and parameter set.
+
+    Owns a device handle (k-space plan and grow-only device buffers) so
+    repeated per-step evaluations pay no set-up cost.  Forces accumulate
+    into ps.force (ewald.py:599-605).
+    """
+
+    def __init__(self, box, params, workers=None, recip=None):
+        self.box = box
+        self.params = params
+        self.workers = workers
+        self.recip = enumerate_kvectors(box, params) if recip is None else recip
+        self.wide_cutoff = params.r_cutoff > box.max_cutoff()
+        self._h = _lib.Handle()
+        self._h.set_system(box.edge_length, params.alpha, params.r_cutoff)
+        self._h.set_kspace(self.recip.m_int, self.recip.coeff)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def evaluate(self, ps, cell_list=None):
+        """Accumulate Coulomb forces into ps.force; return EwaldEnergies."""
+        require_neutral(ps)
+        if self.wide_cutoff:
+            raise BoxTooSmallError(
+                f"r_cutoff {self.params.r_cutoff:.4g} exceeds L/2 = "
+                f"{self.box.max_cutoff():.4g}: the image-shell real-space "
+                f"path (ewald.py:553-576) is not provided on the device")
+        pos, q = _particles(ps)
+        f, copied = _force_buffer(ps)
+        rho = np.empty(2 * self.recip.n_stored)
+        en, tm = self._h.evaluate(pos, q, f, rho)
+        if copied:
+            ps.force[:] = f
+        self.recip.rho.values[:] = rho
+        return EwaldEnergies(float(en[0]), float(en[1]), float(en[2]),
+                             t_cell=float(tm[0]), t_sr=float(tm[1]),
+                             t_alg1=float(tm[2]), t_alg2=float(tm[3]))
+
+
+def total_coulomb(ps, params, rs=None, cell_list=None, workers=None):
+    """Full Ewald energy U = u_sr + u_lr + u_self; forces accumulate."""
+    solver = EwaldSolver(ps.box, params, workers=workers, recip=rs)
+    return solver.evaluate(ps, cell_list).total

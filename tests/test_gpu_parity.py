@@ -1,0 +1,296 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference's
+golden vectors and the oracle.
+
+Tolerances (BASELINE.json north_star): relative 1e-10 on u_sr, u_lr and
+u_self; max_i |F_i - F_i^ref| <= 1e-9 * F_rms.  rho_hat: the reference's own
+bound, 1e-12 * max|rho| (test_ewald.py:184-190).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import f_rms, golden, random_neutral, rel
+
+pytestmark = pytest.mark.gpu
+
+E_TOL = 1e-10
+F_TOL = 1e-9
+RHO_TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def ew():
+    import paper_1708_01135_b200 as ew
+    return ew
+
+
+@pytest.fixture(scope="module")
+def orc():
+    from oracle import oracle as orc
+    return orc
+
+
+def system(ew, pos, q, L):
+    box = ew.SimulationBox(L)
+    ps = ew.create_particle_set(pos.shape[0], box)
+    ps.position[:] = pos
+    ps.charge[:] = q
+    return box, ps
+
+
+def check_energies(res, u_sr, u_lr, u_self, scale=None):
+    scale = scale or max(abs(u_sr), abs(u_lr), abs(u_self))
+    for got, want, name in ((res.u_sr, u_sr, "u_sr"), (res.u_lr, u_lr, "u_lr"),
+                            (res.u_self, u_self, "u_self")):
+        err = abs(got - want) / (abs(want) if abs(want) > 1e-8 * scale else scale)
+        assert err <= E_TOL, f"{name}: {got!r} vs {want!r} (rel {err:.2e})"
+
+
+SMALL = ["rocksalt8", "rand32_s21", "rand64_s5", "rand200_s7", "rand600_s11",
+         "rand300_cube5"]
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_small_cases_match_reference_golden(ew, name):
+    g = golden(name)
+    box, ps = system(ew, g["pos"], g["q"], float(g["L"]))
+    params = ew.EwaldParams(float(g["alpha"]), float(g["r_cutoff"]),
+                            float(g["k_cutoff"]), float(g["tolerance"]))
+    rs = ew.ReciprocalSpace(box, params, g["m_int"])
+    res = ew.EwaldSolver(box, params, recip=rs).evaluate(ps)
+    check_energies(res, float(g["u_sr"]), float(g["u_lr"]), float(g["u_self"]))
+    F = g["force"]
+    assert np.abs(ps.force - F).max() <= F_TOL * f_rms(F)
+    assert np.abs(rs.rho.values - g["rho"]).max() <= RHO_TOL * np.abs(g["rho"]).max()
+
+
+def _config_run(ew, name):
+    from paper_1708_01135_b200 import workloads as wl
+    cfg = wl.make_config(name, seed=0)
+    box, ps = system(ew, cfg["pos"], cfg["q"], cfg["L"])
+    params = ew.EwaldParams(cfg["alpha_ref"], cfg["r_cutoff"],
+                            wl.k_cutoff_for(cfg), 1e-6)
+    rs = ew.ReciprocalSpace(box, params, cfg["m_int"])
+    solver = ew.EwaldSolver(box, params, recip=rs)
+    res = solver.evaluate(ps)
+    return cfg, ps, rs, res
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_configs_match_reference_golden(ew, name):
+    try:
+        g = golden(name)
+    except FileNotFoundError:
+        pytest.skip(f"no golden for {name}")
+    cfg, ps, rs, res = _config_run(ew, name)
+    check_energies(res, float(g["u_sr"]), float(g["u_lr"]), float(g["u_self"]))
+    fr = float(g["f_rms"])
+    idx = g["f_idx"]
+    assert np.abs(ps.force[idx] - g["f_sample"]).max() <= F_TOL * fr
+    K = rs.n_stored
+    k = g["k_idx"]
+    rmax = max(np.abs(g["rho_re_sample"]).max(), np.abs(g["rho_im_sample"]).max())
+    assert np.abs(rs.rho.values[k] - g["rho_re_sample"]).max() <= RHO_TOL * rmax * 10
+    assert np.abs(rs.rho.values[K + k] - g["rho_im_sample"]).max() <= RHO_TOL * rmax * 10
+    # size-independent properties: net force ~ 0 (momentum), F_rms agrees
+    assert abs(f_rms(ps.force) - fr) <= 1e-9 * fr
+    if "force" in g:
+        assert np.abs(ps.force - g["force"]).max() <= F_TOL * fr
+
+
+def test_c2_full_forces_vs_oracle(ew, orc):
+    cfg, ps, rs, res = _config_run(ew, "c2")
+    ref = orc.evaluate(cfg["pos"], cfg["q"], cfg["L"], cfg["alpha_ref"],
+                       cfg["r_cutoff"], cfg["m_int"], coeff=rs.coeff)
+    fr = f_rms(ref["force"])
+    assert np.abs(ps.force - ref["force"]).max() <= F_TOL * fr
+    assert np.abs(rs.rho.values - ref["rho"]).max() <= RHO_TOL * np.abs(ref["rho"]).max() * 10
+    check_energies(res, ref["u_sr"], ref["u_lr"], ref["u_self"])
+
+
+def test_rho_hat_alone(ew, orc):
+    pos, q = random_neutral(300, 11.0, seed=4)
+    box, ps = system(ew, pos, q, 11.0)
+    params = ew.choose_parameters(300, box, 1e-6)
+    rs = ew.enumerate_kvectors(box, params)
+    ew.compute_rho_hat(ps, rs)
+    ref = orc.rho_hat(pos, q, 11.0, rs.m_int)
+    assert np.abs(rs.rho.values - ref).max() <= RHO_TOL * np.abs(ref).max()
+
+
+def test_rho_single_charge_and_cancellation(ew):
+    box = ew.SimulationBox(8.0)
+    ps = ew.create_particle_set(1, box)
+    ps.charge[0] = 1.0
+    p = ew.EwaldParams(0.5, 4.0, 4.0, 1e-6)
+    rs = ew.enumerate_kvectors(box, p)
+    ew.compute_rho_hat(ps, rs)
+    np.testing.assert_allclose(rs.rho_complex, 1.0 + 0.0j, atol=1e-14)
+    ps2 = ew.create_particle_set(2, box)
+    ps2.charge[:] = (1.0, -1.0)
+    ps2.position[:] = 3.3
+    ew.compute_rho_hat(ps2, rs)
+    np.testing.assert_allclose(rs.rho_complex, 0.0, atol=1e-14)
+
+
+def test_long_range_alone_with_foreign_rho(ew, orc):
+    pos, q = random_neutral(200, 10.0, seed=8)
+    box, ps = system(ew, pos, q, 10.0)
+    params = ew.choose_parameters(200, box, 1e-5)
+    rs = ew.enumerate_kvectors(box, params)
+    rng = np.random.default_rng(3)
+    rs.rho.values[:] = rng.standard_normal(2 * rs.n_stored)
+    ps.force[:] = 1.5
+    u = ew.long_range_energy_forces(ps, rs)
+    f0 = np.full((200, 3), 1.5)
+    u_ref, f_ref = orc.long_range(pos, q, 10.0, rs.m_int, rs.coeff,
+                                  rs.rho.values, force=f0)
+    assert rel(u, u_ref) <= E_TOL
+    assert np.abs(ps.force - f_ref).max() <= F_TOL * f_rms(f_ref - 1.5)
+
+
+def test_single_charge_long_range_is_coeff_sum(ew):
+    box = ew.SimulationBox(8.0)
+    ps = ew.create_particle_set(1, box)
+    ps.charge[0] = 1.0
+    ps.position[0] = (1.1, 2.2, 3.3)
+    s = math.sqrt(-math.log(1e-6))
+    p = ew.EwaldParams(0.5, s / math.sqrt(0.5), 2 * s * math.sqrt(0.5), 1e-6)
+    rs = ew.enumerate_kvectors(box, p)
+    ew.compute_rho_hat(ps, rs)
+    u = ew.long_range_energy_forces(ps, rs)
+    assert u == pytest.approx(float(rs.coeff.sum()), rel=1e-12)
+
+
+def test_self_energy(ew):
+    box = ew.SimulationBox(10.0)
+    ps = ew.create_particle_set(2, box)
+    ps.charge[:] = (1.0, -1.0)
+    p = ew.EwaldParams(math.pi, 1.0, 1.0, 1e-6)
+    assert ew.self_energy(ps, p) == pytest.approx(-2.0, rel=1e-14)
+    ps.charge[:] = 0.0
+    assert ew.self_energy(ps, p) == 0.0
+
+
+def test_short_range_pair_closed_form(ew):
+    from scipy.special import erfc
+    box = ew.SimulationBox(20.0)
+    ps = ew.create_particle_set(2, box)
+    ps.charge[:] = (1.0, -1.0)
+    ps.position[1, 0] = 1.0
+    p = ew.EwaldParams(0.1, 6.0, 2.0, 0.1)
+    rs = ew.ReciprocalSpace(box, p, np.array([[1, 0, 0]]))
+    res = ew.EwaldSolver(box, p, recip=rs).evaluate(ps)
+    assert res.u_sr == pytest.approx(-erfc(math.sqrt(0.1)), rel=1e-12)
+
+
+def test_errors(ew):
+    box = ew.SimulationBox(10.0)
+    ps = ew.create_particle_set(2, box)
+    ps.charge[:] = 1.0
+    ps.position[1, 0] = 2.5
+    p = ew.choose_parameters(2, box, 1e-4)
+    with pytest.raises(ew.NeutralityError):
+        ew.total_coulomb(ps, p)
+    ps.charge[:] = (1.0, -1.0)
+    ps.position[1] = ps.position[0]
+    with pytest.raises(ew.CoincidentParticlesError):
+        ew.total_coulomb(ps, p)
+    ps.position[1] = (-0.5, 1.0, 1.0)
+    with pytest.raises(ValueError):
+        ew.total_coulomb(ps, p)
+    wide = ew.EwaldParams(0.01, 6.0, 2.0, 1e-3)
+    with pytest.raises(ew.BoxTooSmallError):
+        ps.position[1] = (5.0, 1.0, 1.0)
+        ew.EwaldSolver(box, wide).evaluate(ps)
+    with pytest.raises(ew.KSpaceEmptyError):
+        ew.enumerate_kvectors(box, ew.EwaldParams(1.0, 5.0, 0.5, 1e-6))
+
+
+def test_forces_accumulate(ew):
+    pos, q = random_neutral(16, 10.0, seed=30)
+    box, ps = system(ew, pos, q, 10.0)
+    p = ew.choose_parameters(16, box, 1e-4)
+    ew.total_coulomb(ps, p)
+    once = ps.force.copy()
+    ew.total_coulomb(ps, p)
+    np.testing.assert_allclose(ps.force, 2.0 * once, rtol=1e-12)
+
+
+@pytest.mark.parametrize("mcap", [1, 2, 5, 9, 32])
+def test_segment_lengths_and_permuted_table(ew, orc, mcap):
+    g = golden("c1")
+    box, ps = system(ew, g["pos"], g["q"], float(g["L"]))
+    from paper_1708_01135_b200 import workloads as wl
+    m = wl.cube_half_m(8)
+    perm = np.random.default_rng(mcap).permutation(m.shape[0])
+    m = m[perm]
+    params = ew.EwaldParams(float(g["alpha"]), float(g["r_cutoff"]), 9.0, 1e-6)
+    rs = ew.ReciprocalSpace(box, params, m)
+    solver = ew.EwaldSolver(box, params, recip=rs)
+    solver.handle.set_max_segment(mcap)
+    solver.handle.set_kspace(rs.m_int, rs.coeff)
+    res = solver.evaluate(ps)
+    check_energies(res, float(g["u_sr"]), float(g["u_lr"]), float(g["u_self"]))
+    K = m.shape[0]
+    rho_ref = np.concatenate([g["rho"][:K][perm], g["rho"][K:][perm]])
+    assert np.abs(rs.rho.values - rho_ref).max() <= RHO_TOL * np.abs(rho_ref).max()
+    assert np.abs(ps.force - g["force"]).max() <= F_TOL * f_rms(g["force"])
+
+
+def test_cutoff_predicate_exact_on_lattice(ew, orc):
+    # simple cubic lattice: many pairs at exactly r = r_c (excluded, strict <)
+    side, a = 8, 1.0
+    idx = np.arange(side)
+    ix, iy, iz = np.meshgrid(idx, idx, idx, indexing="ij")
+    pos = np.stack([ix.ravel(), iy.ravel(), iz.ravel()], axis=1) * a
+    q = np.where((ix + iy + iz).ravel() % 2 == 0, 1.0, -1.0)
+    for rc in (2.0, math.sqrt(5.0), 3.0, 4.0):
+        box, ps = system(ew, pos, q, side * a)
+        p = ew.EwaldParams(0.6, rc, 3.0, 1e-3)
+        rs = ew.ReciprocalSpace(box, p, np.array([[1, 0, 0], [0, 1, 0]]))
+        res = ew.EwaldSolver(box, p, recip=rs).evaluate(ps)
+        u_ref, f_ref = orc.short_range(pos, q, side * a, rc, 0.6)
+        assert rel(res.u_sr, u_ref) <= E_TOL
+
+
+def test_device_stages_sharded_match_full(ew):
+    """Two logical particle shards / cell slabs on one GPU reproduce the
+    single-shard evaluation (the multi-GPU data flow minus the collective)."""
+    torch = pytest.importorskip("torch")
+    from paper_1708_01135_b200 import _lib
+    from paper_1708_01135_b200 import workloads as wl
+    cfg = wl.make_config("c2", seed=0)
+    dev = torch.device("cuda", 0)
+    pos = torch.from_numpy(cfg["pos"]).to(dev)
+    q = torch.from_numpy(cfg["q"]).to(dev)
+    n = q.shape[0]
+    h = _lib.Handle(0)
+    h.set_stream(torch.cuda.current_stream().cuda_stream)
+    params = ew.EwaldParams(cfg["alpha_ref"], cfg["r_cutoff"], 10.0, 1e-6)
+    rs = ew.ReciprocalSpace(cfg["box"], params, cfg["m_int"])
+    h.set_system(cfg["L"], params.alpha, params.r_cutoff)
+    h.set_kspace(rs.m_int, rs.coeff)
+    f_full = torch.zeros((n, 3), dtype=torch.float64, device=dev)
+    en, _ = h.dev_evaluate(pos.data_ptr(), q.data_ptr(), n, f_full.data_ptr())
+    h.dev_load(pos.data_ptr(), q.data_ptr(), n)
+    ns = h.dev_slot_doubles()
+    s_a = torch.empty(ns, dtype=torch.float64, device=dev)
+    s_b = torch.empty(ns, dtype=torch.float64, device=dev)
+    h.dev_rho_partial(0, n // 3, s_a.data_ptr())
+    h.dev_rho_partial(n // 3, n, s_b.data_ptr())
+    s_a += s_b  # stands in for the all-reduce
+    u_lr = h.dev_kspace_finalize(s_a.data_ptr())
+    f = torch.zeros((n, 3), dtype=torch.float64, device=dev)
+    h.dev_recip_forces(0, n // 3, f.data_ptr())
+    h.dev_recip_forces(n // 3, n, f.data_ptr())
+    u_sr = h.dev_real_space(0, 2, f.data_ptr()) + h.dev_real_space(1, 2, f.data_ptr())
+    u_self = h.dev_self_energy()
+    torch.cuda.synchronize()
+    assert rel(u_lr, en[1]) <= 1e-12
+    assert rel(u_sr, en[0]) <= 1e-12
+    assert rel(u_self, en[2]) <= 1e-14
+    ff = f_full.cpu().numpy()
+    assert np.abs(f.cpu().numpy() - ff).max() <= 1e-12 * f_rms(ff)

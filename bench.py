@@ -1,0 +1,382 @@
+"""Benchmark: Ewald energy+force evaluations/s on BASELINE.json configs[1].
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2]
+                    [--impl ours|reference]
+
+One "step" = one full Ewald energy + force evaluation (real space, S(k),
+force gather, self energy) of the c2 workload: rock-salt 32^3 = 32,768
+charges, L=32, sigma=0.1 jitter (seed 0), beta=0.533 (alpha_ref=beta^2),
+r_c=6, cube |n_i|<=18 (25,326 half-space k-vectors).
+
+* value: evaluations/s with inputs resident in HBM (device pointers through
+  ewb_dev_evaluate); per step the L2 is flushed (256 MiB write) outside the
+  timed region, each step is timed with CUDA events on the library's stream
+  between barrier+synchronize, and the job time is the max over ranks.
+* e2e: the same metric through the reference-facing API
+  (EwaldSolver.evaluate on a ParticleSet whose arrays live in pinned host
+  memory), host<->device copies inside the timed region.
+* roofline: FP64-bound; the kernel with the largest share of the step is
+  reported against the FP64 DFMA peak measured on this device by
+  ewb_probe_fp64_peak (MEASURED_PEAKS.json has no FP64 figure).
+* cpu_baseline: the oracle (C restatement of the reference, OpenMP over all
+  host cores) on one full evaluation of the same config, rank 0 at N=1.
+
+N>1 (torchrun): particles are sharded across ranks, S(k) partials are
+combined by one NCCL all-reduce, real space is split by cell z-slabs; the
+total work is fixed (strong scaling).
+"""
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# algorithmic FP64 flops per particle.k pair of this formulation
+# (DESIGN.md section 4): K1 2 DFMA + 2 DADD = 6; K3 4 DFMA + 1 DADD = 9
+FLOPS_K1 = 6.0
+FLOPS_K3 = 9.0
+# FP64 pipe instructions per pair (K1 4, K3 5)
+INSTR_K1 = 4.0
+INSTR_K3 = 5.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-threads", type=int, default=0)
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index),
+                     f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
+                    capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for nm, v in zip(names, s[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+def setup_dist(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world, device):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t[0])
+
+
+def workload_desc(cfg):
+    return {
+        "workload": f"{cfg['name']}: " + (
+            f"rock-salt {cfg['side']}^3 = {cfg['pos'].shape[0]} charges, L={cfg['L']:g}, "
+            f"jitter sigma={cfg['sigma']}" if cfg["kind"] == "rocksalt" else
+            f"hard-core gas N={cfg['pos'].shape[0]}, L={cfg['L']:g}"),
+        "n_particles": int(cfg["pos"].shape[0]),
+        "k_half": int(cfg["m_int"].shape[0]),
+        "beta_cfg": cfg["alpha_cfg"], "alpha_ref": cfg["alpha_ref"],
+        "r_cutoff": cfg["r_cutoff"], "n_max": cfg["n_max"],
+        "kset": "cube |n_i|<=n_max, half space",
+        "seed": cfg["seed"],
+        "l2": "flushed (256 MiB write) before every timed step",
+    }
+
+
+def cpu_reference(cfg, steps, warmup, threads):
+    """The oracle port on host cores: one full evaluation per step."""
+    from oracle import oracle as orc
+    coeff = orc.kspace_coeff(cfg["m_int"], cfg["L"], cfg["alpha_ref"])
+    times = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        orc.evaluate(cfg["pos"], cfg["q"], cfg["L"], cfg["alpha_ref"],
+                     cfg["r_cutoff"], cfg["m_int"], coeff=coeff,
+                     threads=threads)
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            times.append(dt)
+    return times
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import oracle as orc
+    from paper_1708_01135_b200 import workloads as wl
+    cfg = wl.make_config(args.config, seed=0)
+    threads = args.cpu_threads or orc.host_threads()
+    steps = max(1, args.steps)
+    warm = max(0, min(args.warmup, 1))
+    times = cpu_reference(cfg, steps, warm, threads)
+    t = float(np.sum(times))
+    value = steps / t
+    line = {
+        "metric": "ewald_energy_force_evals_per_s", "value": value,
+        "unit": "evals/s", "impl": "reference", "n_gpus": world,
+        "steps": steps, "warmup": warm, "ms_per_step": 1e3 * t / steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded, BASELINE.json config)",
+        "config": workload_desc(cfg),
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads,
+                         "kind": "port",
+                         "sample": f"{steps} full evaluation(s) of "
+                                   f"{args.config} (oracle C port, OpenMP)"},
+        "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def flush_l2(buf):
+    buf.add_(1.0)
+
+
+def run_ours(args):
+    import torch
+    world, rank, local = setup_dist(args)
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    import paper_1708_01135_b200 as ew
+    from paper_1708_01135_b200 import _lib
+    from paper_1708_01135_b200 import workloads as wl
+    from paper_1708_01135_b200.distributed import DeviceStages, ShardedEwald
+
+    cfg = wl.make_config(args.config, seed=0)
+    n = cfg["pos"].shape[0]
+    params = ew.EwaldParams(cfg["alpha_ref"], cfg["r_cutoff"],
+                            wl.k_cutoff_for(cfg), 1e-6)
+    rs = ew.ReciprocalSpace(cfg["box"], params, cfg["m_int"])
+    K = rs.n_stored
+
+    h = _lib.Handle(local)
+    stream = torch.cuda.Stream(device=dev)
+    h.set_stream(stream.cuda_stream)
+    h.set_system(cfg["L"], params.alpha, params.r_cutoff)
+    h.set_kspace(rs.m_int, rs.coeff)
+    fp64_peak = h.probe_fp64_peak()
+
+    pos_d = torch.from_numpy(cfg["pos"]).to(dev)
+    q_d = torch.from_numpy(cfg["q"]).to(dev)
+    f_d = torch.zeros((n, 3), dtype=torch.float64, device=dev)
+    l2 = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    sharded = ShardedEwald(DeviceStages(h), dev) if world > 1 else None
+
+    def step():
+        if sharded is not None:
+            with torch.cuda.stream(stream):
+                return sharded.evaluate(pos_d, q_d, f_d), None
+        en, tm = h.dev_evaluate(pos_d.data_ptr(), q_d.data_ptr(), n,
+                                f_d.data_ptr(), None, timings=True)
+        return en, tm
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    launches0 = h.launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    total_ms = 0.0
+    stage = np.zeros(4)
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush_l2(l2)
+            barrier(world)
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            en, tm = step()
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            barrier(world)
+            total_ms += ev0.elapsed_time(ev1)
+            if tm is not None:
+                stage += tm
+    launches = h.launch_count() - launches0
+    total_s = max_over_ranks(total_ms * 1e-3, world, dev)
+    value = args.steps / total_s
+    clocks = clk.summary()
+
+    # ---- e2e through the reference-facing API (host buffers) ----
+    e2e = None
+    if world == 1:
+        box = cfg["box"]
+        ps = ew.create_particle_set(n, box)
+        ps.position = torch.from_numpy(cfg["pos"]).pin_memory().numpy()
+        ps.charge = torch.from_numpy(cfg["q"]).pin_memory().numpy()
+        ps.force = torch.zeros((n, 3), dtype=torch.float64).pin_memory().numpy()
+        solver = ew.EwaldSolver(box, params, recip=rs)
+        for _ in range(max(3, args.warmup)):
+            solver.evaluate(ps)
+        t_e2e = 0.0
+        for _ in range(args.steps):
+            flush_l2(l2)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            solver.evaluate(ps)
+            t_e2e += time.perf_counter() - t0
+        e2e = {"value": args.steps / t_e2e, "unit": "evals/s",
+               "h2d_bytes_per_step": int(n * (24 + 8 + 24)),
+               "d2h_bytes_per_step": int(n * 24 + 16 * K + 3 * 8 + 4),
+               "path": "EwaldSolver.evaluate (ctypes -> ewb_evaluate), pinned host arrays"}
+
+    # ---- roofline of the dominant kernel (single GPU stage times) ----
+    roof = None
+    pairs = float(n) * K
+    if world == 1 and args.steps > 0:
+        mean = stage / args.steps
+        t_real = mean[1]
+        t_k1 = mean[2]
+        t_k3 = mean[3]
+        cands = {"k6_real_space": t_real, "k1_structure_factor": t_k1,
+                 "k3_force_gather": t_k3}
+        dom = max(cands, key=cands.get)
+        if dom == "k6_real_space":
+            # report the reciprocal pair throughput too; real space roofline
+            # uses the same FP64 denominator with pair-evaluation flops
+            pass
+        k_flops = {"k1_structure_factor": FLOPS_K1 * pairs,
+                   "k3_force_gather": FLOPS_K3 * pairs}
+        k_instr = {"k1_structure_factor": INSTR_K1 * pairs,
+                   "k3_force_gather": INSTR_K3 * pairs}
+        recip_dom = max(("k1_structure_factor", "k3_force_gather"),
+                        key=lambda k: cands[k])
+        ach = k_flops[recip_dom] / cands[recip_dom] / 1e12
+        sm_peak_instr = fp64_peak / 2.0  # DFMA: 2 flops per pipe slot
+        roof = {
+            "bound": "fp64", "kernel": recip_dom,
+            "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
+            "frac": ach / fp64_peak,
+            "fp64_pipe_frac": k_instr[recip_dom] / cands[recip_dom] / 1e12 / sm_peak_instr,
+            "peak_source": "measured (ewb_probe_fp64_peak, DFMA chains, this run)",
+            "traffic": None,
+            "step_share": {k: v / float(mean[1] + mean[2] + mean[3]) for k, v in cands.items()},
+            "dominant_kernel_of_step": dom,
+            "stage_ms": {"t_cell": 1e3 * mean[0], "t_sr": 1e3 * mean[1],
+                         "t_alg1": 1e3 * mean[2], "t_alg2": 1e3 * mean[3]},
+            "pairs_per_s": pairs / (mean[2] + mean[3]),
+            "flops_per_pair": {"k1": FLOPS_K1, "k3": FLOPS_K3,
+                               "survey_convention": 22.0},
+        }
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import oracle as orc
+        threads = args.cpu_threads or orc.host_threads()
+        times = cpu_reference(cfg, 1, 0, threads)
+        cpu = {"value": 1.0 / times[0], "unit": "evals/s", "cores": threads,
+               "kind": "port",
+               "sample": f"1 full evaluation of {args.config} on the host "
+                         f"(oracle C port, OpenMP, {threads} threads)"}
+
+    if rank == 0:
+        line = {
+            "metric": "ewald_energy_force_evals_per_s", "value": value,
+            "unit": "evals/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": 1e3 * total_s / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded, BASELINE.json config)",
+            "config": dict(workload_desc(cfg),
+                           parallelism=f"particle-shard x{world} + S(k) allreduce"
+                           if world > 1 else "single GPU"),
+            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
+            "gpu_launches": int(launches), "clocks": clocks,
+            "energies": [float(x) for x in en],
+            "fp64_peak_tflops_measured": fp64_peak,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -117,6 +117,9 @@ int ewb_dev_self_energy(ewb_handle *h, double *u_self);
 int ewb_dev_evaluate(ewb_handle *h, const double *d_pos, const double *d_q,
                      int64_t n, double *d_force, double *d_rho_out,
                      double *energies, double *timings);
+/* Sustained FP64 DFMA throughput of this device (TFLOP/s), measured with
+ * independent fma chains; the FP64 roofline denominator. */
+int ewb_probe_fp64_peak(ewb_handle *h, double *tflops);
 /* Kernels launched by this handle since creation (evidence counter). */
 int64_t ewb_launch_count(const ewb_handle *h);
 

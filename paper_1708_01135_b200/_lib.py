@@ -57,6 +57,7 @@ SIGNATURES = {
     "ewb_dev_real_space": (_INT, [_P, _INT, _INT, _P, _P]),
     "ewb_dev_self_energy": (_INT, [_P, _P]),
     "ewb_dev_evaluate": (_INT, [_P, _P, _P, _I64, _P, _P, _P, _P]),
+    "ewb_probe_fp64_peak": (_INT, [_P, _P]),
     "ewb_launch_count": (_I64, [_P]),
 }
 
@@ -177,6 +178,11 @@ class Handle:
 
     def set_stream(self, stream_ptr):
         self._check(self.lib.ewb_set_stream(self.h, int(stream_ptr)))
+
+    def probe_fp64_peak(self):
+        out = ctypes.c_double(0.0)
+        self._check(self.lib.ewb_probe_fp64_peak(self.h, ctypes.byref(out)))
+        return out.value
 
     def launch_count(self):
         return int(self.lib.ewb_launch_count(self.h))

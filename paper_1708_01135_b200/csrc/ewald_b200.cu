@@ -728,7 +728,9 @@ __global__ void __launch_bounds__(K6_WARPS * 32)
             ++tail;
           }
         }
-        while (__all_sync(0xffffffffu, !valid || tail - head > 0)) eval_one();
+        while (__all_sync(0xffffffffu, !valid || tail - head > 0)) {
+          if (tail - head > 0) eval_one();
+        }
         while (__any_sync(0xffffffffu, tail - head > QCAP - 32)) {
           if (tail - head > 0) eval_one();
         }
@@ -767,6 +769,23 @@ __global__ void __launch_bounds__(RED_THREADS) k7_sum_q2(const double4 *__restri
   }
   const double b = block_sum<RED_THREADS>(a, sh);
   if (threadIdx.x == 0) eblk[blockIdx.x] = b;
+}
+
+// FP64 peak probe: independent DFMA chains (2 flops each), for the roofline
+// denominator (MEASURED_PEAKS.json carries no FP64 figure).
+__global__ void __launch_bounds__(256) k_fp64_probe(double *__restrict__ out, int iters, double a,
+                                                    double b) {
+  double x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-9 + k;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = fma(x[k], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k];
+  if (s == 1.2345) out[0] = s;  // keep the chains alive
 }
 
 // ---------------------------------------------------------------------------
@@ -1681,6 +1700,29 @@ int ewb_dev_evaluate(ewb_handle *h, const double *d_pos, const double *d_q, int6
   if ((rc = check_errflag(h, ERR_UNWRAPPED | ERR_COINCIDENT))) return rc;
   if (energies) std::memcpy(energies, en, sizeof en);
   return read_timings(h, timings);
+}
+
+int ewb_probe_fp64_peak(ewb_handle *h, double *tflops) {
+  if (!h || !tflops) return EWB_EINVAL;
+  CK(cudaSetDevice(h->device));
+  CK(h->eblk2.ensure(64));
+  const int iters = 4096;
+  const unsigned blocks = (unsigned)h->n_sm * 8;
+  k_fp64_probe<<<blocks, 256, 0, h->stream>>>(h->eblk2.as<double>(), iters, 0.999999, 1e-7);
+  CKL();
+  CK(cudaEventRecord(h->ev[0], h->stream));
+  const int reps = 5;
+  for (int r = 0; r < reps; ++r) {
+    k_fp64_probe<<<blocks, 256, 0, h->stream>>>(h->eblk2.as<double>(), iters, 0.999999, 1e-7);
+    CKL();
+  }
+  CK(cudaEventRecord(h->ev[1], h->stream));
+  CK(cudaEventSynchronize(h->ev[1]));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]));
+  const double flops = 2.0 * 8.0 * iters * 256.0 * blocks * reps;
+  *tflops = flops / (ms * 1e-3) / 1e12;
+  return EWB_OK;
 }
 
 int64_t ewb_launch_count(const ewb_handle *h) { return h ? h->launches : -1; }

@@ -62,7 +62,10 @@ def test_small_cases_match_reference_golden(ew, name):
     res = ew.EwaldSolver(box, params, recip=rs).evaluate(ps)
     check_energies(res, float(g["u_sr"]), float(g["u_lr"]), float(g["u_self"]))
     F = g["force"]
-    assert np.abs(ps.force - F).max() <= F_TOL * f_rms(F)
+    # perfect lattices have F == 0 by symmetry: floor the scale at |U|/L
+    u_tot = abs(float(g["u_sr"]) + float(g["u_lr"]) + float(g["u_self"]))
+    scale = max(f_rms(F), 1e-6 * u_tot / float(g["L"]))
+    assert np.abs(ps.force - F).max() <= F_TOL * scale
     assert np.abs(rs.rho.values - g["rho"]).max() <= RHO_TOL * np.abs(g["rho"]).max()
 
 

@@ -53,7 +53,7 @@ constexpr int K3_THREADS = 128;
 constexpr int K3_PPT = 2;         // particles per thread in the gather
 constexpr int K3_CH = 32;         // k-items per shared-memory chunk
 constexpr int K6_WARPS = 4;
-constexpr int QCAP = 64;          // per-lane pair queue (power of two)
+constexpr int K6_G = 8;           // centre particles per real-space warp
 constexpr int SORT_CAP = 4096;    // in-cell deterministic sort capacity
 constexpr int RED_THREADS = 256;
 
@@ -232,8 +232,19 @@ __global__ void __launch_bounds__(RED_THREADS)
   double e = 0.0;
   if (s < n_slots) {
     double2 S = make_double2(0.0, 0.0);
-    for (int pc = 0; pc < n_part; ++pc) {
-      const double2 v = spart[(size_t)pc * n_slots + s];
+    int pc = 0;
+    for (; pc + 8 <= n_part; pc += 8) {  // 8 independent loads in flight
+      double2 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcs(spart + (size_t)(pc + u) * n_slots + s);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        S.x += v[u].x;
+        S.y += v[u].y;
+      }
+    }
+    for (; pc < n_part; ++pc) {
+      const double2 v = __ldcs(spart + (size_t)pc * n_slots + s);
       S.x += v.x;
       S.y += v.y;
     }
@@ -432,11 +443,12 @@ __global__ void __launch_bounds__(RED_THREADS)
   double e = 0.0;
   if (i < n_local) {
     double fx = 0.0, fy = 0.0, fz = 0.0, u = 0.0;
+#pragma unroll 4
     for (int ks = 0; ks < n_ks; ++ks) {
       const double *fp = fpart + (size_t)ks * 3 * n_local;
-      fx += fp[i];
-      fy += fp[n_local + i];
-      fz += fp[2 * n_local + i];
+      fx += __ldcs(fp + i);
+      fy += __ldcs(fp + n_local + i);
+      fz += __ldcs(fp + 2 * n_local + i);
       if (energy) u += upart[(size_t)ks * n_local + i];
     }
     const int64_t g = p_begin + i;
@@ -477,7 +489,7 @@ __global__ void k4_bin_count(const double4 *__restrict__ xyzq, int64_t n, double
   slot[i] = atomicAdd(count + c, 1);
 }
 
-// Single-block exclusive scans of cell counts (start) and 32-groups (gstart).
+// Single-block exclusive scans of cell counts (start) and K6_G-groups (gstart).
 __global__ void __launch_bounds__(1024) k_scan_cells(const int *__restrict__ count, int n_cells,
                                                      int *__restrict__ start,
                                                      int *__restrict__ gstart) {
@@ -489,7 +501,7 @@ __global__ void __launch_bounds__(1024) k_scan_cells(const int *__restrict__ cou
   for (int base = 0; base < n_cells; base += 1024) {
     const int c = base + threadIdx.x;
     const int a = c < n_cells ? count[c] : 0;
-    const int b = (a + 31) >> 5;
+    const int b = (a + K6_G - 1) / K6_G;
     int ia = a, ib = b;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -579,6 +591,42 @@ __global__ void k5_gather(const int *__restrict__ order, const double4 *__restri
   sorted[p] = xyzq[order[p]];
 }
 
+// erfcx(x) = exp(x^2) erfc(x) on [0, 6): 12 intervals of width 1/2, degree-12
+// polynomial in t = 4x - (2i+1), generated by tools/gen_erfcx_table.py.
+// max relative error of the double-precision Horner: 8.88e-16
+__constant__ double c_erfcx_tab[12][13] = {
+    {0.7703465477309968, -0.18580147330749627, 0.03653406715146768, -0.0062194752567052616, 0.0009473309967357329, -0.00013180360486534726, 1.699015381892417e-05, -2.0502458027178e-06, 2.334366455001955e-07, -2.5224113349396268e-08, 2.601714124857212e-09, -2.645535522720767e-10, 2.5084180598363034e-11},
+    {0.5069376502931449, -0.09199317291394817, 0.014434883221956088, -0.0020286884686890566, 0.0002609005567498488, -3.1149669808397036e-05, 3.4885738807897664e-06, -3.693567406943463e-07, 3.719543629447327e-08, -3.579272112111564e-09, 3.3061733705972456e-10, -3.010096125292678e-11, 2.581271691748106e-12},
+    {0.3678229164523611, -0.05220546899115238, 0.006674723218537419, -0.0007846605374382521, 8.598189160507216e-05, -8.868776967725166e-06, 8.674584711778801e-07, -8.09194284279868e-08, 7.232217406690809e-09, -6.215429959552571e-10, 5.154261278261677e-11, -4.214961825526736e-12, 3.2747182507155396e-13},
+    {0.2849722347374364, -0.03274408637862129, 0.0034852268804429535, -0.0003478124256469985, 3.2829371903648855e-05, -2.950170555585948e-06, 2.537120414482415e-07, -2.096762028769442e-08, 1.670918660864194e-09, -1.2875251113676387e-10, 9.61847389834657e-12, -7.092030933689514e-13, 5.0048417345007894e-14},
+    {0.23108725873039188, -0.022121625702187286, 0.0019995392131691415, -0.00017190719931942612, 1.4136700602964347e-05, -1.1169223469151147e-06, 8.509165574807611e-08, -6.269598619463966e-09, 4.478950947622092e-10, -3.108856441414792e-11, 2.10082401649295e-12, -1.402683891597517e-13, 9.019823445765036e-15},
+    {0.1936620962790687, -0.01580940939015871, 0.001234912061707679, -9.272402964060302e-05, 6.717116739411538e-06, -4.708936375997823e-07, 3.202680676576849e-08, -2.117835321201201e-09, 1.3641597025404525e-10, -8.572609778060283e-12, 5.263802979021472e-13, -3.1971258939165315e-14, 1.8800738604690586e-15},
+    {0.16633534842682188, -0.011799850580292594, 0.0008085806801886348, -5.367923907668294e-05, 3.4609553809933582e-06, -2.1717047807742037e-07, 1.3286232619299866e-08, -7.937403081265358e-10, 4.636889929605563e-11, -2.651912467909991e-12, 1.4865485154109668e-13, -8.251888719805715e-15, 4.454562117727668e-16},
+    {0.14558972127503855, -0.009114064383180883, 0.0005549222204578311, -3.292629484639286e-05, 1.907118680060835e-06, -1.0798786613289054e-07, 5.985430999920972e-09, -3.251143200862901e-10, 1.732369459208254e-11, -9.063500898261399e-13, 4.659999514606456e-14, -2.3750846277556673e-15, 1.1815817873651303e-16},
+    {0.12934527478598792, -0.007236082853653833, 0.00039574164211704684, -2.1186455736001674e-05, 1.1116217064069037e-06, -5.722216817598962e-08, 2.8926009873682308e-09, -1.4371342152607251e-10, 7.023014024445707e-12, -3.3780170712636556e-13, 1.6003168989041294e-14, -7.522483388703235e-16, 3.462294803041272e-17},
+    {0.11630270721024731, -0.005875862149540788, 0.00029133289806077125, -1.4189045266088957e-05, 6.794074376588104e-07, -3.200759876395623e-08, 1.4846471070136548e-09, -6.784471061780229e-11, 3.056212968617432e-12, -1.3578510096466765e-13, 5.953169824807012e-15, -2.591907760108697e-16, 1.1078471622899968e-17},
+    {0.1056127354688918, -0.004861361168037162, 0.0002202594337569623, -9.829710797539752e-06, 4.323595940196192e-07, -1.8753983078086295e-08, 8.026239453614756e-10, -3.390857582363441e-11, 1.4147478393182942e-12, -5.831704153025278e-14, 2.3759395644914543e-15, -9.619931371665538e-17, 3.832315492243951e-18},
+    {0.09669877816971392, -0.004085804535950621, 0.00017032961517810219, -7.009307785594627e-06, 2.8486050341955844e-07, -1.1437905173582296e-08, 4.5393092554672476e-10, -1.7812390949431116e-11, 6.913427648222772e-13, -2.6548500183324395e-14, 1.0090217232526848e-15, -3.813643120173001e-17, 1.4208519269427467e-18},
+};
+
+constexpr int ERFCX_NI = 12;
+constexpr int ERFCX_NC = 13;
+
+// erfc(x) given e = exp(-x^2) (which the force needs anyway); the table lives
+// in shared memory (lanes index different intervals).
+__device__ __forceinline__ double erfc_from_exp(double x, double e, const double *tab) {
+  if (x < 0.5 * ERFCX_NI) {
+    const int i = (int)(x * 2.0);
+    const double t = fma(4.0, x, -(double)(2 * i + 1));
+    const double *c = tab + i * ERFCX_NC;
+    double r = c[ERFCX_NC - 1];
+#pragma unroll
+    for (int k = ERFCX_NC - 2; k >= 0; --k) r = fma(r, t, c[k]);
+    return r * e;
+  }
+  return erfc(x);
+}
+
 // K6: ordered-pair real-space kernel.  One warp = up to 32 centre particles of
 // one home cell (lanes), candidates broadcast from shared memory; accepted
 // pairs go to a per-lane queue and are evaluated in converged rounds.
@@ -642,60 +690,88 @@ __device__ __forceinline__ double rs_r2(double dx, double dy, double dz) {
 template <bool FOLD>
 __global__ void __launch_bounds__(K6_WARPS * 32)
     k6_real_space(const double4 *__restrict__ sorted, const int *__restrict__ order,
-                  const int *__restrict__ cell_start, const int *__restrict__ gstart, RSParams P,
+                  const int *__restrict__ cell_start, const int *__restrict__ ustart, RSParams P,
                   double *__restrict__ force, double *__restrict__ eblk, int *__restrict__ err) {
-  __shared__ uint32_t qbuf[K6_WARPS][QCAP][32];
-  __shared__ double4 stage[K6_WARPS][32];
+  // One warp = up to K6_G centre particles i of one home cell.  Lanes walk
+  // the stencil's candidates j (coalesced double4 loads), test every centre
+  // with the reference's exact predicate, and append accepted j to the
+  // centre's pair list (ballot compaction).  A list with >= 32 pairs is
+  // evaluated in one converged round: lane l computes pair (i_g, j_l) and
+  // accumulates into its private slot of F_g (shared memory); the 32 slots
+  // are summed at the end.  erfc/exp run on a partially active warp only in
+  // the final round of each centre, and exist once in the instruction
+  // stream (the test loop is unrolled over centres, the evaluation is not).
+  __shared__ double4 s_i[K6_WARPS][K6_G];
+  __shared__ uint32_t s_list[K6_WARPS][K6_G][64];
+  __shared__ double3 s_f[K6_WARPS][K6_G][32];
   __shared__ double sh[K6_WARPS];
+  __shared__ double s_erfcx[ERFCX_NI * ERFCX_NC];
+  for (int t = threadIdx.x; t < ERFCX_NI * ERFCX_NC; t += K6_WARPS * 32)
+    s_erfcx[t] = c_erfcx_tab[t / ERFCX_NC][t % ERFCX_NC];
+  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int u_lo = gstart[P.c_lo], u_hi = gstart[P.c_hi];
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const int u_lo = ustart[P.c_lo], u_hi = ustart[P.c_hi];
   const int u = u_lo + blockIdx.x * K6_WARPS + warp;
   double ue = 0.0;
   if (u < u_hi) {
     int lo = P.c_lo, hi = P.c_hi - 1;
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
-      if (gstart[mid] <= u)
+      if (ustart[mid] <= u)
         lo = mid;
       else
         hi = mid - 1;
     }
     const int c = lo;
     const int cs = cell_start[c], ce = cell_start[c + 1];
-    const int i = cs + 32 * (u - gstart[c]) + lane;
-    const bool valid = i < ce;
-    const double4 pi = sorted[valid ? i : cs];
-    double fx = 0.0, fy = 0.0, fz = 0.0;
-    int head = 0, tail = 0;
+    const int first = cs + K6_G * (u - ustart[c]);
+    const int gi = min(K6_G, ce - first);
+    if (lane < gi) s_i[warp][lane] = sorted[first + lane];
+#pragma unroll
+    for (int g = 0; g < K6_G; ++g) s_f[warp][g][lane] = make_double3(0.0, 0.0, 0.0);
+    __syncwarp();
+    int cnt[K6_G];
+#pragma unroll
+    for (int g = 0; g < K6_G; ++g) cnt[g] = 0;
     bool coincident = false;
 
-    auto eval_one = [&]() {
-      const uint32_t code = qbuf[warp][head & (QCAP - 1)][lane];
-      ++head;
-      const int j = (int)(code & 0x7FFFFFFu);
-      const int s = (int)(code >> 27);
-      const double4 pj = sorted[j];
-      double sx = 0.0, sy = 0.0, sz = 0.0;
-      if (!FOLD) {
-        int nc;
-        rs_shift(c, s, P.cpd, P.L, sx, sy, sz, nc);
+    // evaluate the first n (<= 32) entries of list g: lane l takes entry l
+    auto round = [&](const int g, const int n) {
+      if (lane < n) {
+        const uint32_t code = s_list[warp][g][lane];
+        const int j = (int)(code & 0x7FFFFFFu);
+        const int sc_id = (int)(code >> 27);
+        const double4 pj = sorted[j];
+        const double4 pi = s_i[warp][g];
+        double sx = 0.0, sy = 0.0, sz = 0.0;
+        if (!FOLD) {
+          int nc;
+          rs_shift(c, sc_id, P.cpd, P.L, sx, sy, sz, nc);
+        }
+        const double dx = rs_disp<FOLD>(pi.x, pj.x, sx, P.hl, P.L);
+        const double dy = rs_disp<FOLD>(pi.y, pj.y, sy, P.hl, P.L);
+        const double dz = rs_disp<FOLD>(pi.z, pj.z, sz, P.hl, P.L);
+        const double r2 = rs_r2(dx, dy, dz);
+        if (r2 == 0.0) {
+          coincident = true;
+        } else {
+          // sc = erfc(sqrt(alpha) r)/r, g = qq (sc + 2 sqrt(alpha/pi) e^{-alpha r^2})/r^2
+          // (ewald.py:214-218), with one exp shared by erfc and the force
+          const double qq = pi.w * pj.w;
+          const double inv_r = rsqrt(r2);
+          const double r = r2 * inv_r;
+          const double e = exp(-P.al * r2);
+          const double sc = erfc_from_exp(P.sa * r, e, s_erfcx) * inv_r;
+          ue += 0.5 * qq * sc;
+          const double gg = qq * fma(P.tsap, e, sc) * (inv_r * inv_r);
+          double3 f = s_f[warp][g][lane];
+          f.x = fma(gg, dx, f.x);
+          f.y = fma(gg, dy, f.y);
+          f.z = fma(gg, dz, f.z);
+          s_f[warp][g][lane] = f;
+        }
       }
-      const double dx = rs_disp<FOLD>(pi.x, pj.x, sx, P.hl, P.L);
-      const double dy = rs_disp<FOLD>(pi.y, pj.y, sy, P.hl, P.L);
-      const double dz = rs_disp<FOLD>(pi.z, pj.z, sz, P.hl, P.L);
-      const double r2 = rs_r2(dx, dy, dz);
-      if (r2 == 0.0) {
-        coincident = true;
-        return;
-      }
-      const double qq = pi.w * pj.w;
-      const double r = sqrt(r2);
-      const double sc = erfc(P.sa * r) / r;
-      ue += 0.5 * qq * sc;
-      const double g = qq * (sc + P.tsap * exp(-P.al * r2)) / r2;
-      fx = fma(g, dx, fx);
-      fy = fma(g, dy, fy);
-      fz = fma(g, dz, fz);
     };
 
     const int nst = FOLD ? 1 : 27;
@@ -711,40 +787,81 @@ __global__ void __launch_bounds__(K6_WARPS * 32)
         jb = cell_start[nc];
         je = cell_start[nc + 1];
       }
+      const bool shifted = (sx != 0.0) || (sy != 0.0) || (sz != 0.0);
       for (int j0 = jb; j0 < je; j0 += 32) {
-        const int nb = min(32, je - j0);
-        __syncwarp();
-        if (lane < nb) stage[warp][lane] = sorted[j0 + lane];
-        __syncwarp();
-        for (int t = 0; t < nb; ++t) {
-          const double4 pj = stage[warp][t];
-          const double dx = rs_disp<FOLD>(pi.x, pj.x, sx, P.hl, P.L);
-          const double dy = rs_disp<FOLD>(pi.y, pj.y, sy, P.hl, P.L);
-          const double dz = rs_disp<FOLD>(pi.z, pj.z, sz, P.hl, P.L);
-          const double r2 = rs_r2(dx, dy, dz);
-          const int j = j0 + t;
-          if (valid && r2 < P.rc2 && j != i) {
-            qbuf[warp][tail & (QCAP - 1)][lane] = (uint32_t)j | ((uint32_t)s << 27);
-            ++tail;
+        const int j = j0 + lane;
+        const bool vj = j < je;
+        const double4 pj = sorted[vj ? j : jb];
+        int full = 0;  // bit g: list g holds >= 32 pairs
+#pragma unroll
+        for (int g = 0; g < K6_G; ++g) {
+          if (g < gi) {
+            const double4 pi = s_i[warp][g];
+            double dx, dy, dz;
+            if (FOLD) {
+              dx = rs_disp<true>(pi.x, pj.x, 0.0, P.hl, P.L);
+              dy = rs_disp<true>(pi.y, pj.y, 0.0, P.hl, P.L);
+              dz = rs_disp<true>(pi.z, pj.z, 0.0, P.hl, P.L);
+            } else if (!shifted) {
+              // fl(fl(xi-xj) + 0.0) == fl(xi-xj) up to the sign of zero, so
+              // r2 is bit-identical to the shifted recomputation in round()
+              dx = __dsub_rn(pi.x, pj.x);
+              dy = __dsub_rn(pi.y, pj.y);
+              dz = __dsub_rn(pi.z, pj.z);
+            } else {
+              dx = rs_disp<false>(pi.x, pj.x, sx, P.hl, P.L);
+              dy = rs_disp<false>(pi.y, pj.y, sy, P.hl, P.L);
+              dz = rs_disp<false>(pi.z, pj.z, sz, P.hl, P.L);
+            }
+            const double r2 = rs_r2(dx, dy, dz);
+            const bool acc = vj && (r2 < P.rc2) && (j != first + g);
+            const unsigned bal = __ballot_sync(0xffffffffu, acc);
+            if (acc)
+              s_list[warp][g][cnt[g] + __popc(bal & lt_mask)] = (uint32_t)j | ((uint32_t)s << 27);
+            cnt[g] += __popc(bal);
+            if (cnt[g] >= 32) full |= 1 << g;
           }
         }
-        while (__all_sync(0xffffffffu, !valid || tail - head > 0)) {
-          if (tail - head > 0) eval_one();
-        }
-        while (__any_sync(0xffffffffu, tail - head > QCAP - 32)) {
-          if (tail - head > 0) eval_one();
+        // converged evaluation rounds (one code copy, uniform g)
+        while (full) {
+          const int g = __ffs(full) - 1;
+          full &= full - 1;
+          int ng = 0;
+#pragma unroll
+          for (int t = 0; t < K6_G; ++t)
+            if (t == g) ng = cnt[t];
+          __syncwarp();
+          round(g, 32);
+          __syncwarp();
+          const int rest = ng - 32;
+          const uint32_t mv = lane < rest ? s_list[warp][g][32 + lane] : 0u;
+          __syncwarp();
+          if (lane < rest) s_list[warp][g][lane] = mv;
+#pragma unroll
+          for (int t = 0; t < K6_G; ++t)
+            if (t == g) cnt[t] = rest;
         }
       }
     }
-    while (__any_sync(0xffffffffu, tail > head)) {
-      if (tail > head) eval_one();
+    __syncwarp();
+    for (int g = 0; g < gi; ++g) {
+      int ng = 0;
+#pragma unroll
+      for (int t = 0; t < K6_G; ++t)
+        if (t == g) ng = cnt[t];
+      if (ng > 0) round(g, ng);
     }
     if (coincident) atomicOr(err, ERR_COINCIDENT);
-    if (valid) {
-      const int o = order[i];
-      force[3 * (int64_t)o] += fx;
-      force[3 * (int64_t)o + 1] += fy;
-      force[3 * (int64_t)o + 2] += fz;
+    __syncwarp();
+    for (int g = 0; g < gi; ++g) {
+      const double3 f = s_f[warp][g][lane];
+      const double ax = warp_sum(f.x), ay = warp_sum(f.y), az = warp_sum(f.z);
+      if (lane == 0) {
+        const int64_t o = order[first + g];
+        force[3 * o] += ax;
+        force[3 * o + 1] += ay;
+        force[3 * o + 2] += az;
+      }
     }
   }
   ue = warp_sum(ue);
@@ -1276,7 +1393,7 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
   rp.c_lo = zl * cpd_eff * cpd_eff;
   rp.c_hi = zh * cpd_eff * cpd_eff;
   const int64_t cells_slab = rp.c_hi - rp.c_lo;
-  const int64_t units_max = n / 32 + cells_slab + 1;
+  const int64_t units_max = n / K6_G + cells_slab + 1;
   const unsigned nb = (unsigned)std::max<int64_t>(1, (units_max + K6_WARPS - 1) / K6_WARPS);
   CK(h->eblk.ensure(nb * sizeof(double)));
   if (cells_slab <= 0) {

@@ -63,6 +63,10 @@ int ewb_set_stream(ewb_handle *h, uintptr_t stream);
 /* tuning knob: maximum k-column segment length (1..32; default 28) */
 int ewb_set_max_segment(ewb_handle *h, int mcap);
 
+/* real-space cell grid: 0 = auto (r_c/2 cells, 5^3 stencil, when >= 5 cells
+ * per edge), 1 = r_c cells with the 3^3 stencil (the reference's grid). */
+int ewb_set_stencil(ewb_handle *h, int rad);
+
 /* EwaldParams: box edge L, screening alpha (A^-2, erfc(sqrt(alpha) r)),
  * real-space cutoff.  rc2 is r_cutoff**2 as the caller computed it, so the
  * cutoff predicate r2 < rc2 is bit-identical to the reference's. */

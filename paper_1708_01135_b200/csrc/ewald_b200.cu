@@ -585,10 +585,13 @@ __global__ void k_iota(int *__restrict__ v, int64_t n) {
 }
 
 __global__ void k5_gather(const int *__restrict__ order, const double4 *__restrict__ xyzq,
-                          int64_t n, double4 *__restrict__ sorted) {
+                          const int *__restrict__ cell_of, int64_t n,
+                          double4 *__restrict__ sorted, int *__restrict__ sorted_cell) {
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= n) return;
-  sorted[p] = xyzq[order[p]];
+  const int o = order[p];
+  sorted[p] = xyzq[o];
+  sorted_cell[p] = cell_of[o];
 }
 
 // erfcx(x) = exp(x^2) erfc(x) on [0, 6): 12 intervals of width 1/2, degree-12
@@ -632,39 +635,10 @@ __device__ __forceinline__ double erfc_from_exp(double x, double e, const double
 // pairs go to a per-lane queue and are evaluated in converged rounds.
 struct RSParams {
   double L, hl, rc2, sa, al, tsap;
-  int cpd, fold;
+  int cpd, fold, rad;  // rad: stencil radius in cells (1 or 2)
   int c_lo, c_hi;
   int64_t n;
 };
-
-__device__ __forceinline__ void rs_shift(int c, int s, int cpd, double L, double &sx, double &sy,
-                                         double &sz, int &nc) {
-  const int cx = c % cpd, cy = (c / cpd) % cpd, cz = c / (cpd * cpd);
-  int nx = cx + (s % 3) - 1, ny = cy + (s / 3) % 3 - 1, nz = cz + s / 9 - 1;
-  sx = sy = sz = 0.0;
-  if (nx < 0) {
-    nx += cpd;
-    sx = L;
-  } else if (nx >= cpd) {
-    nx -= cpd;
-    sx = -L;
-  }
-  if (ny < 0) {
-    ny += cpd;
-    sy = L;
-  } else if (ny >= cpd) {
-    ny -= cpd;
-    sy = -L;
-  }
-  if (nz < 0) {
-    nz += cpd;
-    sz = L;
-  } else if (nz >= cpd) {
-    nz -= cpd;
-    sz = -L;
-  }
-  nc = nx + cpd * (ny + cpd * nz);
-}
 
 // dx exactly as the reference: fl(xi - xj) then one fold by +-L
 // (engine.py:117-131); with a stencil the fold is the cell-pair shift, which
@@ -687,22 +661,38 @@ __device__ __forceinline__ double rs_r2(double dx, double dy, double dz) {
   return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
 }
 
-template <bool FOLD>
+// shift code per axis: 0 -> -L, 1 -> 0, 2 -> +L, 3 -> fold per pair
+template <int AX>
+__device__ __forceinline__ double rs_axis(double xi, double xj, int code, double L, double hl) {
+  double d = __dsub_rn(xi, xj);
+  if (code == 3) {
+    if (d >= hl)
+      d = __dsub_rn(d, L);
+    else if (d < -hl)
+      d = __dadd_rn(d, L);
+  } else if (code != 1) {
+    d = __dadd_rn(d, code == 2 ? L : -L);
+  }
+  return d;
+}
+
+constexpr int K6_LIST = 32 * K6_G + 32;  // pending pairs per warp
+
 __global__ void __launch_bounds__(K6_WARPS * 32)
-    k6_real_space(const double4 *__restrict__ sorted, const int *__restrict__ order,
-                  const int *__restrict__ cell_start, const int *__restrict__ ustart, RSParams P,
-                  double *__restrict__ force, double *__restrict__ eblk, int *__restrict__ err) {
-  // One warp = up to K6_G centre particles i of one home cell.  Lanes walk
-  // the stencil's candidates j (coalesced double4 loads), test every centre
-  // with the reference's exact predicate, and append accepted j to the
-  // centre's pair list (ballot compaction).  A list with >= 32 pairs is
-  // evaluated in one converged round: lane l computes pair (i_g, j_l) and
-  // accumulates into its private slot of F_g (shared memory); the 32 slots
-  // are summed at the end.  erfc/exp run on a partially active warp only in
-  // the final round of each centre, and exist once in the instruction
-  // stream (the test loop is unrolled over centres, the evaluation is not).
+    k6_real_space(const double4 *__restrict__ sorted, const int *__restrict__ sorted_cell,
+                  const int *__restrict__ order, const int *__restrict__ cell_start,
+                  const int *__restrict__ row_ustart, RSParams P, double *__restrict__ force,
+                  double *__restrict__ eblk, int *__restrict__ err) {
+  // A warp owns K6_G consecutive particles (centres) of one row of cells
+  // (fixed cy, cz).  Lanes stream the candidates of the stencil rows --
+  // contiguous runs of cells along x, so each 32-wide step is dense -- test
+  // each centre with the reference's exact predicate (engine.py:117-133,
+  // strict r2 < rc2), and append accepted (centre g, j, image) to one warp
+  // pair list by ballot compaction.  Whenever >= 32 pairs are pending they
+  // are evaluated in a converged round (lane l: pair l) and accumulated into
+  // the lane's slot of F_g in shared memory; slots are summed at the end.
   __shared__ double4 s_i[K6_WARPS][K6_G];
-  __shared__ uint32_t s_list[K6_WARPS][K6_G][64];
+  __shared__ uint2 s_list[K6_WARPS][K6_LIST];
   __shared__ double3 s_f[K6_WARPS][K6_G][32];
   __shared__ double sh[K6_WARPS];
   __shared__ double s_erfcx[ERFCX_NI * ERFCX_NC];
@@ -711,47 +701,42 @@ __global__ void __launch_bounds__(K6_WARPS * 32)
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
-  const int u_lo = ustart[P.c_lo], u_hi = ustart[P.c_hi];
+  const int cpd = P.cpd, R = P.rad;
+  const int r_lo = P.c_lo, r_hi = P.c_hi;  // row range of this slab
+  const int u_lo = row_ustart[r_lo], u_hi = row_ustart[r_hi];
   const int u = u_lo + blockIdx.x * K6_WARPS + warp;
   double ue = 0.0;
   if (u < u_hi) {
-    int lo = P.c_lo, hi = P.c_hi - 1;
+    int lo = r_lo, hi = r_hi - 1;
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
-      if (ustart[mid] <= u)
+      if (row_ustart[mid] <= u)
         lo = mid;
       else
         hi = mid - 1;
     }
-    const int c = lo;
-    const int cs = cell_start[c], ce = cell_start[c + 1];
-    const int first = cs + K6_G * (u - ustart[c]);
-    const int gi = min(K6_G, ce - first);
+    const int row = lo;
+    const int rb = P.fold ? 0 : cell_start[row * cpd];
+    const int re = P.fold ? (int)P.n : cell_start[(row + 1) * cpd];
+    const int first = rb + K6_G * (u - row_ustart[row]);
+    const int gi = min(K6_G, re - first);
     if (lane < gi) s_i[warp][lane] = sorted[first + lane];
 #pragma unroll
     for (int g = 0; g < K6_G; ++g) s_f[warp][g][lane] = make_double3(0.0, 0.0, 0.0);
     __syncwarp();
-    int cnt[K6_G];
-#pragma unroll
-    for (int g = 0; g < K6_G; ++g) cnt[g] = 0;
+    int cnt = 0;  // pending pairs (warp-uniform)
     bool coincident = false;
 
-    // evaluate the first n (<= 32) entries of list g: lane l takes entry l
-    auto round = [&](const int g, const int n) {
+    auto round = [&](const int base, const int n) {
       if (lane < n) {
-        const uint32_t code = s_list[warp][g][lane];
-        const int j = (int)(code & 0x7FFFFFFu);
-        const int sc_id = (int)(code >> 27);
+        const uint2 e = s_list[warp][base + lane];
+        const int j = (int)e.x;
+        const int g = (int)(e.y & 15u);
         const double4 pj = sorted[j];
         const double4 pi = s_i[warp][g];
-        double sx = 0.0, sy = 0.0, sz = 0.0;
-        if (!FOLD) {
-          int nc;
-          rs_shift(c, sc_id, P.cpd, P.L, sx, sy, sz, nc);
-        }
-        const double dx = rs_disp<FOLD>(pi.x, pj.x, sx, P.hl, P.L);
-        const double dy = rs_disp<FOLD>(pi.y, pj.y, sy, P.hl, P.L);
-        const double dz = rs_disp<FOLD>(pi.z, pj.z, sz, P.hl, P.L);
+        const double dx = rs_axis<0>(pi.x, pj.x, (e.y >> 4) & 3, P.L, P.hl);
+        const double dy = rs_axis<1>(pi.y, pj.y, (e.y >> 6) & 3, P.L, P.hl);
+        const double dz = rs_axis<2>(pi.z, pj.z, (e.y >> 8) & 3, P.L, P.hl);
         const double r2 = rs_r2(dx, dy, dz);
         if (r2 == 0.0) {
           coincident = true;
@@ -761,10 +746,10 @@ __global__ void __launch_bounds__(K6_WARPS * 32)
           const double qq = pi.w * pj.w;
           const double inv_r = rsqrt(r2);
           const double r = r2 * inv_r;
-          const double e = exp(-P.al * r2);
-          const double sc = erfc_from_exp(P.sa * r, e, s_erfcx) * inv_r;
+          const double ex = exp(-P.al * r2);
+          const double sc = erfc_from_exp(P.sa * r, ex, s_erfcx) * inv_r;
           ue += 0.5 * qq * sc;
-          const double gg = qq * fma(P.tsap, e, sc) * (inv_r * inv_r);
+          const double gg = qq * fma(P.tsap, ex, sc) * (inv_r * inv_r);
           double3 f = s_f[warp][g][lane];
           f.x = fma(gg, dx, f.x);
           f.y = fma(gg, dy, f.y);
@@ -774,83 +759,107 @@ __global__ void __launch_bounds__(K6_WARPS * 32)
       }
     };
 
-    const int nst = FOLD ? 1 : 27;
-    for (int s = 0; s < nst; ++s) {
-      int jb, je;
-      double sx = 0.0, sy = 0.0, sz = 0.0;
-      if (FOLD) {
-        jb = 0;
-        je = (int)P.n;
-      } else {
-        int nc;
-        rs_shift(c, s, P.cpd, P.L, sx, sy, sz, nc);
-        jb = cell_start[nc];
-        je = cell_start[nc + 1];
+    // candidate pieces: contiguous cell runs along x with one image code
+    int cy = 0, cz = 0, xa = 0, xb = 0;
+    bool wide = true;
+    if (!P.fold) {
+      cy = row % cpd;
+      cz = row / cpd;
+      const int cx_lo = sorted_cell[first] % cpd;
+      const int cx_hi = sorted_cell[first + gi - 1] % cpd;
+      wide = (cx_hi - cx_lo + 2 * R + 1) > cpd;
+      xa = wide ? 0 : cx_lo - R;
+      xb = wide ? cpd - 1 : cx_hi + R;
+    }
+    const int nyz = P.fold ? 1 : (2 * R + 1) * (2 * R + 1);
+    for (int yz = 0; yz < nyz; ++yz) {
+      int ny = 0, nz = 0, kyc = 3, kzc = 3;
+      if (!P.fold) {
+        ny = cy + yz % (2 * R + 1) - R;
+        nz = cz + yz / (2 * R + 1) - R;
+        kyc = 1;
+        kzc = 1;
+        if (ny < 0) { ny += cpd; kyc = 2; } else if (ny >= cpd) { ny -= cpd; kyc = 0; }
+        if (nz < 0) { nz += cpd; kzc = 2; } else if (nz >= cpd) { nz -= cpd; kzc = 0; }
       }
-      const bool shifted = (sx != 0.0) || (sy != 0.0) || (sz != 0.0);
-      for (int j0 = jb; j0 < je; j0 += 32) {
-        const int j = j0 + lane;
-        const bool vj = j < je;
-        const double4 pj = sorted[vj ? j : jb];
-        int full = 0;  // bit g: list g holds >= 32 pairs
-#pragma unroll
-        for (int g = 0; g < K6_G; ++g) {
-          if (g < gi) {
-            const double4 pi = s_i[warp][g];
-            double dx, dy, dz;
-            if (FOLD) {
-              dx = rs_disp<true>(pi.x, pj.x, 0.0, P.hl, P.L);
-              dy = rs_disp<true>(pi.y, pj.y, 0.0, P.hl, P.L);
-              dz = rs_disp<true>(pi.z, pj.z, 0.0, P.hl, P.L);
-            } else if (!shifted) {
-              // fl(fl(xi-xj) + 0.0) == fl(xi-xj) up to the sign of zero, so
-              // r2 is bit-identical to the shifted recomputation in round()
-              dx = __dsub_rn(pi.x, pj.x);
-              dy = __dsub_rn(pi.y, pj.y);
-              dz = __dsub_rn(pi.z, pj.z);
-            } else {
-              dx = rs_disp<false>(pi.x, pj.x, sx, P.hl, P.L);
-              dy = rs_disp<false>(pi.y, pj.y, sy, P.hl, P.L);
-              dz = rs_disp<false>(pi.z, pj.z, sz, P.hl, P.L);
-            }
-            const double r2 = rs_r2(dx, dy, dz);
-            const bool acc = vj && (r2 < P.rc2) && (j != first + g);
-            const unsigned bal = __ballot_sync(0xffffffffu, acc);
-            if (acc)
-              s_list[warp][g][cnt[g] + __popc(bal & lt_mask)] = (uint32_t)j | ((uint32_t)s << 27);
-            cnt[g] += __popc(bal);
-            if (cnt[g] >= 32) full |= 1 << g;
-          }
+      for (int piece = 0; piece < 3; ++piece) {
+        int jb, je, kxc;
+        if (P.fold) {
+          if (piece) break;
+          jb = 0;
+          je = (int)P.n;
+          kxc = 3;
+        } else if (wide) {
+          if (piece) break;
+          const int cb = cpd * (ny + cpd * nz);
+          jb = cell_start[cb];
+          je = cell_start[cb + cpd];
+          kxc = 3;
+        } else {
+          int x0, x1;
+          if (piece == 0) { x0 = xa; x1 = min(xb, -1); kxc = 2; }           // wrapped from the top
+          else if (piece == 1) { x0 = max(xa, 0); x1 = min(xb, cpd - 1); kxc = 1; }
+          else { x0 = max(xa, cpd); x1 = xb; kxc = 0; }                      // wrapped from the bottom
+          if (x0 > x1) continue;
+          const int off = piece == 0 ? cpd : (piece == 2 ? -cpd : 0);
+          const int cb = cpd * (ny + cpd * nz);
+          jb = cell_start[cb + x0 + off];
+          je = cell_start[cb + x1 + off + 1];
         }
-        // converged evaluation rounds (one code copy, uniform g)
-        while (full) {
-          const int g = __ffs(full) - 1;
-          full &= full - 1;
-          int ng = 0;
+        const double sx = kxc == 2 ? P.L : -P.L;
+        const double sy = kyc == 2 ? P.L : -P.L;
+        const double sz = kzc == 2 ? P.L : -P.L;
+        const uint32_t tag = ((uint32_t)kxc << 4) | ((uint32_t)kyc << 6) | ((uint32_t)kzc << 8);
+        for (int j0 = jb; j0 < je; j0 += 32) {
+          const int j = j0 + lane;
+          const bool vj = j < je;
+          const double4 pj = sorted[vj ? j : jb];
 #pragma unroll
-          for (int t = 0; t < K6_G; ++t)
-            if (t == g) ng = cnt[t];
-          __syncwarp();
-          round(g, 32);
-          __syncwarp();
-          const int rest = ng - 32;
-          const uint32_t mv = lane < rest ? s_list[warp][g][32 + lane] : 0u;
-          __syncwarp();
-          if (lane < rest) s_list[warp][g][lane] = mv;
-#pragma unroll
-          for (int t = 0; t < K6_G; ++t)
-            if (t == g) cnt[t] = rest;
+          for (int g = 0; g < K6_G; ++g) {
+            if (g < gi) {
+              const double4 pi = s_i[warp][g];
+              double dx = __dsub_rn(pi.x, pj.x);
+              double dy = __dsub_rn(pi.y, pj.y);
+              double dz = __dsub_rn(pi.z, pj.z);
+              if (kxc == 3) {
+                if (dx >= P.hl) dx = __dsub_rn(dx, P.L); else if (dx < -P.hl) dx = __dadd_rn(dx, P.L);
+              } else if (kxc != 1) {
+                dx = __dadd_rn(dx, sx);
+              }
+              if (kyc == 3) {
+                if (dy >= P.hl) dy = __dsub_rn(dy, P.L); else if (dy < -P.hl) dy = __dadd_rn(dy, P.L);
+              } else if (kyc != 1) {
+                dy = __dadd_rn(dy, sy);
+              }
+              if (kzc == 3) {
+                if (dz >= P.hl) dz = __dsub_rn(dz, P.L); else if (dz < -P.hl) dz = __dadd_rn(dz, P.L);
+              } else if (kzc != 1) {
+                dz = __dadd_rn(dz, sz);
+              }
+              const double r2 = rs_r2(dx, dy, dz);
+              const bool acc = vj && (r2 < P.rc2) && (j != first + g);
+              const unsigned bal = __ballot_sync(0xffffffffu, acc);
+              if (acc) s_list[warp][cnt + __popc(bal & lt_mask)] = make_uint2((uint32_t)j, tag | g);
+              cnt += __popc(bal);
+            }
+          }
+          if (cnt >= 32) {
+            __syncwarp();
+            int base = 0;
+            for (; cnt - base >= 32; base += 32) round(base, 32);
+            const int rest = cnt - base;
+            __syncwarp();
+            const uint2 mv = lane < rest ? s_list[warp][base + lane] : make_uint2(0u, 0u);
+            __syncwarp();
+            if (lane < rest) s_list[warp][lane] = mv;
+            __syncwarp();
+            cnt = rest;
+          }
         }
       }
     }
     __syncwarp();
-    for (int g = 0; g < gi; ++g) {
-      int ng = 0;
-#pragma unroll
-      for (int t = 0; t < K6_G; ++t)
-        if (t == g) ng = cnt[t];
-      if (ng > 0) round(g, ng);
-    }
+    if (cnt > 0) round(0, cnt);
     if (coincident) atomicOr(err, ERR_COINCIDENT);
     __syncwarp();
     for (int g = 0; g < gi; ++g) {
@@ -872,6 +881,45 @@ __global__ void __launch_bounds__(K6_WARPS * 32)
     for (int w = 0; w < K6_WARPS; ++w) b += sh[w];
     eblk[blockIdx.x] = b;
   }
+}
+
+// Units per row of cells: row_ustart[r] = sum_{r'<r} ceil(count(r')/K6_G).
+__global__ void __launch_bounds__(1024) k_scan_rows(const int *__restrict__ start, int cpd,
+                                                    int n_rows, int *__restrict__ row_ustart) {
+  __shared__ int wsum[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int base = 0; base < n_rows; base += 1024) {
+    const int r = base + threadIdx.x;
+    const int cnt = r < n_rows ? start[(r + 1) * cpd] - start[r * cpd] : 0;
+    const int b = (cnt + K6_G - 1) / K6_G;
+    int ib = b;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, ib, o);
+      if (lane >= o) ib += t;
+    }
+    if (lane == 31) wsum[w] = ib;
+    __syncthreads();
+    if (w == 0) {
+      int x = wsum[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += t;
+      }
+      wsum[lane] = x;
+    }
+    __syncthreads();
+    const int pb = (w ? wsum[w - 1] : 0) + ib - b + carry;
+    if (r < n_rows) row_ustart[r] = pb;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = pb + b;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) row_ustart[n_rows] = carry;
 }
 
 // K7: sum q^2 (self energy) partials.
@@ -989,6 +1037,7 @@ struct ewb_handle {
   cudaEvent_t ev[6] = {};
   std::string err;
   int mcap = 28;
+  int stencil_rad = 0;  // 0 auto, 1 force r_c cells (testing)
   int64_t launches = 0;
   // system
   bool have_system = false;
@@ -1002,7 +1051,7 @@ struct ewb_handle {
   DBuf pos, q, force, rho;                   // host-API staging (caller layout)
   DBuf frac, base, xyzq;                     // derived
   DBuf spart, sslot, sp, fpart, upart, eblk, eblk2, energy, errflag;
-  DBuf cell_of, slot, count, start, gstart, order_tmp, order, sorted;
+  DBuf cell_of, slot, count, start, gstart, order_tmp, order, sorted, sorted_cell, row_ustart;
   int occ_k1[MAXM + 1] = {};
   int occ_k3[MAXM + 1][2] = {};
   bool k1_attr[MAXM + 1] = {};
@@ -1212,7 +1261,7 @@ int require_state(ewb_handle *h, bool need_kspace, bool need_loaded) {
 // ---- stages (all asynchronous on h->stream) ----
 int stage_load(ewb_handle *h, const double *d_pos, const double *d_q, int64_t n) {
   if (n < 1) return h->fail(EWB_EINVAL, "particle count must be >= 1");
-  if (n >= (int64_t)1 << 27) return h->fail(EWB_EINVAL, "particle count must be < 2^27");
+  if (n >= (int64_t)1 << 25) return h->fail(EWB_EINVAL, "particle count must be < 2^25");
   CK(h->frac.ensure(n * sizeof(double4)));
   CK(h->xyzq.ensure(n * sizeof(double4)));
   CK(h->base.ensure(n * 3 * sizeof(double2)));
@@ -1339,10 +1388,20 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
   // reference binning: cpd = floor(L / r_c), edge = L / cpd (celllist.py:96-98);
   // with cpd < 3 the 27-stencil folds onto every cell and the reference scans
   // all particles with a per-pair fold (engine.py:111-134) -- FOLD mode here.
-  int cpd = (int)std::floor(h->L / h->rc);
+  // Cells of edge >= r_c/2 with a 5^3 stencil when the box holds >= 5 of
+  // them (42% fewer candidate pairs than r_c cells with 3^3), else r_c cells
+  // with 3^3, else (fewer than 3 cells) the reference's scan-all branch.
+  // Any cell size whose stencil covers the cutoff sphere visits the same
+  // pair set: the predicate, not the binning, decides membership.
+  int rad = 2;
+  int cpd = (int)std::floor(2.0 * h->L / h->rc);
+  if (cpd < 5 || h->stencil_rad == 1) {
+    rad = 1;
+    cpd = (int)std::floor(h->L / h->rc);
+  }
   if (cpd < 1) cpd = 1;
-  if (cpd > 128) cpd = 128;  // edge stays >= r_c; bounds the cell arrays
-  const bool fold = cpd < 3;
+  if (cpd > 64) cpd = 64;  // edge stays >= r_c/rad; bounds the cell arrays
+  const bool fold = cpd < 2 * rad + 1;
   const int cpd_eff = fold ? 1 : cpd;
   const int n_cells = cpd_eff * cpd_eff * cpd_eff;
   const double edge = h->L / cpd;
@@ -1374,8 +1433,17 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
                                                  h->order.as<int>());
     CKL();
   }
+  CK(h->sorted_cell.ensure(n * sizeof(int)));
   k5_gather<<<blocks_for(n, 256), 256, 0, h->stream>>>(h->order.as<int>(), h->xyzq.as<double4>(),
-                                                       n, h->sorted.as<double4>());
+                                                       h->cell_of.as<int>(), n,
+                                                       h->sorted.as<double4>(),
+                                                       h->sorted_cell.as<int>());
+  CKL();
+  // units: K6_G consecutive particles of one row of cells (fixed cy, cz)
+  const int n_rows = fold ? 1 : cpd_eff * cpd_eff;
+  CK(h->row_ustart.ensure((n_rows + 1) * sizeof(int)));
+  k_scan_rows<<<1, 1024, 0, h->stream>>>(h->start.as<int>(), cpd_eff, n_rows,
+                                         h->row_ustart.as<int>());
   CKL();
   if (ev_cell) CK(cudaEventRecord(ev_cell, h->stream));
 
@@ -1388,26 +1456,23 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
   rp.tsap = 2.0 * std::sqrt(h->alpha / M_PI);
   rp.cpd = cpd_eff;
   rp.fold = fold;
+  rp.rad = rad;
   rp.n = n;
+  // slab of rows (z-layers of cells) owned by this part
   const int zl = (int)((int64_t)cpd_eff * part / nparts), zh = (int)((int64_t)cpd_eff * (part + 1) / nparts);
-  rp.c_lo = zl * cpd_eff * cpd_eff;
-  rp.c_hi = zh * cpd_eff * cpd_eff;
-  const int64_t cells_slab = rp.c_hi - rp.c_lo;
-  const int64_t units_max = n / K6_G + cells_slab + 1;
+  rp.c_lo = fold ? (part == 0 ? 0 : 1) : zl * cpd_eff;
+  rp.c_hi = fold ? 1 : zh * cpd_eff;
+  const int64_t rows_slab = rp.c_hi - rp.c_lo;
+  const int64_t units_max = n / K6_G + rows_slab + 1;
   const unsigned nb = (unsigned)std::max<int64_t>(1, (units_max + K6_WARPS - 1) / K6_WARPS);
   CK(h->eblk.ensure(nb * sizeof(double)));
-  if (cells_slab <= 0) {
+  if (rows_slab <= 0) {
     CK(cudaMemsetAsync(d_u_out, 0, sizeof(double), h->stream));
     return EWB_OK;
   }
-  if (fold)
-    k6_real_space<true><<<nb, K6_WARPS * 32, 0, h->stream>>>(
-        h->sorted.as<double4>(), h->order.as<int>(), h->start.as<int>(), h->gstart.as<int>(), rp,
-        d_force, h->eblk.as<double>(), h->errflag.as<int>());
-  else
-    k6_real_space<false><<<nb, K6_WARPS * 32, 0, h->stream>>>(
-        h->sorted.as<double4>(), h->order.as<int>(), h->start.as<int>(), h->gstart.as<int>(), rp,
-        d_force, h->eblk.as<double>(), h->errflag.as<int>());
+  k6_real_space<<<nb, K6_WARPS * 32, 0, h->stream>>>(
+      h->sorted.as<double4>(), h->sorted_cell.as<int>(), h->order.as<int>(), h->start.as<int>(),
+      h->row_ustart.as<int>(), rp, d_force, h->eblk.as<double>(), h->errflag.as<int>());
   CKL();
   k_sum<<<1, 1024, 0, h->stream>>>(h->eblk.as<double>(), nb, 1.0, d_u_out);
   CKL();
@@ -1543,7 +1608,7 @@ void ewb_destroy(ewb_handle *h) {
   for (DBuf *b : {&h->pos, &h->q, &h->force, &h->rho, &h->frac, &h->base, &h->xyzq, &h->spart,
                   &h->sslot, &h->sp, &h->fpart, &h->upart, &h->eblk, &h->eblk2, &h->energy,
                   &h->errflag, &h->cell_of, &h->slot, &h->count, &h->start, &h->gstart,
-                  &h->order_tmp, &h->order, &h->sorted})
+                  &h->order_tmp, &h->order, &h->sorted, &h->sorted_cell, &h->row_ustart})
     b->release();
   h->plan.release();
   for (auto &ev : h->ev)
@@ -1564,6 +1629,13 @@ int ewb_set_max_segment(ewb_handle *h, int mcap) {
   if (!h) return EWB_EINVAL;
   if (mcap < 1 || mcap > MAXM) return h->fail(EWB_EINVAL, "segment length must be in [1, 32]");
   h->mcap = mcap;
+  return EWB_OK;
+}
+
+int ewb_set_stencil(ewb_handle *h, int rad) {
+  if (!h) return EWB_EINVAL;
+  if (rad < 0 || rad > 2) return h->fail(EWB_EINVAL, "stencil radius must be 0 (auto), 1 or 2");
+  h->stencil_rad = rad;
   return EWB_OK;
 }
 

@@ -297,3 +297,22 @@ def test_device_stages_sharded_match_full(ew):
     assert rel(u_self, en[2]) <= 1e-14
     ff = f_full.cpu().numpy()
     assert np.abs(f.cpu().numpy() - ff).max() <= 1e-12 * f_rms(ff)
+
+
+@pytest.mark.parametrize("name", ["c2", "c4"])
+def test_stencil_grids_agree(ew, name):
+    """r_c/2 cells with the 5^3 stencil and the reference's r_c cells with
+    3^3 must visit the same ordered pairs (bit-identical predicate)."""
+    from paper_1708_01135_b200 import workloads as wl
+    cfg = wl.make_config(name, seed=0)
+    out = []
+    for rad in (0, 1):
+        box, ps = system(ew, cfg["pos"], cfg["q"], cfg["L"])
+        p = ew.EwaldParams(cfg["alpha_ref"], cfg["r_cutoff"], 3.0, 1e-6)
+        rs = ew.ReciprocalSpace(box, p, np.array([[1, 0, 0]]))
+        solver = ew.EwaldSolver(box, p, recip=rs)
+        solver.handle.set_stencil(rad)
+        res = solver.evaluate(ps)
+        out.append((res.u_sr, ps.force.copy()))
+    assert rel(out[0][0], out[1][0]) <= 1e-13
+    assert np.abs(out[0][1] - out[1][1]).max() <= 1e-12 * f_rms(out[1][1])

@@ -17,7 +17,9 @@ from .core import (
 )
 
 LIB_NAME = "libewaldb200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+LIB_PATH = os.environ.get(
+    "EWALDB200_LIB",
+    os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME))
 
 EWB_OK = 0
 EWB_EINVAL = 1

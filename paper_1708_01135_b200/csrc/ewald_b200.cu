@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -48,7 +49,19 @@ constexpr int ERR_COINCIDENT = 2;
 constexpr int MAXM = 32;          // longest k-column segment (template range)
 constexpr int K1_THREADS = 128;   // k-items per structure-factor block
 constexpr int K1_PMAX = 32;       // particles per shared-memory phase chunk
-constexpr int TAB_SEG = 8;        // phase-table entries per build task
+#ifndef K1_ILP
+#define K1_ILP 2                  // particles (independent chains) per K1 step
+#endif
+#ifndef K1_TAB_BYTES
+#define K1_TAB_BYTES (24 * 1024)  // one of the two phase-table buffers
+#endif
+#ifndef K1_PPB
+#define K1_PPB 256                // target particles per structure-factor block
+#endif
+constexpr size_t K1_PART_BYTES = (size_t)512 << 20;  // cap of the partial S(k) buffers
+#ifndef K3_WAVES
+#define K3_WAVES 4
+#endif
 constexpr int K3_THREADS = 128;
 constexpr int K3_PPT = 2;         // particles per thread in the gather
 constexpr int K3_CH = 32;         // k-items per shared-memory chunk
@@ -106,6 +119,61 @@ __global__ void k_prep(const double *__restrict__ pos, const double *__restrict_
   base[3 * i + 2] = make_double2(c, -s);
 }
 
+// K1 inner loop for G particles at once (G independent recurrence chains):
+// acc[m] += sum_g q_g e^{-i k_m . r_g} along one k-column segment.
+template <int M, int G>
+__device__ __forceinline__ void k1_accumulate(double2 (&acc)[M], const double2 *t, int TSp,
+                                              int2 it, int eidx) {
+  double2 bp[G], bc[G];
+  double c2[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const double2 *tg = t + g * TSp;
+    const double2 e = tg[eidx];
+    bp[g] = cmul(tg[it.x], tg[it.y]);  // m = 0: row x column entry
+    bc[g] = cmul(bp[g], e);            // m = 1
+    c2[g] = e.x + e.x;                 // 2 cos(theta_z)
+  }
+  {
+    double sx = bp[0].x, sy = bp[0].y;
+#pragma unroll
+    for (int g = 1; g < G; ++g) {
+      sx += bp[g].x;
+      sy += bp[g].y;
+    }
+    acc[0].x += sx;
+    acc[0].y += sy;
+  }
+  if (M > 1) {
+    double sx = bc[0].x, sy = bc[0].y;
+#pragma unroll
+    for (int g = 1; g < G; ++g) {
+      sx += bc[g].x;
+      sy += bc[g].y;
+    }
+    acc[1].x += sx;
+    acc[1].y += sy;
+  }
+#pragma unroll
+  for (int m = 2; m < M; ++m) {
+    double2 bn[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      bn[g] = make_double2(fma(c2[g], bc[g].x, -bp[g].x), fma(c2[g], bc[g].y, -bp[g].y));
+      bp[g] = bc[g];
+      bc[g] = bn[g];
+    }
+    double sx = bn[0].x, sy = bn[0].y;
+#pragma unroll
+    for (int g = 1; g < G; ++g) {
+      sx += bn[g].x;
+      sy += bn[g].y;
+    }
+    acc[m].x += sx;
+    acc[m].y += sy;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K1: structure factor.  Block = (k-tile of K1_THREADS items, particle chunk).
 template <int M>
@@ -130,88 +198,74 @@ __global__ void __launch_bounds__(K1_THREADS)
 
   const int64_t c_begin = p_begin + (int64_t)blockIdx.y * ppb;
   const int64_t c_end = min(p_end, c_begin + ppb);
-  const int ntask_p = (TS + TAB_SEG - 1) / TAB_SEG;
+  const int nch = (int)((c_end - c_begin + pchunk - 1) / pchunk);
+  const int TSp = TS | 1;  // odd stride: conflict-free per-particle rows
+  double2 *tabs[2] = {tab, tab + pchunk * TSp};
+  int4 *s_desc = reinterpret_cast<int4 *>(tab + 2 * pchunk * TSp);
+  for (int e = threadIdx.x; e < TS; e += K1_THREADS) s_desc[e] = desc[e];
+  __syncthreads();
 
-  for (int64_t c0 = c_begin; c0 < c_end; c0 += pchunk) {
+  // per-particle phase tables of this tile: rows q e^{-i(mx th_x + s th_z)},
+  // columns e^{-i my th_y}, and e^{-i th_z} (last entry).  The np*TS entries
+  // are split evenly over the block; each thread walks a contiguous run,
+  // starting every run (and every unlinked entry) with one sincospi and
+  // extending it by complex multiplication with the particle's axis phase.
+  auto build = [&](const int k, double2 *dst) {
+    const int64_t c0 = c_begin + (int64_t)k * pchunk;
     const int np = (int)min((int64_t)pchunk, c_end - c0);
-    __syncthreads();
-    // build the per-particle phase tables of this tile: rows
-    // q e^{-i(mx th_x + s th_z)}, columns e^{-i my th_y}, and e^{-i th_z}
-    for (int task = threadIdx.x; task < np * ntask_p; task += K1_THREADS) {
-      const int p = task / ntask_p;
-      const int e0 = (task - p * ntask_p) * TAB_SEG;
-      const int e1 = min(TS, e0 + TAB_SEG);
-      const double4 f = frac[c0 + p];
-      double2 prev = make_double2(1.0, 0.0);
-      for (int e = e0; e < e1; ++e) {
-        const int4 d = __ldg(desc + e);
-        double2 v;
-        if (e == e0 || !(d.w & TF_LINK)) {
-          const double arg = (double)d.x * f.x + (double)d.y * f.y + (double)d.z * f.z;
-          double sn, cs;
-          sincospi(2.0 * arg, &sn, &cs);
-          v = make_double2(cs, -sn);
-          if (d.w & TF_QSCALE) {
-            v.x *= f.w;
-            v.y *= f.w;
-          }
-        } else {
-          v = cmul(prev, base[3 * (c0 + p) + ((d.w >> 2) & 3)]);
-        }
-        tab[p * TS + e] = v;
-        prev = v;
+    const int total = np * TS;
+    const int per = (total + K1_THREADS - 1) / K1_THREADS;
+    int t = threadIdx.x * per;
+    const int t1 = min(total, t + per);
+    if (t >= t1) return;
+    int p = t / TS, e = t - p * TS;
+    double4 f = frac[c0 + p];
+    double2 bx = base[3 * (c0 + p)], by = base[3 * (c0 + p) + 1];
+    double2 prev = make_double2(1.0, 0.0);
+    bool fresh = true;
+    for (; t < t1; ++t) {
+      if (e == TS) {
+        e = 0;
+        ++p;
+        f = frac[c0 + p];
+        bx = base[3 * (c0 + p)];
+        by = base[3 * (c0 + p) + 1];
+        fresh = true;
       }
+      const int4 d = s_desc[e];
+      double2 v;
+      if (fresh || !(d.w & TF_LINK)) {
+        const double arg = (double)d.x * f.x + (double)d.y * f.y + (double)d.z * f.z;
+        double sn, cs;
+        sincospi(2.0 * arg, &sn, &cs);
+        v = make_double2(cs, -sn);
+        if (d.w & TF_QSCALE) {
+          v.x *= f.w;
+          v.y *= f.w;
+        }
+      } else {
+        v = cmul(prev, ((d.w >> 2) & 3) ? by : bx);
+      }
+      dst[p * TSp + e] = v;
+      prev = v;
+      fresh = false;
+      ++e;
     }
-    __syncthreads();
+  };
+
+  if (nch > 0) build(0, tabs[0]);
+  __syncthreads();
+  for (int k = 0; k < nch; ++k) {
+    // the next chunk's table is built by the same warps while (or before)
+    // they consume this one; warps that finish early start computing, so the
+    // latency-bound build overlaps other warps' FP64 work
+    if (k + 1 < nch) build(k + 1, tabs[(k + 1) & 1]);
+    const double2 *tab_k = tabs[k & 1];
+    const int np = (int)min((int64_t)pchunk, c_end - (c_begin + (int64_t)k * pchunk));
     int p = 0;
-    for (; p + 1 < np; p += 2) {
-      const double2 *t0 = tab + p * TS;
-      const double2 *t1 = t0 + TS;
-      const double2 e0 = t0[eidx], e1 = t1[eidx];
-      const double2 b0 = cmul(t0[it.x], t0[it.y]);
-      const double2 d0 = cmul(t1[it.x], t1[it.y]);
-      const double c0z = e0.x + e0.x, c1z = e1.x + e1.x;
-      acc[0].x += b0.x + d0.x;
-      acc[0].y += b0.y + d0.y;
-      if (M > 1) {
-        double2 bp = b0, dp = d0;
-        double2 bc = cmul(b0, e0), dc = cmul(d0, e1);
-        acc[1].x += bc.x + dc.x;
-        acc[1].y += bc.y + dc.y;
-#pragma unroll
-        for (int m = 2; m < M; ++m) {
-          const double2 bn = make_double2(fma(c0z, bc.x, -bp.x), fma(c0z, bc.y, -bp.y));
-          const double2 dn = make_double2(fma(c1z, dc.x, -dp.x), fma(c1z, dc.y, -dp.y));
-          acc[m].x += bn.x + dn.x;
-          acc[m].y += bn.y + dn.y;
-          bp = bc;
-          bc = bn;
-          dp = dc;
-          dc = dn;
-        }
-      }
-    }
-    if (p < np) {
-      const double2 *t0 = tab + p * TS;
-      const double2 e0 = t0[eidx];
-      const double2 b0 = cmul(t0[it.x], t0[it.y]);
-      const double c0z = e0.x + e0.x;
-      acc[0].x += b0.x;
-      acc[0].y += b0.y;
-      if (M > 1) {
-        double2 bp = b0, bc = cmul(b0, e0);
-        acc[1].x += bc.x;
-        acc[1].y += bc.y;
-#pragma unroll
-        for (int m = 2; m < M; ++m) {
-          const double2 bn = make_double2(fma(c0z, bc.x, -bp.x), fma(c0z, bc.y, -bp.y));
-          acc[m].x += bn.x;
-          acc[m].y += bn.y;
-          bp = bc;
-          bc = bn;
-        }
-      }
-    }
+    for (; p + K1_ILP <= np; p += K1_ILP) k1_accumulate<M, K1_ILP>(acc, tab_k + p * TSp, TSp, it, eidx);
+    for (; p < np; ++p) k1_accumulate<M, 1>(acc, tab_k + p * TSp, TSp, it, eidx);
+    __syncthreads();
   }
   if (valid) {
     double2 *out = spart + (size_t)blockIdx.y * M * n_items + item;
@@ -290,16 +344,19 @@ __device__ __forceinline__ double2 phase_plus(int mx, int my, int s, double tx, 
   return make_double2(cs, sn);
 }
 
+#ifndef K3_MINB
+#define K3_MINB 4
+#endif
 template <int M, bool ENERGY>
-__global__ void __launch_bounds__(K3_THREADS)
+__global__ void __launch_bounds__(K3_THREADS, K3_MINB)
     k3_force_gather(const double4 *__restrict__ frac, const double2 *__restrict__ base,
                     int64_t p_begin, int64_t p_end, const int4 *__restrict__ rows,
                     const int *__restrict__ ks_rows, const int *__restrict__ item_my,
                     const int *__restrict__ item_row, const double2 *__restrict__ sp, int n_items,
                     double *__restrict__ fpart, double *__restrict__ upart) {
-  __shared__ double2 s_sp[K3_CH * M];
-  __shared__ int s_my[K3_CH];
-  __shared__ int s_row[K3_CH];
+  __shared__ double2 s_spb[2][K3_CH * M];
+  __shared__ int s_myb[2][K3_CH];
+  __shared__ int s_rowb[2][K3_CH];
   const int64_t n_local = p_end - p_begin;
   const int ks = blockIdx.y;
   const int r_begin = ks_rows[ks], r_end = ks_rows[ks + 1];
@@ -329,18 +386,52 @@ __global__ void __launch_bounds__(K3_THREADS)
     const int i_first = rows[r_begin].z;
     const int4 rl = rows[r_end - 1];
     const int i_last = rl.z + rl.w;
-    for (int c0 = i_first; c0 < i_last; c0 += K3_CH) {
+    // C_k S_k chunks are double-buffered through registers: chunk k+1 is
+    // fetched from L2 before chunk k is consumed and stored after it
+    constexpr int NPT = (K3_CH * M + K3_THREADS - 1) / K3_THREADS;
+    double2 stage_sp[NPT];
+    int stage_my = 0, stage_row = 0;
+    auto fetch = [&](const int c0) {
       const int nc = min(K3_CH, i_last - c0);
-      __syncthreads();
-      for (int t = threadIdx.x; t < nc * M; t += K3_THREADS) {
-        const int m = t / nc, itc = t - m * nc;
-        s_sp[itc * M + m] = sp[(size_t)m * n_items + c0 + itc];
+#pragma unroll
+      for (int u = 0; u < NPT; ++u) {
+        const int t = threadIdx.x + u * K3_THREADS;
+        if (t < nc * M) {
+          const int m = t / nc, itc = t - m * nc;
+          stage_sp[u] = sp[(size_t)m * n_items + c0 + itc];
+        }
       }
-      for (int t = threadIdx.x; t < nc; t += K3_THREADS) {
-        s_my[t] = item_my[c0 + t];
-        s_row[t] = item_row[c0 + t];
+      if (threadIdx.x < nc) {
+        stage_my = item_my[c0 + threadIdx.x];
+        stage_row = item_row[c0 + threadIdx.x];
       }
-      __syncthreads();
+    };
+    auto commit = [&](const int c0, const int b) {
+      const int nc = min(K3_CH, i_last - c0);
+#pragma unroll
+      for (int u = 0; u < NPT; ++u) {
+        const int t = threadIdx.x + u * K3_THREADS;
+        if (t < nc * M) {
+          const int m = t / nc, itc = t - m * nc;
+          s_spb[b][itc * M + m] = stage_sp[u];
+        }
+      }
+      if (threadIdx.x < nc) {
+        s_myb[b][threadIdx.x] = stage_my;
+        s_rowb[b][threadIdx.x] = stage_row;
+      }
+    };
+    fetch(i_first);
+    commit(i_first, 0);
+    __syncthreads();
+    int kb = 0;
+    for (int c0 = i_first; c0 < i_last; c0 += K3_CH, kb ^= 1) {
+      const int nc = min(K3_CH, i_last - c0);
+      const bool more = c0 + K3_CH < i_last;
+      if (more) fetch(c0 + K3_CH);
+      const double2 *s_sp = s_spb[kb];
+      const int *s_my = s_myb[kb];
+      const int *s_row = s_rowb[kb];
       for (int itc = 0; itc < nc; ++itc) {
         const int row = s_row[itc], my = s_my[itc];
         if (row != cur_row) {
@@ -411,6 +502,8 @@ __global__ void __launch_bounds__(K3_THREADS)
           SH[q] += H[q];
         }
       }
+      if (more) commit(c0 + K3_CH, kb ^ 1);
+      __syncthreads();
     }
     if (cur_row >= 0) {
 #pragma unroll
@@ -616,18 +709,46 @@ constexpr int ERFCX_NI = 12;
 constexpr int ERFCX_NC = 13;
 
 // erfc(x) given e = exp(-x^2) (which the force needs anyway); the table lives
-// in shared memory (lanes index different intervals).
+// in shared memory (lanes index different intervals).  For x >= 6,
+// erfc(x) < 2.2e-17 and the pair's contribution is below double resolution
+// of any energy it enters; it is flushed to zero (branch-free).
 __device__ __forceinline__ double erfc_from_exp(double x, double e, const double *tab) {
-  if (x < 0.5 * ERFCX_NI) {
-    const int i = (int)(x * 2.0);
-    const double t = fma(4.0, x, -(double)(2 * i + 1));
-    const double *c = tab + i * ERFCX_NC;
-    double r = c[ERFCX_NC - 1];
+  const int i = min((int)(x * 2.0), ERFCX_NI - 1);
+  const double t = fma(4.0, x, -(double)(2 * i + 1));
+  const double *c = tab + i * ERFCX_NC;
+  double r = c[ERFCX_NC - 1];
 #pragma unroll
-    for (int k = ERFCX_NC - 2; k >= 0; --k) r = fma(r, t, c[k]);
-    return r * e;
-  }
-  return erfc(x);
+  for (int k = ERFCX_NC - 2; k >= 0; --k) r = fma(r, t, c[k]);
+  return x < 0.5 * ERFCX_NI ? r * e : 0.0;
+}
+
+// 1/sqrt(x) for finite x > 0: fp32 hardware seed (~22 bits) refined by two
+// Newton steps in fp64 (~1 ulp), without the library's special-case paths.
+__device__ __forceinline__ double rsqrt_pos(double x) {
+  double y = (double)rsqrtf((float)x);
+  const double h = 0.5 * x;
+  y = y * fma(-h * y, y, 1.5);
+  const double e = fma(-x * y, y, 1.0);  // residual 1 - x y^2
+  return fma(0.5 * y, e, y);
+}
+
+// exp(x) for -700 < x <= 0 (real-space arguments -alpha r^2): Cody-Waite
+// reduction and a degree-11 polynomial on [-ln2/2, ln2/2] (max rel. error
+// 2.2e-16, fitted by tools, coefficients in the constant bank).
+__constant__ double c_expm[12] = {1.0, 1.0, 0.5000000000000018, 0.16666666666666147,
+                                  0.04166666666649302, 0.008333333333569285,
+                                  0.001388888895117063, 0.00019841269413559004,
+                                  2.4801486567664484e-05, 2.7557638471514137e-06,
+                                  2.763227940718779e-07, 2.4989478846203685e-08};
+__device__ __forceinline__ double exp_neg(double x) {
+  const double n = rint(x * 1.4426950408889634);
+  double r = fma(n, -6.93147180559945286e-01, x);
+  r = fma(n, -2.319046813846299558e-17, r);
+  double p = c_expm[11];
+#pragma unroll
+  for (int k = 10; k >= 0; --k) p = fma(p, r, c_expm[k]);
+  const long long ni = (long long)n;
+  return __longlong_as_double(__double_as_longlong(p) + (ni << 52));
 }
 
 // K6: ordered-pair real-space kernel.  One warp = up to 32 centre particles of
@@ -661,24 +782,14 @@ __device__ __forceinline__ double rs_r2(double dx, double dy, double dz) {
   return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
 }
 
-// shift code per axis: 0 -> -L, 1 -> 0, 2 -> +L, 3 -> fold per pair
-template <int AX>
-__device__ __forceinline__ double rs_axis(double xi, double xj, int code, double L, double hl) {
-  double d = __dsub_rn(xi, xj);
-  if (code == 3) {
-    if (d >= hl)
-      d = __dsub_rn(d, L);
-    else if (d < -hl)
-      d = __dadd_rn(d, L);
-  } else if (code != 1) {
-    d = __dadd_rn(d, code == 2 ? L : -L);
-  }
-  return d;
-}
-
+// pair-list entry: x = j (sorted index), y = g | kx<<4 | ky<<6 | kz<<8 with
+// k = 0: -L, 1: 0, 2: +L, 3: fold per pair
 constexpr int K6_LIST = 32 * K6_G + 32;  // pending pairs per warp
 
-__global__ void __launch_bounds__(K6_WARPS * 32)
+#ifndef K6_MINB
+#define K6_MINB 4
+#endif
+__global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
     k6_real_space(const double4 *__restrict__ sorted, const int *__restrict__ sorted_cell,
                   const int *__restrict__ order, const int *__restrict__ cell_start,
                   const int *__restrict__ row_ustart, RSParams P, double *__restrict__ force,
@@ -727,39 +838,124 @@ __global__ void __launch_bounds__(K6_WARPS * 32)
     int cnt = 0;  // pending pairs (warp-uniform)
     bool coincident = false;
 
+    // Each accepted pair stores, per axis, which image the reference's fold
+    // chose (k = 0: d - L, 1: d, 2: d + L; engine.py:117-131), so the
+    // evaluation recomputes d = fl(fl(xi - xj) + shift_k) bit-identically
+    // without branches.
+    auto shift = [&](uint32_t k) { return k == 0u ? -P.L : (k == 2u ? P.L : 0.0); };
+    // one pair: force factor gg (0 for a coincident pair); accumulates energy
+    auto pair_eval = [&](const uint2 e, double &dx, double &dy, double &dz, double &gg) {
+      const int j = (int)e.x;
+      const int g = (int)(e.y & 15u);
+      const double4 pj = sorted[j];
+      const double4 pi = s_i[warp][g];
+      dx = __dadd_rn(__dsub_rn(pi.x, pj.x), shift((e.y >> 4) & 3u));
+      dy = __dadd_rn(__dsub_rn(pi.y, pj.y), shift((e.y >> 6) & 3u));
+      dz = __dadd_rn(__dsub_rn(pi.z, pj.z), shift((e.y >> 8) & 3u));
+      const double r2raw = rs_r2(dx, dy, dz);
+      const bool zero = r2raw == 0.0;
+      coincident |= zero;
+      const double r2 = zero ? 1.0 : r2raw;
+      // sc = erfc(sqrt(alpha) r)/r, g = qq (sc + 2 sqrt(alpha/pi) e^{-alpha r^2})/r^2
+      // (ewald.py:214-218), with one exp shared by erfc and the force
+      const double qq = zero ? 0.0 : pi.w * pj.w;
+      const double inv_r = rsqrt_pos(r2);
+      const double r = r2 * inv_r;
+      const double ex = exp_neg(-P.al * r2);
+      const double sc = erfc_from_exp(P.sa * r, ex, s_erfcx) * inv_r;
+      ue = fma(0.5 * qq, sc, ue);
+      gg = qq * fma(P.tsap, ex, sc) * (inv_r * inv_r);
+    };
+    auto accum = [&](const uint2 e, double dx, double dy, double dz, double gg) {
+      const int g = (int)(e.y & 15u);
+      double3 f = s_f[warp][g][lane];
+      f.x = fma(gg, dx, f.x);
+      f.y = fma(gg, dy, f.y);
+      f.z = fma(gg, dz, f.z);
+      s_f[warp][g][lane] = f;
+    };
+    // evaluate entries [base, base+n) (n <= 32): lane l takes entry base+l
     auto round = [&](const int base, const int n) {
       if (lane < n) {
         const uint2 e = s_list[warp][base + lane];
-        const int j = (int)e.x;
-        const int g = (int)(e.y & 15u);
-        const double4 pj = sorted[j];
-        const double4 pi = s_i[warp][g];
-        const double dx = rs_axis<0>(pi.x, pj.x, (e.y >> 4) & 3, P.L, P.hl);
-        const double dy = rs_axis<1>(pi.y, pj.y, (e.y >> 6) & 3, P.L, P.hl);
-        const double dz = rs_axis<2>(pi.z, pj.z, (e.y >> 8) & 3, P.L, P.hl);
-        const double r2 = rs_r2(dx, dy, dz);
-        if (r2 == 0.0) {
-          coincident = true;
-        } else {
-          // sc = erfc(sqrt(alpha) r)/r, g = qq (sc + 2 sqrt(alpha/pi) e^{-alpha r^2})/r^2
-          // (ewald.py:214-218), with one exp shared by erfc and the force
-          const double qq = pi.w * pj.w;
-          const double inv_r = rsqrt(r2);
-          const double r = r2 * inv_r;
-          const double ex = exp(-P.al * r2);
-          const double sc = erfc_from_exp(P.sa * r, ex, s_erfcx) * inv_r;
-          ue += 0.5 * qq * sc;
-          const double gg = qq * fma(P.tsap, ex, sc) * (inv_r * inv_r);
-          double3 f = s_f[warp][g][lane];
-          f.x = fma(gg, dx, f.x);
-          f.y = fma(gg, dy, f.y);
-          f.z = fma(gg, dz, f.z);
-          s_f[warp][g][lane] = f;
+        double dx, dy, dz, gg;
+        pair_eval(e, dx, dy, dz, gg);
+        accum(e, dx, dy, dz, gg);
+      }
+    };
+    // 64 entries, two independent pairs per lane (ILP)
+    auto round2 = [&](const int base) {
+      const uint2 e0 = s_list[warp][base + lane];
+      const uint2 e1 = s_list[warp][base + 32 + lane];
+      double dx0, dy0, dz0, g0, dx1, dy1, dz1, g1;
+      pair_eval(e0, dx0, dy0, dz0, g0);
+      pair_eval(e1, dx1, dy1, dz1, g1);
+      accum(e0, dx0, dy0, dz0, g0);
+      accum(e1, dx1, dy1, dz1, g1);
+    };
+    auto drain = [&]() {
+      __syncwarp();
+      int base = 0;
+      for (; cnt - base >= 64; base += 64) round2(base);
+      if (cnt - base >= 32) {
+        round(base, 32);
+        base += 32;
+      }
+      const int rest = cnt - base;
+      __syncwarp();
+      const uint2 mv = lane < rest ? s_list[warp][base + lane] : make_uint2(0u, 0u);
+      __syncwarp();
+      if (lane < rest) s_list[warp][lane] = mv;
+      __syncwarp();
+      cnt = rest;
+    };
+    // candidate step: lane = candidate j, test all centres.  FX / FYZ:
+    // fold x / y,z per pair (reference rule), else add the piece's shift.
+    auto test_range = [&](auto fx_tag, auto fyz_tag, const int jb, const int je, const double sx,
+                          const double sy, const double sz, const uint32_t tag) {
+      constexpr bool FX = decltype(fx_tag)::value;
+      constexpr bool FYZ = decltype(fyz_tag)::value;
+      auto fold = [&](double d, uint32_t &k) {
+        k = d >= P.hl ? 0u : (d < -P.hl ? 2u : 1u);
+        return k == 1u ? d : (k == 0u ? __dsub_rn(d, P.L) : __dadd_rn(d, P.L));
+      };
+      for (int j0 = jb; j0 < je; j0 += 32) {
+        const int j = j0 + lane;
+        const bool vj = j < je;
+        const double4 pj = sorted[vj ? j : jb];
+#pragma unroll
+        for (int g = 0; g < K6_G; ++g) {
+          if (g < gi) {
+            const double4 pi = s_i[warp][g];
+            uint32_t kx = 1u, ky = 1u, kz = 1u;
+            double dx = __dsub_rn(pi.x, pj.x);
+            double dy = __dsub_rn(pi.y, pj.y);
+            double dz = __dsub_rn(pi.z, pj.z);
+            if (FX) dx = fold(dx, kx); else dx = __dadd_rn(dx, sx);
+            if (FYZ) {
+              dy = fold(dy, ky);
+              dz = fold(dz, kz);
+            } else {
+              dy = __dadd_rn(dy, sy);
+              dz = __dadd_rn(dz, sz);
+            }
+            const double r2 = rs_r2(dx, dy, dz);
+            const bool acc = vj && (r2 < P.rc2) && (j != first + g);
+            const unsigned bal = __ballot_sync(0xffffffffu, acc);
+            if (acc) {
+              uint32_t t = tag | (uint32_t)g;
+              if (FX) t = (t & ~(3u << 4)) | (kx << 4);
+              if (FYZ) t = (t & ~(15u << 6)) | (ky << 6) | (kz << 8);
+              s_list[warp][cnt + __popc(bal & lt_mask)] = make_uint2((uint32_t)j, t);
+            }
+            cnt += __popc(bal);
+          }
         }
+        if (cnt >= 32) drain();
       }
     };
 
-    // candidate pieces: contiguous cell runs along x with one image code
+    // candidate pieces: contiguous cell runs along x with one image shift
     int cy = 0, cz = 0, xa = 0, xb = 0;
     bool wide = true;
     if (!P.fold) {
@@ -771,90 +967,36 @@ __global__ void __launch_bounds__(K6_WARPS * 32)
       xa = wide ? 0 : cx_lo - R;
       xb = wide ? cpd - 1 : cx_hi + R;
     }
-    const int nyz = P.fold ? 1 : (2 * R + 1) * (2 * R + 1);
-    for (int yz = 0; yz < nyz; ++yz) {
-      int ny = 0, nz = 0, kyc = 3, kzc = 3;
-      if (!P.fold) {
-        ny = cy + yz % (2 * R + 1) - R;
-        nz = cz + yz / (2 * R + 1) - R;
-        kyc = 1;
-        kzc = 1;
-        if (ny < 0) { ny += cpd; kyc = 2; } else if (ny >= cpd) { ny -= cpd; kyc = 0; }
-        if (nz < 0) { nz += cpd; kzc = 2; } else if (nz >= cpd) { nz -= cpd; kzc = 0; }
-      }
-      for (int piece = 0; piece < 3; ++piece) {
-        int jb, je, kxc;
-        if (P.fold) {
-          if (piece) break;
-          jb = 0;
-          je = (int)P.n;
-          kxc = 3;
-        } else if (wide) {
-          if (piece) break;
-          const int cb = cpd * (ny + cpd * nz);
-          jb = cell_start[cb];
-          je = cell_start[cb + cpd];
-          kxc = 3;
-        } else {
+    using T_ = std::integral_constant<bool, true>;
+    using F_ = std::integral_constant<bool, false>;
+    if (P.fold) {
+      // fewer than 2R+1 cells per edge: every particle is a candidate and
+      // every axis folds per pair (the reference's scan-all branch)
+      test_range(T_{}, T_{}, 0, (int)P.n, 0.0, 0.0, 0.0, 0u);
+    } else {
+      for (int yz = 0; yz < (2 * R + 1) * (2 * R + 1); ++yz) {
+        int ny = cy + yz % (2 * R + 1) - R;
+        int nz = cz + yz / (2 * R + 1) - R;
+        uint32_t kyc = 1u, kzc = 1u;
+        if (ny < 0) { ny += cpd; kyc = 2u; } else if (ny >= cpd) { ny -= cpd; kyc = 0u; }
+        if (nz < 0) { nz += cpd; kzc = 2u; } else if (nz >= cpd) { nz -= cpd; kzc = 0u; }
+        const double sy = shift(kyc), sz = shift(kzc);
+        const int cb = cpd * (ny + cpd * nz);
+        if (wide) {
+          test_range(T_{}, F_{}, cell_start[cb], cell_start[cb + cpd], 0.0, sy, sz,
+                     (kyc << 6) | (kzc << 8));
+          continue;
+        }
+        for (int piece = 0; piece < 3; ++piece) {
           int x0, x1;
-          if (piece == 0) { x0 = xa; x1 = min(xb, -1); kxc = 2; }           // wrapped from the top
-          else if (piece == 1) { x0 = max(xa, 0); x1 = min(xb, cpd - 1); kxc = 1; }
-          else { x0 = max(xa, cpd); x1 = xb; kxc = 0; }                      // wrapped from the bottom
+          uint32_t kxc;
+          if (piece == 0) { x0 = xa; x1 = min(xb, -1); kxc = 2u; }           // wrapped from the top
+          else if (piece == 1) { x0 = max(xa, 0); x1 = min(xb, cpd - 1); kxc = 1u; }
+          else { x0 = max(xa, cpd); x1 = xb; kxc = 0u; }                      // wrapped from the bottom
           if (x0 > x1) continue;
           const int off = piece == 0 ? cpd : (piece == 2 ? -cpd : 0);
-          const int cb = cpd * (ny + cpd * nz);
-          jb = cell_start[cb + x0 + off];
-          je = cell_start[cb + x1 + off + 1];
-        }
-        const double sx = kxc == 2 ? P.L : -P.L;
-        const double sy = kyc == 2 ? P.L : -P.L;
-        const double sz = kzc == 2 ? P.L : -P.L;
-        const uint32_t tag = ((uint32_t)kxc << 4) | ((uint32_t)kyc << 6) | ((uint32_t)kzc << 8);
-        for (int j0 = jb; j0 < je; j0 += 32) {
-          const int j = j0 + lane;
-          const bool vj = j < je;
-          const double4 pj = sorted[vj ? j : jb];
-#pragma unroll
-          for (int g = 0; g < K6_G; ++g) {
-            if (g < gi) {
-              const double4 pi = s_i[warp][g];
-              double dx = __dsub_rn(pi.x, pj.x);
-              double dy = __dsub_rn(pi.y, pj.y);
-              double dz = __dsub_rn(pi.z, pj.z);
-              if (kxc == 3) {
-                if (dx >= P.hl) dx = __dsub_rn(dx, P.L); else if (dx < -P.hl) dx = __dadd_rn(dx, P.L);
-              } else if (kxc != 1) {
-                dx = __dadd_rn(dx, sx);
-              }
-              if (kyc == 3) {
-                if (dy >= P.hl) dy = __dsub_rn(dy, P.L); else if (dy < -P.hl) dy = __dadd_rn(dy, P.L);
-              } else if (kyc != 1) {
-                dy = __dadd_rn(dy, sy);
-              }
-              if (kzc == 3) {
-                if (dz >= P.hl) dz = __dsub_rn(dz, P.L); else if (dz < -P.hl) dz = __dadd_rn(dz, P.L);
-              } else if (kzc != 1) {
-                dz = __dadd_rn(dz, sz);
-              }
-              const double r2 = rs_r2(dx, dy, dz);
-              const bool acc = vj && (r2 < P.rc2) && (j != first + g);
-              const unsigned bal = __ballot_sync(0xffffffffu, acc);
-              if (acc) s_list[warp][cnt + __popc(bal & lt_mask)] = make_uint2((uint32_t)j, tag | g);
-              cnt += __popc(bal);
-            }
-          }
-          if (cnt >= 32) {
-            __syncwarp();
-            int base = 0;
-            for (; cnt - base >= 32; base += 32) round(base, 32);
-            const int rest = cnt - base;
-            __syncwarp();
-            const uint2 mv = lane < rest ? s_list[warp][base + lane] : make_uint2(0u, 0u);
-            __syncwarp();
-            if (lane < rest) s_list[warp][lane] = mv;
-            __syncwarp();
-            cnt = rest;
-          }
+          test_range(F_{}, F_{}, cell_start[cb + x0 + off], cell_start[cb + x1 + off + 1],
+                     shift(kxc), sy, sz, (kxc << 4) | (kyc << 6) | (kzc << 8));
         }
       }
     }
@@ -994,7 +1136,12 @@ struct DBuf {
   size_t cap = 0;
   cudaError_t ensure(size_t bytes) {
     if (bytes <= cap && p) return cudaSuccess;
-    if (p) cudaFree(p);
+    if (p) {
+      // growth is rare; make sure no queued kernel still uses the old buffer
+      cudaError_t e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) return e;
+      cudaFree(p);
+    }
     p = nullptr;
     cap = 0;
     if (bytes == 0) bytes = 16;
@@ -1018,12 +1165,13 @@ struct Plan {
   int M = 0, n_items = 0, n_rows = 0, n_tiles = 0, ts_max = 0, pchunk = K1_PMAX;
   std::vector<int> row_item_prefix;  // n_rows+1
   DBuf item_tab, item_my, item_row, rows, tab_desc, tile_off, tile_ts, slot_k, slot_coeff;
-  DBuf ks_rows;
-  int ks_cached = -1;
+  std::vector<std::pair<int, DBuf>> ks_cache;  // n_ks -> row boundaries
   void release() {
     for (DBuf *b : {&item_tab, &item_my, &item_row, &rows, &tab_desc, &tile_off, &tile_ts,
-                    &slot_k, &slot_coeff, &ks_rows})
+                    &slot_k, &slot_coeff})
       b->release();
+    for (auto &c : ks_cache) c.second.release();
+    ks_cache.clear();
   }
 };
 
@@ -1081,19 +1229,14 @@ namespace {
 
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
-// number of blocks along the split axis minimising ceil(tiles*s/slots)/s
-int best_split(int64_t tiles, int64_t slots, int max_split) {
-  int best = 1;
-  double best_cost = 1e300;
-  for (int s = 1; s <= max_split; ++s) {
-    const double waves = std::ceil((double)(tiles * s) / (double)slots);
-    const double cost = waves / s;
-    if (cost < best_cost * (1.0 - 1e-9)) {
-      best_cost = cost;
-      best = s;
-    }
-  }
-  return best;
+// Split factor along the reduction axis: fill whole waves of resident
+// blocks with the fewest splits (each split costs a partial-sum buffer that
+// a second kernel must reduce), never below min_work units per block.
+int split_for(int64_t tiles, int64_t slots, int64_t work, int64_t min_work) {
+  const int64_t waves = std::max<int64_t>(1, (tiles + slots - 1) / slots);
+  int64_t s = std::max<int64_t>(1, (waves * slots) / std::max<int64_t>(1, tiles));
+  const int64_t cap = std::max<int64_t>(1, work / std::max<int64_t>(1, min_work));
+  return (int)std::min(s, cap);
 }
 
 template <class T>
@@ -1106,6 +1249,7 @@ int upload(ewb_handle *h, DBuf &b, const std::vector<T> &v) {
 // Host planning of the k-space work decomposition.
 int build_plan(ewb_handle *h, const int64_t *m, int64_t K, const double *coeff) {
   Plan &P = h->plan;
+  CK(cudaStreamSynchronize(h->stream));  // queued kernels may read the old plan
   if (K <= 0) return h->fail(EWB_EKSPACE, "empty reciprocal-space table");
   for (int64_t i = 0; i < 3 * K; ++i)
     if (m[i] > 1000000 || m[i] < -1000000)
@@ -1217,8 +1361,9 @@ int build_plan(ewb_handle *h, const int64_t *m, int64_t K, const double *coeff) 
   P.n_rows = n_rows;
   P.n_tiles = n_tiles;
   P.ts_max = ts_max;
-  P.pchunk = std::max(1, std::min(K1_PMAX, (160 * 1024) / (16 * ts_max)));
-  P.ks_cached = -1;
+  P.pchunk = std::max(1, std::min(K1_PMAX, (K1_TAB_BYTES) / (16 * (ts_max | 1))));
+  for (auto &c : P.ks_cache) c.second.release();
+  P.ks_cache.clear();
   int rc;
   if ((rc = upload(h, P.item_tab, item_tab))) return rc;
   if ((rc = upload(h, P.item_my, item_my))) return rc;
@@ -1232,9 +1377,12 @@ int build_plan(ewb_handle *h, const int64_t *m, int64_t K, const double *coeff) 
   return EWB_OK;
 }
 
-int ensure_ks(ewb_handle *h, int n_ks) {
+// k-split row boundaries for n_ks splits; cached per n_ks so a buffer a
+// queued kernel may still read is never overwritten
+const int *ensure_ks(ewb_handle *h, int n_ks, int *status) {
   Plan &P = h->plan;
-  if (P.ks_cached == n_ks) return EWB_OK;
+  for (auto &c : P.ks_cache)
+    if (c.first == n_ks) return c.second.as<int>();
   std::vector<int> b(n_ks + 1);
   b[0] = 0;
   b[n_ks] = P.n_rows;
@@ -1244,10 +1392,18 @@ int ensure_ks(ewb_handle *h, int n_ks) {
                   P.row_item_prefix.begin());
     b[q] = std::max(b[q - 1], std::min(r, P.n_rows));
   }
-  int rc = upload(h, P.ks_rows, b);
-  if (rc) return rc;
-  P.ks_cached = n_ks;
-  return EWB_OK;
+  P.ks_cache.emplace_back(n_ks, DBuf());
+  DBuf &buf = P.ks_cache.back().second;
+  cudaError_t e = buf.ensure(b.size() * sizeof(int));
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(buf.p, b.data(), b.size() * sizeof(int), cudaMemcpyHostToDevice,
+                        h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);  // b is a local vector
+  if (e != cudaSuccess) {
+    *status = h->fail(EWB_ECUDA, std::string("k-split upload: ") + cudaGetErrorString(e));
+    return nullptr;
+  }
+  return buf.as<int>();
 }
 
 int require_state(ewb_handle *h, bool need_kspace, bool need_loaded) {
@@ -1294,25 +1450,31 @@ int occupancy_k1(ewb_handle *h, int M, size_t smem, int *occ_out) {
 int stage_rho(ewb_handle *h, int64_t i0, int64_t i1, int *n_part_out) {
   Plan &P = h->plan;
   const int M = P.M;
-  const size_t smem = (size_t)P.pchunk * P.ts_max * sizeof(double2);
+  const size_t smem = 2 * (size_t)P.pchunk * (P.ts_max | 1) * sizeof(double2) +
+                      (size_t)P.ts_max * sizeof(int4);
   int occ = 1;
   int rc = occupancy_k1(h, M, smem, &occ);
   if (rc) return rc;
   const int64_t n = std::max<int64_t>(0, i1 - i0);
-  const int64_t max_pc = std::max<int64_t>(1, std::min<int64_t>(4096, (n + 31) / 32));
-  int n_pc = best_split(P.n_tiles, (int64_t)h->n_sm * occ, (int)max_pc);
-  int64_t ppb = (n + n_pc - 1) / std::max(1, n_pc);
+  // many short blocks (they desynchronise the table-build phases of
+  // co-resident blocks), bounded by the partial-sum buffer size
+  const size_t slot_bytes = (size_t)M * P.n_items * sizeof(double2);
+  int64_t n_pc = std::max<int64_t>(1, (n + K1_PPB - 1) / K1_PPB);
+  n_pc = std::min<int64_t>(n_pc, std::max<int64_t>(1, (int64_t)(K1_PART_BYTES / slot_bytes)));
+  n_pc = std::max<int64_t>(n_pc, split_for(P.n_tiles, (int64_t)h->n_sm * occ, n, 64));
+  n_pc = std::min<int64_t>(n_pc, std::max<int64_t>(1, n));
+  int64_t ppb = (n + n_pc - 1) / std::max<int64_t>(1, n_pc);
   ppb = std::max<int64_t>(1, ppb);
-  n_pc = (int)std::max<int64_t>(1, (n + ppb - 1) / ppb);
+  n_pc = std::max<int64_t>(1, (n + ppb - 1) / ppb);
   const size_t n_slots = (size_t)M * P.n_items;
   CK(h->spart.ensure((size_t)n_pc * n_slots * sizeof(double2)));
-  dim3 grid(P.n_tiles, n_pc);
+  dim3 grid(P.n_tiles, (unsigned)n_pc);
   k1_table(M)<<<grid, K1_THREADS, smem, h->stream>>>(
       h->frac.as<double4>(), h->base.as<double2>(), i0, std::max(i0, i1), ppb, P.pchunk,
       P.item_tab.as<int2>(), P.n_items, P.tab_desc.as<int4>(), P.tile_off.as<int>(),
       P.tile_ts.as<int>(), h->spart.as<double2>());
   CKL();
-  *n_part_out = n_pc;
+  *n_part_out = (int)n_pc;
   return EWB_OK;
 }
 
@@ -1350,15 +1512,19 @@ int stage_recip_forces(ewb_handle *h, int64_t i0, int64_t i1, double *d_force, b
     occ = std::max(1, occ);
   }
   const int64_t ptiles = (n_local + K3_THREADS * K3_PPT - 1) / (K3_THREADS * K3_PPT);
-  const int max_ks = std::max(1, std::min(P.n_rows, 64));
-  const int n_ks = best_split(ptiles, (int64_t)h->n_sm * occ, max_ks);
-  int rc = ensure_ks(h, n_ks);
-  if (rc) return rc;
+  // enough k-splits for K3_WAVES waves of resident blocks (short blocks
+  // balance the tail), each split keeping >= 2 rows
+  const int64_t slots3 = (int64_t)h->n_sm * occ;
+  int n_ks = (int)std::max<int64_t>(1, (K3_WAVES * slots3 + ptiles - 1) / ptiles);
+  n_ks = std::max(1, std::min(n_ks, std::max(1, P.n_rows / 2)));
+  int rc = EWB_OK;
+  const int *ks_rows = ensure_ks(h, n_ks, &rc);
+  if (!ks_rows) return rc;
   CK(h->fpart.ensure((size_t)n_ks * 3 * n_local * sizeof(double)));
   if (energy) CK(h->upart.ensure((size_t)n_ks * n_local * sizeof(double)));
   dim3 grid((unsigned)ptiles, n_ks);
   fn<<<grid, K3_THREADS, 0, h->stream>>>(h->frac.as<double4>(), h->base.as<double2>(), i0, i1,
-                                         P.rows.as<int4>(), P.ks_rows.as<int>(),
+                                         P.rows.as<int4>(), ks_rows,
                                          P.item_my.as<int>(), P.item_row.as<int>(),
                                          h->sp.as<double2>(), P.n_items, h->fpart.as<double>(),
                                          energy ? h->upart.as<double>() : nullptr);

@@ -1,0 +1,75 @@
+"""Summarise ncu artefacts for profiles/: per-kernel duration, FP64 pipe and
+issue utilisation, DRAM bytes, occupancy, top stall reasons (from a
+--set full report), and per-kernel share of the step (from a launch list)."""
+import csv
+import io
+import subprocess
+import sys
+from collections import defaultdict
+
+KEYS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "fp64 pipe % (active)"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
+    ("smsp__thread_inst_executed_per_inst_executed.ratio", "active threads/warp"),
+    ("dram__bytes_read.sum", "dram read"),
+    ("dram__bytes_write.sum", "dram write"),
+    ("launch__registers_per_thread", "registers/thread"),
+    ("launch__grid_size", "grid"),
+    ("sm__cycles_elapsed.avg.per_second", "SM clock"),
+]
+
+
+def full_report(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units, data = rows[0], rows[1], rows[2:]
+    ki = hdr.index("Kernel Name")
+    lines = []
+    for r in data:
+        name = r[ki].split("(")[0].replace("void ", "").replace("<unnamed>::", "")
+        lines.append(f"### {name}")
+        for k, lab in KEYS:
+            if k in hdr:
+                i = hdr.index(k)
+                lines.append(f"- {lab}: {r[i]} {units[i]}")
+        st = []
+        for i, h in enumerate(hdr):
+            if h.startswith("smsp__average_warps_issue_stalled") and h.endswith("per_issue_active.ratio"):
+                try:
+                    v = float(r[i])
+                except ValueError:
+                    continue
+                nm = h.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", "")
+                if nm != "selected":
+                    st.append((v, nm))
+        st.sort(reverse=True)
+        lines.append("- top stalls (warps per issue): " + ", ".join(f"{n} {v:.2f}" for v, n in st[:5]))
+        lines.append("")
+    return "\n".join(lines)
+
+
+def launch_list(path, skip_prefix=None):
+    rows = list(csv.reader(open(path)))
+    h = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    hdr = rows[h]
+    ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
+    tot = defaultdict(float)
+    cnt = defaultdict(int)
+    for r in rows[h + 1:]:
+        name = r[ki].split("(")[0].replace("void ", "").replace("<unnamed>::", "")
+        v = float(r[vi].replace(",", ""))
+        tot[name] += v
+        cnt[name] += 1
+    s = sum(tot.values())
+    lines = ["| kernel | launches | total ns | share |", "|---|---|---|---|"]
+    for k, v in sorted(tot.items(), key=lambda x: -x[1]):
+        lines.append(f"| {k} | {cnt[k]} | {v:.0f} | {100 * v / s:.1f}% |")
+    return "\n".join(lines)
+
+
+if __name__ == "__main__":
+    kind, path = sys.argv[1], sys.argv[2]
+    print(full_report(path) if kind == "full" else launch_list(path))

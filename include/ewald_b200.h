@@ -67,6 +67,12 @@ int ewb_set_max_segment(ewb_handle *h, int mcap);
  * per edge), 1 = r_c cells with the 3^3 stencil (the reference's grid). */
 int ewb_set_stencil(ewb_handle *h, int rad);
 
+/* 0 (default): real space visits each unordered pair once and scatters
+ * the partner's force with fp64 atomics (fastest; summation order varies
+ * run to run at the 1e-16 level).  1: ordered pairs, write-to-centre only
+ * (engine.py:10-14) -- bitwise reproducible, ~1.6x more real-space work. */
+int ewb_set_deterministic(ewb_handle *h, int on);
+
 /* EwaldParams: box edge L, screening alpha (A^-2, erfc(sqrt(alpha) r)),
  * real-space cutoff.  rc2 is r_cutoff**2 as the caller computed it, so the
  * cutoff predicate r2 < rc2 is bit-identical to the reference's. */

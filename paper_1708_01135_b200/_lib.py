@@ -44,6 +44,7 @@ SIGNATURES = {
     "ewb_set_stream": (_INT, [_P, ctypes.c_size_t]),
     "ewb_set_max_segment": (_INT, [_P, _INT]),
     "ewb_set_stencil": (_INT, [_P, _INT]),
+    "ewb_set_deterministic": (_INT, [_P, _INT]),
     "ewb_set_system": (_INT, [_P, _D, _D, _D, _D]),
     "ewb_set_kspace": (_INT, [_P, _P, _I64, _P]),
     "ewb_kspace_info": (_INT, [_P, _P]),
@@ -172,6 +173,9 @@ class Handle:
     def set_max_segment(self, mcap):
         self._check(self.lib.ewb_set_max_segment(self.h, int(mcap)))
         self.kspace_key = None
+
+    def set_deterministic(self, on):
+        self._check(self.lib.ewb_set_deterministic(self.h, 1 if on else 0))
 
     def set_stencil(self, rad):
         self._check(self.lib.ewb_set_stencil(self.h, int(rad)))

@@ -757,6 +757,7 @@ __device__ __forceinline__ double exp_neg(double x) {
 struct RSParams {
   double L, hl, rc2, sa, al, tsap;
   int cpd, fold, rad;  // rad: stencil radius in cells (1 or 2)
+  int half;            // 1: each unordered pair once (Newton 3rd law, atomics)
   int c_lo, c_hi;
   int64_t n;
 };
@@ -863,7 +864,7 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
       const double r = r2 * inv_r;
       const double ex = exp_neg(-P.al * r2);
       const double sc = erfc_from_exp(P.sa * r, ex, s_erfcx) * inv_r;
-      ue = fma(0.5 * qq, sc, ue);
+      ue = fma(P.half ? qq : 0.5 * qq, sc, ue);  // ordered pairs carry 1/2 (ewald.py:217)
       gg = qq * fma(P.tsap, ex, sc) * (inv_r * inv_r);
     };
     auto accum = [&](const uint2 e, double dx, double dy, double dz, double gg) {
@@ -873,6 +874,12 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
       f.y = fma(gg, dy, f.y);
       f.z = fma(gg, dz, f.z);
       s_f[warp][g][lane] = f;
+      if (P.half) {  // F_j = -F_i for the same pair (r2 is symmetric bitwise)
+        const int64_t o = order[e.x];
+        atomicAdd(force + 3 * o, -gg * dx);
+        atomicAdd(force + 3 * o + 1, -gg * dy);
+        atomicAdd(force + 3 * o + 2, -gg * dz);
+      }
     };
     // evaluate entries [base, base+n) (n <= 32): lane l takes entry base+l
     auto round = [&](const int base, const int n) {
@@ -911,8 +918,9 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
     };
     // candidate step: lane = candidate j, test all centres.  FX / FYZ:
     // fold x / y,z per pair (reference rule), else add the piece's shift.
+    // after: candidates must satisfy j > i (half shell, same row / scan-all)
     auto test_range = [&](auto fx_tag, auto fyz_tag, const int jb, const int je, const double sx,
-                          const double sy, const double sz, const uint32_t tag) {
+                          const double sy, const double sz, const uint32_t tag, const bool after) {
       constexpr bool FX = decltype(fx_tag)::value;
       constexpr bool FYZ = decltype(fyz_tag)::value;
       auto fold = [&](double d, uint32_t &k) {
@@ -940,7 +948,7 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
               dz = __dadd_rn(dz, sz);
             }
             const double r2 = rs_r2(dx, dy, dz);
-            const bool acc = vj && (r2 < P.rc2) && (j != first + g);
+            const bool acc = vj && (r2 < P.rc2) && (after ? j > first + g : j != first + g);
             const unsigned bal = __ballot_sync(0xffffffffu, acc);
             if (acc) {
               uint32_t t = tag | (uint32_t)g;
@@ -972,11 +980,17 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
     if (P.fold) {
       // fewer than 2R+1 cells per edge: every particle is a candidate and
       // every axis folds per pair (the reference's scan-all branch)
-      test_range(T_{}, T_{}, 0, (int)P.n, 0.0, 0.0, 0.0, 0u);
+      test_range(T_{}, T_{}, P.half ? first : 0, (int)P.n, 0.0, 0.0, 0.0, 0u, P.half != 0);
     } else {
       for (int yz = 0; yz < (2 * R + 1) * (2 * R + 1); ++yz) {
-        int ny = cy + yz % (2 * R + 1) - R;
-        int nz = cz + yz / (2 * R + 1) - R;
+        const int oy = yz % (2 * R + 1) - R, oz = yz / (2 * R + 1) - R;
+        // half shell: rows with (oz, oy) lexicographically positive, plus
+        // this row restricted to j > i; the opposite rows find the pair
+        // from the other particle's unit
+        if (P.half && (oz < 0 || (oz == 0 && oy < 0))) continue;
+        const bool self_row = P.half && oz == 0 && oy == 0;
+        int ny = cy + oy;
+        int nz = cz + oz;
         uint32_t kyc = 1u, kzc = 1u;
         if (ny < 0) { ny += cpd; kyc = 2u; } else if (ny >= cpd) { ny -= cpd; kyc = 0u; }
         if (nz < 0) { nz += cpd; kzc = 2u; } else if (nz >= cpd) { nz -= cpd; kzc = 0u; }
@@ -984,7 +998,7 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
         const int cb = cpd * (ny + cpd * nz);
         if (wide) {
           test_range(T_{}, F_{}, cell_start[cb], cell_start[cb + cpd], 0.0, sy, sz,
-                     (kyc << 6) | (kzc << 8));
+                     (kyc << 6) | (kzc << 8), self_row);
           continue;
         }
         for (int piece = 0; piece < 3; ++piece) {
@@ -995,8 +1009,11 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
           else { x0 = max(xa, cpd); x1 = xb; kxc = 0u; }                      // wrapped from the bottom
           if (x0 > x1) continue;
           const int off = piece == 0 ? cpd : (piece == 2 ? -cpd : 0);
-          test_range(F_{}, F_{}, cell_start[cb + x0 + off], cell_start[cb + x1 + off + 1],
-                     shift(kxc), sy, sz, (kxc << 4) | (kyc << 6) | (kzc << 8));
+          int jb = cell_start[cb + x0 + off];
+          const int je = cell_start[cb + x1 + off + 1];
+          if (self_row) jb = max(jb, first + 1);  // j > i for some centre
+          test_range(F_{}, F_{}, jb, je, shift(kxc), sy, sz,
+                     (kxc << 4) | (kyc << 6) | (kzc << 8), self_row);
         }
       }
     }
@@ -1009,9 +1026,15 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
       const double ax = warp_sum(f.x), ay = warp_sum(f.y), az = warp_sum(f.z);
       if (lane == 0) {
         const int64_t o = order[first + g];
-        force[3 * o] += ax;
-        force[3 * o + 1] += ay;
-        force[3 * o + 2] += az;
+        if (P.half) {  // other warps scatter partner forces into this row
+          atomicAdd(force + 3 * o, ax);
+          atomicAdd(force + 3 * o + 1, ay);
+          atomicAdd(force + 3 * o + 2, az);
+        } else {
+          force[3 * o] += ax;
+          force[3 * o + 1] += ay;
+          force[3 * o + 2] += az;
+        }
       }
     }
   }
@@ -1186,6 +1209,7 @@ struct ewb_handle {
   std::string err;
   int mcap = 28;
   int stencil_rad = 0;  // 0 auto, 1 force r_c cells (testing)
+  int deterministic = 0;  // 1: full-shell real space, no atomics (bitwise reproducible)
   int64_t launches = 0;
   // system
   bool have_system = false;
@@ -1623,6 +1647,7 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
   rp.cpd = cpd_eff;
   rp.fold = fold;
   rp.rad = rad;
+  rp.half = h->deterministic ? 0 : 1;
   rp.n = n;
   // slab of rows (z-layers of cells) owned by this part
   const int zl = (int)((int64_t)cpd_eff * part / nparts), zh = (int)((int64_t)cpd_eff * (part + 1) / nparts);
@@ -1802,6 +1827,12 @@ int ewb_set_stencil(ewb_handle *h, int rad) {
   if (!h) return EWB_EINVAL;
   if (rad < 0 || rad > 2) return h->fail(EWB_EINVAL, "stencil radius must be 0 (auto), 1 or 2");
   h->stencil_rad = rad;
+  return EWB_OK;
+}
+
+int ewb_set_deterministic(ewb_handle *h, int on) {
+  if (!h) return EWB_EINVAL;
+  h->deterministic = on ? 1 : 0;
   return EWB_OK;
 }
 

@@ -316,3 +316,38 @@ def test_stencil_grids_agree(ew, name):
         out.append((res.u_sr, ps.force.copy()))
     assert rel(out[0][0], out[1][0]) <= 1e-13
     assert np.abs(out[0][1] - out[1][1]).max() <= 1e-12 * f_rms(out[1][1])
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c4"])
+def test_half_shell_matches_deterministic_full_shell(ew, name):
+    """Default real space (each unordered pair once + atomics) against the
+    ordered-pair write-to-centre mode (engine.py:10-14)."""
+    from paper_1708_01135_b200 import workloads as wl
+    cfg = wl.make_config(name, seed=0)
+    out = []
+    for det in (False, True):
+        box, ps = system(ew, cfg["pos"], cfg["q"], cfg["L"])
+        p = ew.EwaldParams(cfg["alpha_ref"], cfg["r_cutoff"], 3.0, 1e-6)
+        rs = ew.ReciprocalSpace(box, p, np.array([[1, 0, 0]]))
+        solver = ew.EwaldSolver(box, p, recip=rs)
+        solver.handle.set_deterministic(det)
+        res = solver.evaluate(ps)
+        out.append((res.u_sr, ps.force.copy()))
+    assert rel(out[0][0], out[1][0]) <= 1e-13
+    assert np.abs(out[0][1] - out[1][1]).max() <= 1e-12 * f_rms(out[1][1])
+
+
+def test_deterministic_mode_is_bitwise_reproducible(ew):
+    from paper_1708_01135_b200 import workloads as wl
+    cfg = wl.make_config("c2", seed=0)
+    box, ps = system(ew, cfg["pos"], cfg["q"], cfg["L"])
+    p = ew.EwaldParams(cfg["alpha_ref"], cfg["r_cutoff"], 10.0, 1e-6)
+    rs = ew.ReciprocalSpace(box, p, cfg["m_int"])
+    solver = ew.EwaldSolver(box, p, recip=rs)
+    solver.handle.set_deterministic(True)
+    r1 = solver.evaluate(ps)
+    f1 = ps.force.copy()
+    ps.force[:] = 0.0
+    r2 = solver.evaluate(ps)
+    assert (r1.u_sr, r1.u_lr, r1.u_self) == (r2.u_sr, r2.u_lr, r2.u_self)
+    assert np.array_equal(f1, ps.force)

@@ -66,7 +66,9 @@ constexpr int K3_THREADS = 128;
 constexpr int K3_PPT = 2;         // particles per thread in the gather
 constexpr int K3_CH = 32;         // k-items per shared-memory chunk
 constexpr int K6_WARPS = 4;
-constexpr int K6_G = 8;           // centre particles per real-space warp
+#ifndef K6_G
+#define K6_G 8                    // centre particles per real-space warp
+#endif
 constexpr int SORT_CAP = 4096;    // in-cell deterministic sort capacity
 constexpr int RED_THREADS = 256;
 
@@ -716,9 +718,15 @@ __device__ __forceinline__ double erfc_from_exp(double x, double e, const double
   const int i = min((int)(x * 2.0), ERFCX_NI - 1);
   const double t = fma(4.0, x, -(double)(2 * i + 1));
   const double *c = tab + i * ERFCX_NC;
-  double r = c[ERFCX_NC - 1];
-#pragma unroll
-  for (int k = ERFCX_NC - 2; k >= 0; --k) r = fma(r, t, c[k]);
+  // Estrin's scheme (dependency depth 5 instead of 12 for Horner)
+  static_assert(ERFCX_NC == 13, "Estrin tree below assumes degree 12");
+  const double t2 = t * t, t4 = t2 * t2, t8 = t4 * t4;
+  const double p01 = fma(c[1], t, c[0]), p23 = fma(c[3], t, c[2]);
+  const double p45 = fma(c[5], t, c[4]), p67 = fma(c[7], t, c[6]);
+  const double p89 = fma(c[9], t, c[8]), pab = fma(c[11], t, c[10]);
+  const double q0 = fma(p23, t2, p01), q1 = fma(p67, t2, p45);
+  const double q2 = fma(pab, t2, p89);
+  const double r = fma(fma(c[12], t4, q2), t8, fma(q1, t4, q0));
   return x < 0.5 * ERFCX_NI ? r * e : 0.0;
 }
 
@@ -744,9 +752,12 @@ __device__ __forceinline__ double exp_neg(double x) {
   const double n = rint(x * 1.4426950408889634);
   double r = fma(n, -6.93147180559945286e-01, x);
   r = fma(n, -2.319046813846299558e-17, r);
-  double p = c_expm[11];
-#pragma unroll
-  for (int k = 10; k >= 0; --k) p = fma(p, r, c_expm[k]);
+  // Estrin's scheme (depth 5 instead of 11)
+  const double r2 = r * r, r4 = r2 * r2, r8 = r4 * r4;
+  const double p01 = fma(c_expm[1], r, c_expm[0]), p23 = fma(c_expm[3], r, c_expm[2]);
+  const double p45 = fma(c_expm[5], r, c_expm[4]), p67 = fma(c_expm[7], r, c_expm[6]);
+  const double p89 = fma(c_expm[9], r, c_expm[8]), pab = fma(c_expm[11], r, c_expm[10]);
+  const double p = fma(fma(pab, r2, p89), r8, fma(fma(p67, r2, p45), r4, fma(p23, r2, p01)));
   const long long ni = (long long)n;
   return __longlong_as_double(__double_as_longlong(p) + (ni << 52));
 }
@@ -919,10 +930,12 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
     // candidate step: lane = candidate j, test all centres.  FX / FYZ:
     // fold x / y,z per pair (reference rule), else add the piece's shift.
     // after: candidates must satisfy j > i (half shell, same row / scan-all)
-    auto test_range = [&](auto fx_tag, auto fyz_tag, const int jb, const int je, const double sx,
-                          const double sy, const double sz, const uint32_t tag, const bool after) {
+    auto test_range = [&](auto fx_tag, auto fyz_tag, auto nosh_tag, const int jb, const int je,
+                          const double sx, const double sy, const double sz, const uint32_t tag,
+                          const bool after) {
       constexpr bool FX = decltype(fx_tag)::value;
       constexpr bool FYZ = decltype(fyz_tag)::value;
+      constexpr bool NOSH = decltype(nosh_tag)::value;
       auto fold = [&](double d, uint32_t &k) {
         k = d >= P.hl ? 0u : (d < -P.hl ? 2u : 1u);
         return k == 1u ? d : (k == 0u ? __dsub_rn(d, P.L) : __dadd_rn(d, P.L));
@@ -939,11 +952,13 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
             double dx = __dsub_rn(pi.x, pj.x);
             double dy = __dsub_rn(pi.y, pj.y);
             double dz = __dsub_rn(pi.z, pj.z);
-            if (FX) dx = fold(dx, kx); else dx = __dadd_rn(dx, sx);
+            // (NOSH: no image shift on any axis; fl(d + 0.0) == d up to the
+            // sign of zero, so r2 matches the evaluation's recomputation)
+            if (FX) dx = fold(dx, kx); else if (!NOSH) dx = __dadd_rn(dx, sx);
             if (FYZ) {
               dy = fold(dy, ky);
               dz = fold(dz, kz);
-            } else {
+            } else if (!NOSH) {
               dy = __dadd_rn(dy, sy);
               dz = __dadd_rn(dz, sz);
             }
@@ -980,7 +995,7 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
     if (P.fold) {
       // fewer than 2R+1 cells per edge: every particle is a candidate and
       // every axis folds per pair (the reference's scan-all branch)
-      test_range(T_{}, T_{}, P.half ? first : 0, (int)P.n, 0.0, 0.0, 0.0, 0u, P.half != 0);
+      test_range(T_{}, T_{}, F_{}, P.half ? first : 0, (int)P.n, 0.0, 0.0, 0.0, 0u, P.half != 0);
     } else {
       for (int yz = 0; yz < (2 * R + 1) * (2 * R + 1); ++yz) {
         const int oy = yz % (2 * R + 1) - R, oz = yz / (2 * R + 1) - R;
@@ -997,7 +1012,7 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
         const double sy = shift(kyc), sz = shift(kzc);
         const int cb = cpd * (ny + cpd * nz);
         if (wide) {
-          test_range(T_{}, F_{}, cell_start[cb], cell_start[cb + cpd], 0.0, sy, sz,
+          test_range(T_{}, F_{}, F_{}, cell_start[cb], cell_start[cb + cpd], 0.0, sy, sz,
                      (kyc << 6) | (kzc << 8), self_row);
           continue;
         }
@@ -1012,8 +1027,11 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
           int jb = cell_start[cb + x0 + off];
           const int je = cell_start[cb + x1 + off + 1];
           if (self_row) jb = max(jb, first + 1);  // j > i for some centre
-          test_range(F_{}, F_{}, jb, je, shift(kxc), sy, sz,
-                     (kxc << 4) | (kyc << 6) | (kzc << 8), self_row);
+          const uint32_t tg = (kxc << 4) | (kyc << 6) | (kzc << 8);
+          if (kxc == 1u && kyc == 1u && kzc == 1u)
+            test_range(F_{}, F_{}, T_{}, jb, je, 0.0, 0.0, 0.0, tg, self_row);
+          else
+            test_range(F_{}, F_{}, F_{}, jb, je, shift(kxc), sy, sz, tg, self_row);
         }
       }
     }
@@ -1483,9 +1501,15 @@ int stage_rho(ewb_handle *h, int64_t i0, int64_t i1, int *n_part_out) {
   // many short blocks (they desynchronise the table-build phases of
   // co-resident blocks), bounded by the partial-sum buffer size
   const size_t slot_bytes = (size_t)M * P.n_items * sizeof(double2);
+  const int64_t slots1 = (int64_t)h->n_sm * occ;
   int64_t n_pc = std::max<int64_t>(1, (n + K1_PPB - 1) / K1_PPB);
   n_pc = std::min<int64_t>(n_pc, std::max<int64_t>(1, (int64_t)(K1_PART_BYTES / slot_bytes)));
-  n_pc = std::max<int64_t>(n_pc, split_for(P.n_tiles, (int64_t)h->n_sm * occ, n, 64));
+  // round the grid to whole waves of resident blocks (no partial last wave)
+  {
+    const int64_t waves = std::max<int64_t>(1, (P.n_tiles * n_pc + slots1 - 1) / slots1);
+    const int64_t fit = (waves * slots1) / P.n_tiles;
+    if (fit >= 1) n_pc = std::min<int64_t>(fit, std::max<int64_t>(1, (int64_t)(K1_PART_BYTES / slot_bytes)));
+  }
   n_pc = std::min<int64_t>(n_pc, std::max<int64_t>(1, n));
   int64_t ppb = (n + n_pc - 1) / std::max<int64_t>(1, n_pc);
   ppb = std::max<int64_t>(1, ppb);

@@ -67,6 +67,10 @@ int ewb_set_max_segment(ewb_handle *h, int mcap);
  * per edge), 1 = r_c cells with the 3^3 stencil (the reference's grid). */
 int ewb_set_stencil(ewb_handle *h, int rad);
 
+/* CUDA-graph replay of the evaluation pipeline (default on): the second
+ * evaluate with unchanged shapes/pointers/configuration is captured, later
+ * ones replay the graph.  0 runs every kernel eagerly. */
+int ewb_set_graphs(ewb_handle *h, int on);
 /* 0 (default): real space visits each unordered pair once and scatters
  * the partner's force with fp64 atomics (fastest; summation order varies
  * run to run at the 1e-16 level).  1: ordered pairs, write-to-centre only

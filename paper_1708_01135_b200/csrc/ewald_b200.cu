@@ -769,6 +769,7 @@ struct RSParams {
   double L, hl, rc2, sa, al, tsap;
   int cpd, fold, rad;  // rad: stencil radius in cells (1 or 2)
   int half;            // 1: each unordered pair once (Newton 3rd law, atomics)
+  int jsplit;          // scan-all mode: candidate range split over this many warps
   int c_lo, c_hi;
   int64_t n;
 };
@@ -827,7 +828,9 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
   const int cpd = P.cpd, R = P.rad;
   const int r_lo = P.c_lo, r_hi = P.c_hi;  // row range of this slab
   const int u_lo = row_ustart[r_lo], u_hi = row_ustart[r_hi];
-  const int u = u_lo + blockIdx.x * K6_WARPS + warp;
+  const int uw = blockIdx.x * K6_WARPS + warp;  // (unit, candidate split)
+  const int u = u_lo + uw / P.jsplit;
+  const int jpart = uw % P.jsplit;
   double ue = 0.0;
   if (u < u_hi) {
     int lo = r_lo, hi = r_hi - 1;
@@ -995,7 +998,10 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
     if (P.fold) {
       // fewer than 2R+1 cells per edge: every particle is a candidate and
       // every axis folds per pair (the reference's scan-all branch)
-      test_range(T_{}, T_{}, F_{}, P.half ? first : 0, (int)P.n, 0.0, 0.0, 0.0, 0u, P.half != 0);
+      const int jb0 = P.half ? first : 0, span = (int)P.n - jb0;
+      const int jb = jb0 + (int)((int64_t)span * jpart / P.jsplit);
+      const int je = jb0 + (int)((int64_t)span * (jpart + 1) / P.jsplit);
+      test_range(T_{}, T_{}, F_{}, jb, je, 0.0, 0.0, 0.0, 0u, P.half != 0);
     } else {
       for (int yz = 0; yz < (2 * R + 1) * (2 * R + 1); ++yz) {
         const int oy = yz % (2 * R + 1) - R, oz = yz / (2 * R + 1) - R;
@@ -1172,6 +1178,9 @@ k3_fn k3_table(int M, bool energy) {
 
 // ---------------------------------------------------------------------------
 // host side
+// bumped on every device reallocation: captured graphs bake in pointers
+uint64_t g_realloc_epoch = 0;
+
 struct DBuf {
   void *p = nullptr;
   size_t cap = 0;
@@ -1186,6 +1195,7 @@ struct DBuf {
     p = nullptr;
     cap = 0;
     if (bytes == 0) bytes = 16;
+    ++g_realloc_epoch;
     cudaError_t e = cudaMalloc(&p, bytes);
     if (e == cudaSuccess) cap = bytes;
     return e;
@@ -1242,6 +1252,24 @@ struct ewb_handle {
   DBuf frac, base, xyzq;                     // derived
   DBuf spart, sslot, sp, fpart, upart, eblk, eblk2, energy, errflag;
   DBuf cell_of, slot, count, start, gstart, order_tmp, order, sorted, sorted_cell, row_ustart;
+  // CUDA graph of the device pipeline (prep + real space + S(k) + forces +
+  // self energy), captured on the second call with an unchanged key
+  struct GKey {
+    const void *pos = nullptr, *q = nullptr;
+    void *force = nullptr, *rho = nullptr;
+    int64_t n = -1;
+    bool timed = false;
+    uint64_t gen = 0, epoch = 0;
+    bool operator==(const GKey &o) const {
+      return pos == o.pos && q == o.q && force == o.force && rho == o.rho && n == o.n &&
+             timed == o.timed && gen == o.gen && epoch == o.epoch;
+    }
+  };
+  bool use_graphs = true;
+  uint64_t gen = 0;  // bumped by every configuration change
+  GKey gkey, warm_key;
+  cudaGraphExec_t gexec[5] = {};
+  int64_t glaunch[5] = {};
   int occ_k1[MAXM + 1] = {};
   int occ_k3[MAXM + 1][2] = {};
   bool k1_attr[MAXM + 1] = {};
@@ -1592,8 +1620,9 @@ int stage_recip_forces(ewb_handle *h, int64_t i0, int64_t i1, double *d_force, b
 }
 
 // Cell list + real space for z-slab part/nparts; u_sr into d_u_out.
+constexpr int RS_CELLS = 1, RS_PAIRS = 2;
 int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, double *d_u_out,
-                     cudaEvent_t ev_cell) {
+                     cudaEvent_t ev_cell, int which = RS_CELLS | RS_PAIRS) {
   const int64_t n = h->n;
   if (!(h->rc > 0.0)) return h->fail(EWB_EINVAL, "cutoff must be positive");
   if (h->rc > 0.5 * h->L)
@@ -1619,6 +1648,7 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
   const int cpd_eff = fold ? 1 : cpd;
   const int n_cells = cpd_eff * cpd_eff * cpd_eff;
   const double edge = h->L / cpd;
+  if (which & RS_CELLS) {
   CK(h->cell_of.ensure(n * sizeof(int)));
   CK(h->slot.ensure(n * sizeof(int)));
   CK(h->count.ensure((n_cells + 1) * sizeof(int)));
@@ -1660,6 +1690,8 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
                                          h->row_ustart.as<int>());
   CKL();
   if (ev_cell) CK(cudaEventRecord(ev_cell, h->stream));
+  }
+  if (!(which & RS_PAIRS)) return EWB_OK;
 
   RSParams rp;
   rp.L = h->L;
@@ -1679,7 +1711,16 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
   rp.c_hi = fold ? 1 : zh * cpd_eff;
   const int64_t rows_slab = rp.c_hi - rp.c_lo;
   const int64_t units_max = n / K6_G + rows_slab + 1;
-  const unsigned nb = (unsigned)std::max<int64_t>(1, (units_max + K6_WARPS - 1) / K6_WARPS);
+  // scan-all mode with few units: split every unit's candidates over
+  // several warps (partial sums meet in the atomics of the half shell)
+  rp.jsplit = 1;
+  if (fold && rp.half) {
+    const int64_t want = 4 * (int64_t)h->n_sm * K6_WARPS;
+    rp.jsplit = (int)std::max<int64_t>(1, std::min<int64_t>(64, want / std::max<int64_t>(1, units_max)));
+    rp.jsplit = (int)std::min<int64_t>(rp.jsplit, std::max<int64_t>(1, n / 64));
+  }
+  const unsigned nb = (unsigned)std::max<int64_t>(
+      1, (units_max * rp.jsplit + K6_WARPS - 1) / K6_WARPS);
   CK(h->eblk.ensure(nb * sizeof(double)));
   if (rows_slab <= 0) {
     CK(cudaMemsetAsync(d_u_out, 0, sizeof(double), h->stream));
@@ -1733,20 +1774,101 @@ int h2d_force(ewb_handle *h, const double *force, int64_t n) {
 }
 
 // full single-GPU pipeline on loaded particles; energies stay on device
-int pipeline(ewb_handle *h, double *d_force, double *d_rho_out, bool timed) {
+// evaluation pipeline in five segments; timing events sit between them
+// (outside any captured graph): ev0 | cells | ev1 | pairs | ev2 | S(k) |
+// ev3 | forces + self | ev4
+constexpr int N_SEG = 5;
+int pipeline_seg(ewb_handle *h, int seg, const double *d_pos, const double *d_q, int64_t n,
+                 double *d_force, double *d_rho_out) {
   int rc;
-  CK(h->energy.ensure(8 * sizeof(double)));
   double *en = h->energy.as<double>();
-  if (timed) CK(cudaEventRecord(h->ev[0], h->stream));
-  if ((rc = stage_real_space(h, 0, 1, d_force, en + 0, timed ? h->ev[1] : nullptr))) return rc;
-  if (timed) CK(cudaEventRecord(h->ev[2], h->stream));
-  int n_part = 0;
-  if ((rc = stage_rho(h, 0, h->n, &n_part))) return rc;
-  if ((rc = stage_finalize(h, h->spart.as<double2>(), n_part, d_rho_out, en + 1))) return rc;
-  if (timed) CK(cudaEventRecord(h->ev[3], h->stream));
-  if ((rc = stage_recip_forces(h, 0, h->n, d_force, false, nullptr))) return rc;
-  if (timed) CK(cudaEventRecord(h->ev[4], h->stream));
-  if ((rc = stage_self(h, en + 2))) return rc;
+  switch (seg) {
+    case 0:
+      return stage_load(h, d_pos, d_q, n);
+    case 1:
+      return stage_real_space(h, 0, 1, d_force, en + 0, nullptr, RS_CELLS);
+    case 2:
+      return stage_real_space(h, 0, 1, d_force, en + 0, nullptr, RS_PAIRS);
+    case 3: {
+      int n_part = 0;
+      if ((rc = stage_rho(h, 0, h->n, &n_part))) return rc;
+      return stage_finalize(h, h->spart.as<double2>(), n_part, d_rho_out, en + 1);
+    }
+    default:
+      if ((rc = stage_recip_forces(h, 0, h->n, d_force, false, nullptr))) return rc;
+      return stage_self(h, en + 2);
+  }
+}
+
+// prep + pipeline; segments are replayed from CUDA graphs when the key
+// (pointers, size, configuration, buffer epoch) is unchanged
+int run_eval(ewb_handle *h, const double *d_pos, const double *d_q, int64_t n, double *d_force,
+             double *d_rho, bool timed) {
+  CK(h->energy.ensure(8 * sizeof(double)));
+  ewb_handle::GKey k;
+  k.pos = d_pos;
+  k.q = d_q;
+  k.force = d_force;
+  k.rho = d_rho;
+  k.n = n;
+  k.timed = false;  // events live outside the graphs
+  k.gen = h->gen;
+  k.epoch = g_realloc_epoch;
+  const bool replay = h->use_graphs && h->gexec[0] && k == h->gkey;
+  const bool capture = !replay && h->use_graphs && k == h->warm_key;
+  const int64_t l0 = h->launches;
+  int rc = EWB_OK;
+  bool captured_all = capture;
+  for (int seg = 0; seg < N_SEG; ++seg) {
+    if (timed && seg >= 1) CK(cudaEventRecord(h->ev[seg - 1], h->stream));
+    if (replay) {
+      CK(cudaGraphLaunch(h->gexec[seg], h->stream));
+      continue;
+    }
+    if (capture && captured_all) {
+      CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+      const int64_t s0 = h->launches;
+      rc = pipeline_seg(h, seg, d_pos, d_q, n, d_force, d_rho);
+      cudaGraph_t g = nullptr;
+      const cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+      if (rc) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+      }
+      if (e == cudaSuccess && k.epoch == g_realloc_epoch) {
+        if (h->gexec[seg]) cudaGraphExecDestroy(h->gexec[seg]);
+        h->gexec[seg] = nullptr;
+        const cudaError_t ei = cudaGraphInstantiate(&h->gexec[seg], g, 0);
+        cudaGraphDestroy(g);
+        CK(ei);
+        h->glaunch[seg] = h->launches - s0;
+        CK(cudaGraphLaunch(h->gexec[seg], h->stream));
+        continue;
+      }
+      // capture failed (or a buffer moved): finish this call eagerly
+      if (g) cudaGraphDestroy(g);
+      cudaGetLastError();
+      captured_all = false;
+      h->launches = s0;
+    }
+    if ((rc = pipeline_seg(h, seg, d_pos, d_q, n, d_force, d_rho))) return rc;
+  }
+  if (timed) CK(cudaEventRecord(h->ev[N_SEG - 1], h->stream));
+  if (replay) {
+    for (int seg = 0; seg < N_SEG; ++seg) h->launches += h->glaunch[seg];
+    h->n = n;
+    h->loaded = true;
+  } else if (capture && captured_all) {
+    h->gkey = k;
+  } else {
+    if (!capture) {
+      k.epoch = g_realloc_epoch;  // the first call may have grown buffers
+      h->warm_key = k;
+    } else {
+      h->warm_key = ewb_handle::GKey();
+    }
+    (void)l0;
+  }
   return EWB_OK;
 }
 
@@ -1826,6 +1948,8 @@ void ewb_destroy(ewb_handle *h) {
                   &h->order_tmp, &h->order, &h->sorted, &h->sorted_cell, &h->row_ustart})
     b->release();
   h->plan.release();
+  for (auto &ge : h->gexec)
+    if (ge) cudaGraphExecDestroy(ge);
   for (auto &ev : h->ev)
     if (ev) cudaEventDestroy(ev);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
@@ -1836,12 +1960,14 @@ const char *ewb_last_error(const ewb_handle *h) { return h ? h->err.c_str() : "n
 
 int ewb_set_stream(ewb_handle *h, uintptr_t stream) {
   if (!h) return EWB_EINVAL;
+  ++h->gen;
   h->stream = stream ? reinterpret_cast<cudaStream_t>(stream) : h->own_stream;
   return EWB_OK;
 }
 
 int ewb_set_max_segment(ewb_handle *h, int mcap) {
   if (!h) return EWB_EINVAL;
+  ++h->gen;
   if (mcap < 1 || mcap > MAXM) return h->fail(EWB_EINVAL, "segment length must be in [1, 32]");
   h->mcap = mcap;
   return EWB_OK;
@@ -1849,13 +1975,22 @@ int ewb_set_max_segment(ewb_handle *h, int mcap) {
 
 int ewb_set_stencil(ewb_handle *h, int rad) {
   if (!h) return EWB_EINVAL;
+  ++h->gen;
   if (rad < 0 || rad > 2) return h->fail(EWB_EINVAL, "stencil radius must be 0 (auto), 1 or 2");
   h->stencil_rad = rad;
   return EWB_OK;
 }
 
+int ewb_set_graphs(ewb_handle *h, int on) {
+  if (!h) return EWB_EINVAL;
+  h->use_graphs = on != 0;
+  ++h->gen;
+  return EWB_OK;
+}
+
 int ewb_set_deterministic(ewb_handle *h, int on) {
   if (!h) return EWB_EINVAL;
+  ++h->gen;
   h->deterministic = on ? 1 : 0;
   return EWB_OK;
 }
@@ -1869,6 +2004,7 @@ int ewb_set_system(ewb_handle *h, double L, double alpha, double r_cutoff, doubl
   h->rc = r_cutoff;
   h->rc2 = rc2;
   h->have_system = true;
+  ++h->gen;
   return EWB_OK;
 }
 
@@ -1877,6 +2013,7 @@ int ewb_set_kspace(ewb_handle *h, const int64_t *m_int, int64_t K, const double 
   if (!m_int && K > 0) return h->fail(EWB_EINVAL, "null m_int");
   CK(cudaSetDevice(h->device));
   int rc = build_plan(h, m_int, K, coeff);
+  ++h->gen;
   if (rc) return rc;
   h->have_kspace = true;
   return EWB_OK;
@@ -1992,10 +2129,18 @@ int ewb_evaluate(ewb_handle *h, const double *pos, const double *q, int64_t n,
   if (!(h->rc > 0.0)) return h->fail(EWB_EINVAL, "cutoff must be positive");
   if (h->rc > 0.5 * h->L)
     return h->fail(EWB_ECUTOFF, "cutoff exceeds L/2 (minimum-image bound)");
-  if ((rc = h2d_particles(h, pos, q, n))) return rc;
-  if ((rc = h2d_force(h, force_inout, n))) return rc;
+  if (!pos || !q) return h->fail(EWB_EINVAL, "null particle arrays");
+  if (n < 1) return h->fail(EWB_EINVAL, "particle count must be >= 1");
+  CK(h->pos.ensure(n * 3 * sizeof(double)));
+  CK(h->q.ensure(n * sizeof(double)));
+  CK(h->force.ensure(n * 3 * sizeof(double)));
   if (rho_out) CK(h->rho.ensure(2 * h->plan.K * sizeof(double)));
-  if ((rc = pipeline(h, h->force.as<double>(), rho_out ? h->rho.as<double>() : nullptr, true)))
+  CK(cudaMemcpyAsync(h->pos.p, pos, n * 3 * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  CK(cudaMemcpyAsync(h->q.p, q, n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  CK(cudaMemcpyAsync(h->force.p, force_inout, n * 3 * sizeof(double), cudaMemcpyHostToDevice,
+                     h->stream));
+  if ((rc = run_eval(h, h->pos.as<double>(), h->q.as<double>(), n, h->force.as<double>(),
+                     rho_out ? h->rho.as<double>() : nullptr, true)))
     return rc;
   double en[3];
   CK(cudaMemcpyAsync(en, h->energy.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
@@ -2103,8 +2248,7 @@ int ewb_dev_evaluate(ewb_handle *h, const double *d_pos, const double *d_q, int6
   if (!(h->rc > 0.0)) return h->fail(EWB_EINVAL, "cutoff must be positive");
   if (h->rc > 0.5 * h->L)
     return h->fail(EWB_ECUTOFF, "cutoff exceeds L/2 (minimum-image bound)");
-  if ((rc = stage_load(h, d_pos, d_q, n))) return rc;
-  if ((rc = pipeline(h, d_force, d_rho_out, timings != nullptr))) return rc;
+  if ((rc = run_eval(h, d_pos, d_q, n, d_force, d_rho_out, timings != nullptr))) return rc;
   double en[3];
   CK(cudaMemcpyAsync(en, h->energy.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
   if ((rc = check_errflag(h, ERR_UNWRAPPED | ERR_COINCIDENT))) return rc;

@@ -351,3 +351,27 @@ def test_deterministic_mode_is_bitwise_reproducible(ew):
     r2 = solver.evaluate(ps)
     assert (r1.u_sr, r1.u_lr, r1.u_self) == (r2.u_sr, r2.u_lr, r2.u_self)
     assert np.array_equal(f1, ps.force)
+
+
+def test_graph_replay_matches_eager(ew):
+    """Evaluations 2.. are captured/replayed as a CUDA graph; results must be
+    bitwise identical to eager execution (deterministic real-space mode)."""
+    from paper_1708_01135_b200 import workloads as wl
+    cfg = wl.make_config("c1", seed=0)
+    results = {}
+    for graphs in (False, True):
+        box, ps = system(ew, cfg["pos"], cfg["q"], cfg["L"])
+        p = ew.EwaldParams(cfg["alpha_ref"], cfg["r_cutoff"], 9.0, 1e-6)
+        rs = ew.ReciprocalSpace(box, p, cfg["m_int"])
+        solver = ew.EwaldSolver(box, p, recip=rs)
+        solver.handle.set_graphs(graphs)
+        solver.handle.set_deterministic(True)
+        out = []
+        for _ in range(4):
+            ps.force[:] = 0.0
+            r = solver.evaluate(ps)
+            out.append((r.u_sr, r.u_lr, r.u_self, ps.force.copy(), rs.rho.values.copy()))
+        results[graphs] = out
+    for a, b in zip(results[False], results[True]):
+        assert a[:3] == b[:3]
+        assert np.array_equal(a[3], b[3]) and np.array_equal(a[4], b[4])

@@ -49,8 +49,10 @@ typedef enum {
     EWB_ECUTOFF = 3,     /* CutoffTooLargeError (r_c > L/2)  */
     EWB_EUNWRAPPED = 4,  /* ValueError: positions not in [0,L) */
     EWB_ECUDA = 5,       /* RuntimeError: CUDA failure        */
+    EWB_EBOX = 6,        /* BoxTooSmallError (r_c > L)        */
     EWB_EKSPACE = 7,     /* KSpaceEmptyError                  */
-    EWB_ESTATE = 8       /* RuntimeError: call order violated */
+    EWB_ESTATE = 8,      /* RuntimeError: call order violated */
+    EWB_ESIZE = 9        /* OracleSizeError (image-shell path, N > 4096) */
 } ewb_status;
 
 /* library / handle lifetime */

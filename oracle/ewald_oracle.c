@@ -295,6 +295,58 @@ int orc_short_range(const double *pos, const double *q, int64_t n, double L, dou
     return err ? ORC_ECOINCIDENT : ORC_OK;
 }
 
+/* short_range_wide_cutoff / _sr_wide_jit (ewald.py:490-576): every j != i
+ * over the 27 nearest images, no fold; for r_c in (L/2, L], N <= 4096. */
+int orc_short_range_wide(const double *pos, const double *q, int64_t n, double L, double rc,
+                         double alpha, int nthreads, double *force_inout, double *u_out) {
+    if (!(rc > 0.0)) return ORC_EINVAL;
+    if (rc > L) return 6;      /* BoxTooSmallError */
+    if (n > 4096) return 7;    /* OracleSizeError */
+    const double rc2 = rc * rc;
+    const double c0 = sqrt(alpha), c1 = alpha, c2 = 2.0 * sqrt(alpha / M_PI);
+    int workers = clamp_workers(nthreads, n);
+    int64_t *bounds = (int64_t *)malloc(sizeof(int64_t) * (workers + 1));
+    double *ups = (double *)calloc((size_t)workers, sizeof(double));
+    int *errs = (int *)calloc((size_t)workers, sizeof(int));
+    block_bounds(n, workers, bounds);
+#pragma omp parallel for num_threads(workers) schedule(static, 1)
+    for (int w = 0; w < workers; ++w) {
+        double uw = 0.0;
+        for (int64_t i = bounds[w]; i < bounds[w + 1]; ++i)
+            for (int64_t j = 0; j < n; ++j) {
+                if (j == i) continue;
+                for (int nx = -1; nx <= 1; ++nx)
+                    for (int ny = -1; ny <= 1; ++ny)
+                        for (int nz = -1; nz <= 1; ++nz) {
+                            const double dx = pos[3 * i] - pos[3 * j] + L * nx;
+                            const double dy = pos[3 * i + 1] - pos[3 * j + 1] + L * ny;
+                            const double dz = pos[3 * i + 2] - pos[3 * j + 2] + L * nz;
+                            volatile double t1 = dx * dx;
+                            volatile double t2 = dy * dy;
+                            volatile double t3 = dz * dz;
+                            const double r2 = (t1 + t2) + t3;
+                            if (r2 >= rc2) continue;
+                            if (r2 == 0.0) { errs[w] = 1; continue; }
+                            const double qq = q[i] * q[j];
+                            const double r = sqrt(r2);
+                            const double sc = erfc(c0 * r) / r;
+                            uw += 0.5 * qq * sc;
+                            const double g = qq * (sc + c2 * exp(-c1 * r2)) / r2;
+                            force_inout[3 * i] += g * dx;
+                            force_inout[3 * i + 1] += g * dy;
+                            force_inout[3 * i + 2] += g * dz;
+                        }
+            }
+        ups[w] = uw;
+    }
+    int err = 0;
+    double u = 0.0;
+    for (int w = 0; w < workers; ++w) { u += ups[w]; err |= errs[w]; }
+    *u_out = u;
+    free(bounds); free(ups); free(errs);
+    return err ? ORC_ECOINCIDENT : ORC_OK;
+}
+
 int orc_num_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

@@ -27,6 +27,7 @@ _SIG = {
     "orc_rho_hat": [_P, _P, _I64, _D, _P, _I64, _INT, _P],
     "orc_long_range": [_P, _P, _I64, _D, _P, _I64, _P, _P, _INT, _P, _P],
     "orc_short_range": [_P, _P, _I64, _D, _D, _D, _INT, _P, _I64, _P, _P],
+    "orc_short_range_wide": [_P, _P, _I64, _D, _D, _D, _INT, _P, _P],
 }
 
 _LIB = None
@@ -112,6 +113,21 @@ def short_range(pos, q, L, r_cutoff, alpha, sel=None, force=None,
     return u.value, f
 
 
+def short_range_wide(pos, q, L, r_cutoff, alpha, force=None, threads=None):
+    """Image-shell real space for r_c > L/2 (ewald.py:490-576)."""
+    pos, q = _c(pos), _c(q)
+    n = q.shape[0]
+    f = np.zeros((n, 3)) if force is None else force
+    u = ctypes.c_double(0.0)
+    rc = lib().orc_short_range_wide(_p(pos), _p(q), n, float(L),
+                                    float(r_cutoff), float(alpha),
+                                    threads or host_threads(), _p(f),
+                                    ctypes.byref(u))
+    if rc:
+        raise OracleError(rc, "short_range_wide")
+    return u.value, f
+
+
 def self_energy(q, alpha):
     """-sqrt(alpha/pi) * q.q (ewald.py:482-484)."""
     q = _c(q)
@@ -124,7 +140,12 @@ def evaluate(pos, q, L, alpha, r_cutoff, m_int, coeff=None, threads=None):
         coeff = kspace_coeff(m_int, L, alpha)
     f = np.zeros((np.asarray(q).shape[0], 3))
     u_self = self_energy(q, alpha)
-    u_sr, _ = short_range(pos, q, L, r_cutoff, alpha, force=f, threads=threads)
+    if r_cutoff > 0.5 * L:   # the reference's wide-cutoff branch (ewald.py:635-637)
+        u_sr, _ = short_range_wide(pos, q, L, r_cutoff, alpha, force=f,
+                                   threads=threads)
+    else:
+        u_sr, _ = short_range(pos, q, L, r_cutoff, alpha, force=f,
+                              threads=threads)
     rho = rho_hat(pos, q, L, m_int, threads=threads)
     u_lr, _ = long_range(pos, q, L, m_int, coeff, rho, force=f,
                          threads=threads)

@@ -11,9 +11,11 @@ import os
 import numpy as np
 
 from .core import (
+    BoxTooSmallError,
     CoincidentParticlesError,
     CutoffTooLargeError,
     KSpaceEmptyError,
+    OracleSizeError,
 )
 
 LIB_NAME = "libewaldb200.so"
@@ -27,8 +29,10 @@ EWB_ECOINCIDENT = 2
 EWB_ECUTOFF = 3
 EWB_EUNWRAPPED = 4
 EWB_ECUDA = 5
+EWB_EBOX = 6
 EWB_EKSPACE = 7
 EWB_ESTATE = 8
+EWB_ESIZE = 9
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
@@ -104,6 +108,10 @@ def raise_for(status, message, lib=None):
         raise CutoffTooLargeError(message)
     if status == EWB_EKSPACE:
         raise KSpaceEmptyError(message)
+    if status == EWB_EBOX:
+        raise BoxTooSmallError(message)
+    if status == EWB_ESIZE:
+        raise OracleSizeError(message)
     if status in (EWB_EINVAL, EWB_EUNWRAPPED):
         raise ValueError(message)
     raise DeviceError(f"libewaldb200 status {status}: {message}")

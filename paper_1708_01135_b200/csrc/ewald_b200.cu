@@ -45,6 +45,7 @@ namespace {
 
 constexpr int ERR_UNWRAPPED = 1;
 constexpr int ERR_COINCIDENT = 2;
+constexpr int64_t WIDE_MAX_N = 4096;  // _WIDE_CUTOFF_MAX_N (ewald.py:490)
 
 constexpr int MAXM = 32;          // longest k-column segment (template range)
 constexpr int K1_THREADS = 128;   // k-items per structure-factor block
@@ -1111,6 +1112,71 @@ __global__ void __launch_bounds__(1024) k_scan_rows(const int *__restrict__ star
   if (threadIdx.x == 0) row_ustart[n_rows] = carry;
 }
 
+// Image-shell real space for r_c > L/2 (short_range_wide_cutoff,
+// ewald.py:492-523): every j != i over the 27 nearest images, no fold,
+// dx = fl(fl(xi - xj) + L n_x), strict r2 < rc2, self images skipped as in
+// the reference.  Block = one centre; threads stride over j; deterministic
+// block reduction.  Validation-scale path (the reference guards N <= 4096).
+__global__ void __launch_bounds__(128)
+    k6w_wide(const double4 *__restrict__ xyzq, int64_t n, double L, double rc2, double sa,
+             double al, double tsap, double *__restrict__ force, double *__restrict__ eblk,
+             int *__restrict__ err) {
+  __shared__ double s_erfcx[ERFCX_NI * ERFCX_NC];
+  __shared__ double sh[4][4];
+  for (int t = threadIdx.x; t < ERFCX_NI * ERFCX_NC; t += 128)
+    s_erfcx[t] = c_erfcx_tab[t / ERFCX_NC][t % ERFCX_NC];
+  __syncthreads();
+  const int64_t i = blockIdx.x;
+  const double4 pi = xyzq[i];
+  double fx = 0.0, fy = 0.0, fz = 0.0, ue = 0.0;
+  bool coincident = false;
+  for (int64_t j = threadIdx.x; j < n; j += 128) {
+    if (j == i) continue;
+    const double4 pj = xyzq[j];
+    const double ddx = __dsub_rn(pi.x, pj.x), ddy = __dsub_rn(pi.y, pj.y),
+                 ddz = __dsub_rn(pi.z, pj.z);
+    for (int img = 0; img < 27; ++img) {
+      const double dx = __dadd_rn(ddx, L * (double)(img / 9 - 1));
+      const double dy = __dadd_rn(ddy, L * (double)((img / 3) % 3 - 1));
+      const double dz = __dadd_rn(ddz, L * (double)(img % 3 - 1));
+      const double r2 = rs_r2(dx, dy, dz);
+      if (!(r2 < rc2)) continue;
+      if (r2 == 0.0) {
+        coincident = true;
+        continue;
+      }
+      const double qq = pi.w * pj.w;
+      const double inv_r = rsqrt_pos(r2);
+      const double r = r2 * inv_r;
+      const double ex = exp_neg(-al * r2);
+      const double sc = erfc_from_exp(sa * r, ex, s_erfcx) * inv_r;
+      ue = fma(0.5 * qq, sc, ue);
+      const double gg = qq * fma(tsap, ex, sc) * (inv_r * inv_r);
+      fx = fma(gg, dx, fx);
+      fy = fma(gg, dy, fy);
+      fz = fma(gg, dz, fz);
+    }
+  }
+  if (coincident) atomicOr(err, ERR_COINCIDENT);
+  const double v[4] = {fx, fy, fz, ue};
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const double t = warp_sum(v[c]);
+    if (l == 0) sh[w][c] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a[4] = {0, 0, 0, 0};
+    for (int ww = 0; ww < 4; ++ww)
+      for (int c = 0; c < 4; ++c) a[c] += sh[ww][c];
+    force[3 * i] += a[0];
+    force[3 * i + 1] += a[1];
+    force[3 * i + 2] += a[2];
+    eblk[i] = a[3];
+  }
+}
+
 // K7: sum q^2 (self energy) partials.
 __global__ void __launch_bounds__(RED_THREADS) k7_sum_q2(const double4 *__restrict__ frac, int64_t n,
                                                          double *__restrict__ eblk) {
@@ -1625,9 +1691,28 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
                      cudaEvent_t ev_cell, int which = RS_CELLS | RS_PAIRS) {
   const int64_t n = h->n;
   if (!(h->rc > 0.0)) return h->fail(EWB_EINVAL, "cutoff must be positive");
-  if (h->rc > 0.5 * h->L)
-    return h->fail(EWB_ECUTOFF, "cutoff " + std::to_string(h->rc) + " exceeds L/2 = " +
-                                    std::to_string(0.5 * h->L) + " (minimum-image bound)");
+  if (h->rc > 0.5 * h->L) {
+    // r_c > L/2: the reference's image-shell path (ewald.py:553-576)
+    if (h->rc > h->L)
+      return h->fail(EWB_EBOX, "r_cutoff exceeds the box edge; a single image shell no longer "
+                               "covers the interaction range");
+    if (n > WIDE_MAX_N)
+      return h->fail(EWB_ESIZE, "wide-cutoff real-space path is O(N^2); N exceeds the 4096 guard");
+    if (!(which & RS_PAIRS)) return EWB_OK;
+    if (part != 0) {  // not sharded: the first part owns every centre
+      CK(cudaMemsetAsync(d_u_out, 0, sizeof(double), h->stream));
+      return EWB_OK;
+    }
+    CK(h->eblk.ensure(n * sizeof(double)));
+    k6w_wide<<<(unsigned)n, 128, 0, h->stream>>>(h->xyzq.as<double4>(), n, h->L, h->rc2,
+                                                 std::sqrt(h->alpha), h->alpha,
+                                                 2.0 * std::sqrt(h->alpha / M_PI), d_force,
+                                                 h->eblk.as<double>(), h->errflag.as<int>());
+    CKL();
+    k_sum<<<1, 1024, 0, h->stream>>>(h->eblk.as<double>(), n, 1.0, d_u_out);
+    CKL();
+    return EWB_OK;
+  }
   // reference binning: cpd = floor(L / r_c), edge = L / cpd (celllist.py:96-98);
   // with cpd < 3 the 27-stencil folds onto every cell and the reference scans
   // all particles with a per-pair fold (engine.py:111-134) -- FOLD mode here.
@@ -2127,8 +2212,6 @@ int ewb_evaluate(ewb_handle *h, const double *pos, const double *q, int64_t n,
   if (rc) return rc;
   CK(cudaSetDevice(h->device));
   if (!(h->rc > 0.0)) return h->fail(EWB_EINVAL, "cutoff must be positive");
-  if (h->rc > 0.5 * h->L)
-    return h->fail(EWB_ECUTOFF, "cutoff exceeds L/2 (minimum-image bound)");
   if (!pos || !q) return h->fail(EWB_EINVAL, "null particle arrays");
   if (n < 1) return h->fail(EWB_EINVAL, "particle count must be >= 1");
   CK(h->pos.ensure(n * 3 * sizeof(double)));
@@ -2144,7 +2227,8 @@ int ewb_evaluate(ewb_handle *h, const double *pos, const double *q, int64_t n,
     return rc;
   double en[3];
   CK(cudaMemcpyAsync(en, h->energy.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-  if ((rc = check_errflag(h, ERR_UNWRAPPED | ERR_COINCIDENT))) return rc;
+  if ((rc = check_errflag(h, (h->rc > 0.5 * h->L ? 0 : ERR_UNWRAPPED) | ERR_COINCIDENT)))
+    return rc;
   CK(cudaMemcpy(force_inout, h->force.p, n * 3 * sizeof(double), cudaMemcpyDeviceToHost));
   if (rho_out)
     CK(cudaMemcpy(rho_out, h->rho.p, 2 * h->plan.K * sizeof(double), cudaMemcpyDeviceToHost));
@@ -2246,12 +2330,11 @@ int ewb_dev_evaluate(ewb_handle *h, const double *d_pos, const double *d_q, int6
   if (rc) return rc;
   CK(cudaSetDevice(h->device));
   if (!(h->rc > 0.0)) return h->fail(EWB_EINVAL, "cutoff must be positive");
-  if (h->rc > 0.5 * h->L)
-    return h->fail(EWB_ECUTOFF, "cutoff exceeds L/2 (minimum-image bound)");
   if ((rc = run_eval(h, d_pos, d_q, n, d_force, d_rho_out, timings != nullptr))) return rc;
   double en[3];
   CK(cudaMemcpyAsync(en, h->energy.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-  if ((rc = check_errflag(h, ERR_UNWRAPPED | ERR_COINCIDENT))) return rc;
+  if ((rc = check_errflag(h, (h->rc > 0.5 * h->L ? 0 : ERR_UNWRAPPED) | ERR_COINCIDENT)))
+    return rc;
   if (energies) std::memcpy(energies, en, sizeof en);
   return read_timings(h, timings);
 }

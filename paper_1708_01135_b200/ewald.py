@@ -289,11 +289,9 @@ class EwaldSolver:
     def evaluate(self, ps, cell_list=None):
         """Accumulate Coulomb forces into ps.force; return EwaldEnergies."""
         require_neutral(ps)
-        if self.wide_cutoff:
-            raise BoxTooSmallError(
-                f"r_cutoff {self.params.r_cutoff:.4g} exceeds L/2 = "
-                f"{self.box.max_cutoff():.4g}: the image-shell real-space "
-                f"path (ewald.py:553-576) is not provided on the device")
+        # r_cutoff > L/2 runs the image-shell real space on the device
+        # (ewald.py:553-576), with the reference's r_c > L and N > 4096
+        # guards (BoxTooSmallError, OracleSizeError)
         pos, q = _particles(ps)
         f, copied = _force_buffer(ps)
         rho = np.empty(2 * self.recip.n_stored)

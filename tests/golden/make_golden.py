@@ -109,6 +109,22 @@ def small_cases():
     pos, q = random_neutral(300, 10.0, 3)
     p = em.EwaldParams(alpha=0.5, r_cutoff=3.3, k_cutoff=3.0, tolerance=1e-4)
     cases.append(("rand300_cube5", pos, q, 10.0, p, wl.cube_half_m(5)))
+    # r_cutoff > L/2: the reference's image-shell real space (ewald.py:553-576)
+    pos, q = random_neutral(64, 12.0, 41)
+    s_ = math.sqrt(-math.log(1e-6))
+    p = em.EwaldParams(alpha=0.1, r_cutoff=s_ / math.sqrt(0.1),
+                       k_cutoff=2.0 * s_ * math.sqrt(0.1), tolerance=1e-6)
+    cases.append(("wide_rand64", pos, q, 12.0, p, None))
+    ps8 = em.init_rocksalt(3, 2.5)
+    rng = np.random.default_rng(3)
+    pos8 = ps8.position + 0.1 * rng.standard_normal(ps8.position.shape)
+    L8 = ps8.box.edge_length
+    pos8 = pos8 - L8 * np.floor(pos8 / L8)
+    base = em.choose_parameters(ps8.count, ps8.box, 1e-6)
+    a = base.alpha * 0.5
+    p = em.EwaldParams(alpha=a, r_cutoff=s_ / math.sqrt(a),
+                       k_cutoff=2.0 * s_ * math.sqrt(a), tolerance=1e-6)
+    cases.append(("wide_nacl216", pos8, ps8.charge.copy(), L8, p, None))
     for name, pos, q, L, p, m in cases:
         out = ref_evaluate(pos, q, L, p, m)
         save(name, pos=pos, q=q, L=L, alpha=p.alpha, r_cutoff=p.r_cutoff,

@@ -49,7 +49,7 @@ def check_energies(res, u_sr, u_lr, u_self, scale=None):
 
 
 SMALL = ["rocksalt8", "rand32_s21", "rand64_s5", "rand200_s7", "rand600_s11",
-         "rand300_cube5"]
+         "rand300_cube5", "wide_rand64", "wide_nacl216"]
 
 
 @pytest.mark.parametrize("name", SMALL)
@@ -204,10 +204,15 @@ def test_errors(ew):
     ps.position[1] = (-0.5, 1.0, 1.0)
     with pytest.raises(ValueError):
         ew.total_coulomb(ps, p)
-    wide = ew.EwaldParams(0.01, 6.0, 2.0, 1e-3)
-    with pytest.raises(ew.BoxTooSmallError):
-        ps.position[1] = (5.0, 1.0, 1.0)
-        ew.EwaldSolver(box, wide).evaluate(ps)
+    ps.position[1] = (5.0, 1.0, 1.0)
+    with pytest.raises(ew.BoxTooSmallError):   # r_c > L (ewald.py:561-565)
+        ew.EwaldSolver(box, ew.EwaldParams(0.01, 11.0, 2.0, 1e-3)).evaluate(ps)
+    big = ew.create_particle_set(4098, box)     # image-shell guard (ewald.py:566-570)
+    big.position[:] = np.random.default_rng(0).random((4098, 3)) * 10.0
+    big.charge[:2049] = 1.0
+    big.charge[2049:] = -1.0
+    with pytest.raises(ew.OracleSizeError):
+        ew.EwaldSolver(box, ew.EwaldParams(0.01, 6.0, 2.0, 1e-3)).evaluate(big)
     with pytest.raises(ew.KSpaceEmptyError):
         ew.enumerate_kvectors(box, ew.EwaldParams(1.0, 5.0, 0.5, 1e-6))
 

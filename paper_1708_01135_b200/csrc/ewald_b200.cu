@@ -66,7 +66,9 @@ constexpr size_t K1_PART_BYTES = (size_t)512 << 20;  // cap of the partial S(k) 
 constexpr int K3_THREADS = 128;
 constexpr int K3_PPT = 2;         // particles per thread in the gather
 constexpr int K3_CH = 32;         // k-items per shared-memory chunk
-constexpr int K6_WARPS = 4;
+#ifndef K6_WARPS
+#define K6_WARPS 4
+#endif
 #ifndef K6_G
 #define K6_G 8                    // centre particles per real-space warp
 #endif

@@ -62,8 +62,11 @@ void ewb_destroy(ewb_handle *h);
 const char *ewb_last_error(const ewb_handle *h);
 /* stream used by every later call (0 = the handle's own stream) */
 int ewb_set_stream(ewb_handle *h, uintptr_t stream);
-/* tuning knob: maximum k-column segment length (1..32; default 28) */
+/* tuning knobs (take effect at the next ewb_set_kspace): maximum k-column
+ * segment length of the force gather (1..32; default 28) and of the
+ * structure factor's +-m_x pair items (1..20; default 20) */
 int ewb_set_max_segment(ewb_handle *h, int mcap);
+int ewb_set_max_pair_segment(ewb_handle *h, int mcap1);
 
 /* real-space cell grid: 0 = auto (r_c/2 cells, 5^3 stencil, when >= 5 cells
  * per edge), 1 = r_c cells with the 3^3 stencil (the reference's grid). */
@@ -88,8 +91,8 @@ int ewb_set_system(ewb_handle *h, double L, double alpha, double r_cutoff,
 /* ReciprocalSpace: m_int (K,3) int64 in caller order, coeff (K,) C_k. */
 int ewb_set_kspace(ewb_handle *h, const int64_t *m_int, int64_t K,
                    const double *coeff);
-/* plan summary: [K, n_items, M, n_rows, n_tiles, max_table] */
-int ewb_kspace_info(const ewb_handle *h, int64_t *info6);
+/* plan summary: [K, n_items, M, n_rows, n_tiles, max_table, n_pair_items, M1] */
+int ewb_kspace_info(const ewb_handle *h, int64_t *info8);
 
 /* ---- host-pointer entry points (reference-facing) ---- */
 int ewb_compute_rho_hat(ewb_handle *h, const double *pos, const double *q,
@@ -111,7 +114,7 @@ int ewb_evaluate(ewb_handle *h, const double *pos, const double *q,
 /* Load particles (device pos (N,3), q (N,)); validates wrapping. */
 int ewb_dev_load(ewb_handle *h, const double *d_pos, const double *d_q,
                  int64_t n);
-/* Number of doubles of the slot-layout S(k) buffer (2 * M * n_items). */
+/* Number of doubles of the pair-slot S(k) partial buffer (4 * M1 * n_pair_items). */
 int64_t ewb_dev_slot_doubles(const ewb_handle *h);
 /* S(k) partial over particles [i0, i1) into d_slots (slot layout). */
 int ewb_dev_rho_partial(ewb_handle *h, int64_t i0, int64_t i1,

@@ -47,6 +47,7 @@ SIGNATURES = {
     "ewb_last_error": (ctypes.c_char_p, [_P]),
     "ewb_set_stream": (_INT, [_P, ctypes.c_size_t]),
     "ewb_set_max_segment": (_INT, [_P, _INT]),
+    "ewb_set_max_pair_segment": (_INT, [_P, _INT]),
     "ewb_set_stencil": (_INT, [_P, _INT]),
     "ewb_set_deterministic": (_INT, [_P, _INT]),
     "ewb_set_graphs": (_INT, [_P, _INT]),
@@ -183,6 +184,10 @@ class Handle:
         self._check(self.lib.ewb_set_max_segment(self.h, int(mcap)))
         self.kspace_key = None
 
+    def set_max_pair_segment(self, mcap1):
+        self._check(self.lib.ewb_set_max_pair_segment(self.h, int(mcap1)))
+        self.kspace_key = None
+
     def set_graphs(self, on):
         self._check(self.lib.ewb_set_graphs(self.h, 1 if on else 0))
 
@@ -193,10 +198,10 @@ class Handle:
         self._check(self.lib.ewb_set_stencil(self.h, int(rad)))
 
     def kspace_info(self):
-        info = np.zeros(6, dtype=np.int64)
+        info = np.zeros(8, dtype=np.int64)
         self._check(self.lib.ewb_kspace_info(self.h, _ptr(info)))
         return dict(zip(("K", "n_items", "M", "n_rows", "n_tiles",
-                         "max_table"), info.tolist()))
+                         "max_table", "n_pair_items", "M1"), info.tolist()))
 
     def set_stream(self, stream_ptr):
         self._check(self.lib.ewb_set_stream(self.h, int(stream_ptr)))

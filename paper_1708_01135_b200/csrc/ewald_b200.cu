@@ -28,6 +28,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
+#include <tuple>
 #include <type_traits>
 #include <cmath>
 #include <cstdint>
@@ -48,6 +50,7 @@ constexpr int ERR_COINCIDENT = 2;
 constexpr int64_t WIDE_MAX_N = 4096;  // _WIDE_CUTOFF_MAX_N (ewald.py:490)
 
 constexpr int MAXM = 32;          // longest k-column segment (template range)
+constexpr int MAXM1 = 20;         // longest K1 pair segment (two accumulator sets)
 constexpr int K1_THREADS = 128;   // k-items per structure-factor block
 constexpr int K1_PMAX = 32;       // particles per shared-memory phase chunk
 #ifndef K1_ILP
@@ -78,9 +81,16 @@ constexpr int RED_THREADS = 256;
 // tab_desc flags
 constexpr int TF_QSCALE = 1;
 constexpr int TF_LINK = 2;
+constexpr int TF_SCALE2 = 16;  // x2 (the 2 cos / 2 sin of a pair item)
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+
+__device__ __forceinline__ double4 ldcs4(const double4 *p) {
+  const double2 *q = reinterpret_cast<const double2 *>(p);
+  const double2 a = __ldcs(q), b = __ldcs(q + 1);
+  return make_double4(a.x, a.y, b.x, b.y);
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -124,58 +134,52 @@ __global__ void k_prep(const double *__restrict__ pos, const double *__restrict_
   base[3 * i + 2] = make_double2(c, -s);
 }
 
-// K1 inner loop for G particles at once (G independent recurrence chains):
-// acc[m] += sum_g q_g e^{-i k_m . r_g} along one k-column segment.
+// K1 inner loop for G particles at once (G independent recurrence chains).
+// One pair item = the z-segments of (+|m_x|, m_y) and (-|m_x|, m_y): with
+// YZ_m = q e^{-i(m_y th_y + m_z th_z)} (three-term recurrence along m_z),
+// A+[m] += 2cos(m_x th_x) YZ_m and A-[m] += 2sin(m_x th_x) YZ_m, so that
+// S(+-m_x) = (A+ -+ i A-)/2: 6 FP64 instructions per two k-vectors.
 template <int M, int G>
-__device__ __forceinline__ void k1_accumulate(double2 (&acc)[M], const double2 *t, int TSp,
-                                              int2 it, int eidx) {
+__device__ __forceinline__ void k1_accumulate(double2 (&ap)[M], double2 (&am)[M],
+                                              const double2 *t, int TSp, int4 it, int eidx) {
   double2 bp[G], bc[G];
-  double c2[G];
+  double c2[G], cx[G], sx[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     const double2 *tg = t + g * TSp;
     const double2 e = tg[eidx];
-    bp[g] = cmul(tg[it.x], tg[it.y]);  // m = 0: row x column entry
+    const double2 x = tg[it.z];  // 2 e^{-i |m_x| th_x}
+    cx[g] = x.x;
+    sx[g] = -x.y;
+    bp[g] = cmul(tg[it.x], tg[it.y]);  // m = 0: q e^{-i s th_z} e^{-i m_y th_y}
     bc[g] = cmul(bp[g], e);            // m = 1
     c2[g] = e.x + e.x;                 // 2 cos(theta_z)
   }
-  {
-    double sx = bp[0].x, sy = bp[0].y;
 #pragma unroll
-    for (int g = 1; g < G; ++g) {
-      sx += bp[g].x;
-      sy += bp[g].y;
+  for (int g = 0; g < G; ++g) {
+    ap[0].x = fma(cx[g], bp[g].x, ap[0].x);
+    ap[0].y = fma(cx[g], bp[g].y, ap[0].y);
+    am[0].x = fma(sx[g], bp[g].x, am[0].x);
+    am[0].y = fma(sx[g], bp[g].y, am[0].y);
+    if (M > 1) {
+      ap[1].x = fma(cx[g], bc[g].x, ap[1].x);
+      ap[1].y = fma(cx[g], bc[g].y, ap[1].y);
+      am[1].x = fma(sx[g], bc[g].x, am[1].x);
+      am[1].y = fma(sx[g], bc[g].y, am[1].y);
     }
-    acc[0].x += sx;
-    acc[0].y += sy;
-  }
-  if (M > 1) {
-    double sx = bc[0].x, sy = bc[0].y;
-#pragma unroll
-    for (int g = 1; g < G; ++g) {
-      sx += bc[g].x;
-      sy += bc[g].y;
-    }
-    acc[1].x += sx;
-    acc[1].y += sy;
   }
 #pragma unroll
   for (int m = 2; m < M; ++m) {
-    double2 bn[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      bn[g] = make_double2(fma(c2[g], bc[g].x, -bp[g].x), fma(c2[g], bc[g].y, -bp[g].y));
+      const double2 bn = make_double2(fma(c2[g], bc[g].x, -bp[g].x), fma(c2[g], bc[g].y, -bp[g].y));
       bp[g] = bc[g];
-      bc[g] = bn[g];
+      bc[g] = bn;
+      ap[m].x = fma(cx[g], bn.x, ap[m].x);
+      ap[m].y = fma(cx[g], bn.y, ap[m].y);
+      am[m].x = fma(sx[g], bn.x, am[m].x);
+      am[m].y = fma(sx[g], bn.y, am[m].y);
     }
-    double sx = bn[0].x, sy = bn[0].y;
-#pragma unroll
-    for (int g = 1; g < G; ++g) {
-      sx += bn[g].x;
-      sy += bn[g].y;
-    }
-    acc[m].x += sx;
-    acc[m].y += sy;
   }
 }
 
@@ -185,21 +189,21 @@ template <int M>
 __global__ void __launch_bounds__(K1_THREADS)
     k1_structure_factor(const double4 *__restrict__ frac, const double2 *__restrict__ base,
                         int64_t p_begin, int64_t p_end, int64_t ppb, int pchunk,
-                        const int2 *__restrict__ item_tab, int n_items,
+                        const int4 *__restrict__ item_tab, int n_items,
                         const int4 *__restrict__ tab_desc, const int *__restrict__ tile_off,
-                        const int *__restrict__ tile_ts, double2 *__restrict__ spart) {
+                        const int *__restrict__ tile_ts, double4 *__restrict__ spart) {
   extern __shared__ double2 tab[];
   const int tile = blockIdx.x;
   const int item = tile * K1_THREADS + threadIdx.x;
   const bool valid = item < n_items;
-  const int2 it = item_tab[valid ? item : n_items - 1];
+  const int4 it = item_tab[valid ? item : n_items - 1];
   const int TS = tile_ts[tile];
   const int4 *desc = tab_desc + tile_off[tile];
   const int eidx = TS - 1;
 
-  double2 acc[M];
+  double2 ap[M], am[M];
 #pragma unroll
-  for (int m = 0; m < M; ++m) acc[m] = make_double2(0.0, 0.0);
+  for (int m = 0; m < M; ++m) ap[m] = am[m] = make_double2(0.0, 0.0);
 
   const int64_t c_begin = p_begin + (int64_t)blockIdx.y * ppb;
   const int64_t c_end = min(p_end, c_begin + ppb);
@@ -244,10 +248,9 @@ __global__ void __launch_bounds__(K1_THREADS)
         double sn, cs;
         sincospi(2.0 * arg, &sn, &cs);
         v = make_double2(cs, -sn);
-        if (d.w & TF_QSCALE) {
-          v.x *= f.w;
-          v.y *= f.w;
-        }
+        const double sc = (d.w & TF_QSCALE) ? f.w : ((d.w & TF_SCALE2) ? 2.0 : 1.0);
+        v.x *= sc;
+        v.y *= sc;
       } else {
         v = cmul(prev, ((d.w >> 2) & 3) ? by : bx);
       }
@@ -268,14 +271,16 @@ __global__ void __launch_bounds__(K1_THREADS)
     const double2 *tab_k = tabs[k & 1];
     const int np = (int)min((int64_t)pchunk, c_end - (c_begin + (int64_t)k * pchunk));
     int p = 0;
-    for (; p + K1_ILP <= np; p += K1_ILP) k1_accumulate<M, K1_ILP>(acc, tab_k + p * TSp, TSp, it, eidx);
-    for (; p < np; ++p) k1_accumulate<M, 1>(acc, tab_k + p * TSp, TSp, it, eidx);
+    for (; p + K1_ILP <= np; p += K1_ILP)
+      k1_accumulate<M, K1_ILP>(ap, am, tab_k + p * TSp, TSp, it, eidx);
+    for (; p < np; ++p) k1_accumulate<M, 1>(ap, am, tab_k + p * TSp, TSp, it, eidx);
     __syncthreads();
   }
   if (valid) {
-    double2 *out = spart + (size_t)blockIdx.y * M * n_items + item;
+    double4 *out = spart + (size_t)blockIdx.y * M * n_items + item;
 #pragma unroll
-    for (int m = 0; m < M; ++m) out[(size_t)m * n_items] = acc[m];
+    for (int m = 0; m < M; ++m)
+      out[(size_t)m * n_items] = make_double4(ap[m].x, ap[m].y, am[m].x, am[m].y);
   }
 }
 
@@ -320,6 +325,71 @@ __global__ void __launch_bounds__(RED_THREADS)
         e = C * (S.x * S.x + S.y * S.y);
       } else {
         sp[s] = make_double2(0.0, 0.0);
+      }
+    }
+  }
+  if (finalize) {
+    const double b = block_sum<RED_THREADS>(e, sh);
+    if (threadIdx.x == 0) epart[blockIdx.x] = b;
+  }
+}
+
+// K2 for the K1 pair layout: sum particle-chunk partials (A+, A-) of a pair
+// slot, S(+-m_x) = (A+ -+ i A-)/2, scatter rho to the caller's k order, C*S to
+// the gather's slot layout, and u_lr partials.  finalize=0: only the summed
+// pair slots (multi-GPU partial S before the all-reduce).
+__global__ void __launch_bounds__(RED_THREADS)
+    k2p_finalize(const double4 *__restrict__ spart, int n_part, int64_t n_pslots,
+                 const int4 *__restrict__ pmap, const double *__restrict__ slot_coeff, int64_t K,
+                 double *__restrict__ rho_out, double4 *__restrict__ s_out,
+                 double2 *__restrict__ sp, double *__restrict__ epart, int finalize) {
+  __shared__ double sh[RED_THREADS / 32];
+  const int64_t s = blockIdx.x * (int64_t)RED_THREADS + threadIdx.x;
+  double e = 0.0;
+  if (s < n_pslots) {
+    double4 A = make_double4(0.0, 0.0, 0.0, 0.0);
+    int pc = 0;
+    for (; pc + 8 <= n_part; pc += 8) {
+      double4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = ldcs4(spart + (size_t)(pc + u) * n_pslots + s);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        A.x += v[u].x;
+        A.y += v[u].y;
+        A.z += v[u].z;
+        A.w += v[u].w;
+      }
+    }
+    for (; pc < n_part; ++pc) {
+      const double4 v = ldcs4(spart + (size_t)pc * n_pslots + s);
+      A.x += v.x;
+      A.y += v.y;
+      A.z += v.z;
+      A.w += v.w;
+    }
+    if (s_out) s_out[s] = A;
+    if (finalize) {
+      const int4 mp = pmap[s];
+      const double2 Sp_ = make_double2(0.5 * (A.x + A.w), 0.5 * (A.y - A.z));  // +m_x
+      const double2 Sm_ = make_double2(0.5 * (A.x - A.w), 0.5 * (A.y + A.z));  // -m_x
+      if (mp.x >= 0) {
+        if (rho_out) {
+          rho_out[mp.x] = Sp_.x;
+          rho_out[K + mp.x] = Sp_.y;
+        }
+        const double C = slot_coeff[mp.z];
+        sp[mp.z] = make_double2(C * Sp_.x, C * Sp_.y);
+        e += C * (Sp_.x * Sp_.x + Sp_.y * Sp_.y);
+      }
+      if (mp.y >= 0) {
+        if (rho_out) {
+          rho_out[mp.y] = Sm_.x;
+          rho_out[K + mp.y] = Sm_.y;
+        }
+        const double C = slot_coeff[mp.w];
+        sp[mp.w] = make_double2(C * Sm_.x, C * Sm_.y);
+        e += C * (Sm_.x * Sm_.x + Sm_.y * Sm_.y);
       }
     }
   }
@@ -802,6 +872,9 @@ __device__ __forceinline__ double rs_r2(double dx, double dy, double dz) {
 // k = 0: -L, 1: 0, 2: +L, 3: fold per pair
 constexpr int K6_LIST = 32 * K6_G + 32;  // pending pairs per warp
 
+#ifndef K6_SCAN
+#define K6_SCAN 0  // 1: per-step warp scan compaction, 0: per-centre ballots
+#endif
 #ifndef K6_MINB
 #define K6_MINB 4
 #endif
@@ -950,8 +1023,13 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
         const int j = j0 + lane;
         const bool vj = j < je;
         const double4 pj = sorted[vj ? j : jb];
+#if K6_SCAN
+        // test every centre; bit g of amask: centre g accepts candidate j
+        uint32_t amask = 0u;
+        uint32_t fcode[K6_G];  // per-centre fold outcome (fold modes only)
 #pragma unroll
         for (int g = 0; g < K6_G; ++g) {
+          fcode[g] = 0u;
           if (g < gi) {
             const double4 pi = s_i[warp][g];
             uint32_t kx = 1u, ky = 1u, kz = 1u;
@@ -960,6 +1038,48 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
             double dz = __dsub_rn(pi.z, pj.z);
             // (NOSH: no image shift on any axis; fl(d + 0.0) == d up to the
             // sign of zero, so r2 matches the evaluation's recomputation)
+            if (FX) dx = fold(dx, kx); else if (!NOSH) dx = __dadd_rn(dx, sx);
+            if (FYZ) {
+              dy = fold(dy, ky);
+              dz = fold(dz, kz);
+            } else if (!NOSH) {
+              dy = __dadd_rn(dy, sy);
+              dz = __dadd_rn(dz, sz);
+            }
+            const double r2 = rs_r2(dx, dy, dz);
+            const bool acc = vj && (r2 < P.rc2) && (after ? j > first + g : j != first + g);
+            amask |= acc ? (1u << g) : 0u;
+            if (FX || FYZ) fcode[g] = (kx << 4) | (ky << 6) | (kz << 8);
+          }
+        }
+        // one warp scan places every lane's accepted pairs (lane-major)
+        const int c = __popc(amask);
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        int off = cnt + incl - c;
+        cnt += __shfl_sync(0xffffffffu, incl, 31);
+#pragma unroll
+        for (int g = 0; g < K6_G; ++g) {
+          if (amask & (1u << g)) {
+            uint32_t t = tag | (uint32_t)g;
+            if (FX) t = (t & ~(3u << 4)) | (fcode[g] & (3u << 4));
+            if (FYZ) t = (t & ~(15u << 6)) | (fcode[g] & (15u << 6));
+            s_list[warp][off++] = make_uint2((uint32_t)j, t);
+          }
+        }
+#else
+#pragma unroll
+        for (int g = 0; g < K6_G; ++g) {
+          if (g < gi) {
+            const double4 pi = s_i[warp][g];
+            uint32_t kx = 1u, ky = 1u, kz = 1u;
+            double dx = __dsub_rn(pi.x, pj.x);
+            double dy = __dsub_rn(pi.y, pj.y);
+            double dz = __dsub_rn(pi.z, pj.z);
             if (FX) dx = fold(dx, kx); else if (!NOSH) dx = __dadd_rn(dx, sx);
             if (FYZ) {
               dy = fold(dy, ky);
@@ -980,6 +1100,7 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
             cnt += __popc(bal);
           }
         }
+#endif
         if (cnt >= 32) drain();
       }
     };
@@ -1217,17 +1338,20 @@ __global__ void __launch_bounds__(256) k_fp64_probe(double *__restrict__ out, in
       X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30) X(31) X(32)
 
 typedef void (*k1_fn)(const double4 *, const double2 *, int64_t, int64_t, int64_t, int,
-                      const int2 *, int, const int4 *, const int *, const int *, double2 *);
+                      const int4 *, int, const int4 *, const int *, const int *, double4 *);
 typedef void (*k3_fn)(const double4 *, const double2 *, int64_t, int64_t, const int4 *,
                       const int *, const int *, const int *, const double2 *, int, double *,
                       double *);
 
+#define EWB_M1_CASES(X)                                                                          \
+  X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) X(17) \
+      X(18) X(19) X(20)
 k1_fn k1_table(int M) {
   switch (M) {
 #define X(m) \
   case m:    \
     return k1_structure_factor<m>;
-    EWB_M_CASES(X)
+    EWB_M1_CASES(X)
 #undef X
   }
   return nullptr;
@@ -1281,13 +1405,18 @@ struct DBuf {
 
 struct Plan {
   int64_t K = 0;
-  int M = 0, n_items = 0, n_rows = 0, n_tiles = 0, ts_max = 0, pchunk = K1_PMAX;
+  // K3 (force gather) layout: items = z-segments of <= M k-vectors
+  int M = 0, n_items = 0, n_rows = 0;
   std::vector<int> row_item_prefix;  // n_rows+1
-  DBuf item_tab, item_my, item_row, rows, tab_desc, tile_off, tile_ts, slot_k, slot_coeff;
+  DBuf item_my, item_row, rows, slot_k, slot_coeff;
+  // K1 (structure factor) layout: pair items = the +m_x and -m_x segments of
+  // one (|m_x|, m_y, m_z-run) sharing one z recurrence
+  int M1 = 0, n_pitems = 0, n_tiles = 0, ts_max = 0, pchunk = K1_PMAX;
+  DBuf pitem_tab, tab_desc, tile_off, tile_ts, pslot_map;  // pslot_map: int4 (kp, km, k3p, k3m)
   std::vector<std::pair<int, DBuf>> ks_cache;  // n_ks -> row boundaries
   void release() {
-    for (DBuf *b : {&item_tab, &item_my, &item_row, &rows, &tab_desc, &tile_off, &tile_ts,
-                    &slot_k, &slot_coeff})
+    for (DBuf *b : {&item_my, &item_row, &rows, &slot_k, &slot_coeff, &pitem_tab, &tab_desc,
+                    &tile_off, &tile_ts, &pslot_map})
       b->release();
     for (auto &c : ks_cache) c.second.release();
     ks_cache.clear();
@@ -1303,7 +1432,8 @@ struct ewb_handle {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[6] = {};
   std::string err;
-  int mcap = 28;
+  int mcap = 28;   // K3 segment cap
+  int mcap1 = 20;  // K1 pair segment cap
   int stencil_rad = 0;  // 0 auto, 1 force r_c cells (testing)
   int deterministic = 0;  // 1: full-shell real space, no atomics (bitwise reproducible)
   int64_t launches = 0;
@@ -1461,49 +1591,149 @@ int build_plan(ewb_handle *h, const int64_t *m, int64_t K, const double *coeff) 
       slot_coeff[(size_t)mm * n_items + i] = coeff ? coeff[k] : 0.0;
     }
 
-  // K1 tiles and their phase-table descriptors
-  const int n_tiles = (n_items + K1_THREADS - 1) / K1_THREADS;
-  std::vector<int2> item_tab(n_items);
+  // ---- K1 pair plan (own segmentation, cap mcap1) ----
+  struct Seg {
+    int mx, my, s, len;
+    int64_t off;
+  };
+  std::vector<Seg> segs;
+  const int mcap1 = std::max(1, std::min(MAXM1, h->mcap1));
+  {
+    int64_t a1 = 0;
+    while (a1 < K) {
+      const int64_t i0 = idx[a1];
+      int64_t b1 = a1 + 1;
+      while (b1 < K) {
+        const int64_t ib = idx[b1], ip = idx[b1 - 1];
+        if (m[3 * ib] != m[3 * i0] || m[3 * ib + 1] != m[3 * i0 + 1] ||
+            m[3 * ib + 2] != m[3 * ip + 2] + 1)
+          break;
+        ++b1;
+      }
+      const int64_t len = b1 - a1;
+      // <= mcap1 per segment; long columns (>= 3 segments) use ~14: the
+      // two accumulator sets of longer segments cost occupancy
+      int64_t nseg = (len + mcap1 - 1) / mcap1;
+      if (nseg >= 3 && mcap1 > 14) nseg = (len + 13) / 14;
+      const int64_t base_len = len / nseg, rem = len % nseg;
+      int64_t off = a1;
+      for (int64_t sg = 0; sg < nseg; ++sg) {
+        const int sl = (int)(base_len + (sg < rem ? 1 : 0));
+        segs.push_back(Seg{(int)m[3 * i0], (int)m[3 * i0 + 1], (int)m[3 * idx[off] + 2], sl, off});
+        off += sl;
+      }
+      a1 = b1;
+    }
+  }
+  struct PItem {
+    int ax, my, s, len;
+    int64_t offp, offm;
+  };
+  std::vector<PItem> pitems;
+  {
+    std::map<std::tuple<int, int, int, int>, int> by_key;
+    for (int i = 0; i < (int)segs.size(); ++i)
+      by_key[std::make_tuple(segs[i].mx, segs[i].my, segs[i].s, segs[i].len)] = i;
+    std::vector<char> used(segs.size(), 0);
+    for (int i = 0; i < (int)segs.size(); ++i) {
+      const Seg &g = segs[i];
+      if (used[i] || g.mx <= 0) continue;
+      auto it = by_key.find(std::make_tuple(-g.mx, g.my, g.s, g.len));
+      if (it != by_key.end() && !used[it->second]) {
+        used[i] = used[it->second] = 1;
+        pitems.push_back(PItem{g.mx, g.my, g.s, g.len, g.off, segs[it->second].off});
+      }
+    }
+    for (int i = 0; i < (int)segs.size(); ++i) {
+      if (used[i]) continue;
+      const Seg &g = segs[i];
+      if (g.mx >= 0)
+        pitems.push_back(PItem{g.mx, g.my, g.s, g.len, g.off, -1});
+      else
+        pitems.push_back(PItem{-g.mx, g.my, g.s, g.len, -1, g.off});
+    }
+  }
+  std::sort(pitems.begin(), pitems.end(), [](const PItem &x, const PItem &y) {
+    if (x.s != y.s) return x.s < y.s;
+    if (x.ax != y.ax) return x.ax < y.ax;
+    return x.my < y.my;
+  });
+  const int n_pitems = (int)pitems.size();
+  int M1 = 0;
+  for (auto &it : pitems) M1 = std::max(M1, it.len);
+  // caller index -> K3 slot
+  std::vector<int> k3slot(K, -1);
+  for (size_t sl = 0; sl < n_slots; ++sl)
+    if (slot_k[sl] >= 0) k3slot[slot_k[sl]] = (int)sl;
+  std::vector<int4> pslot((size_t)M1 * n_pitems, make_int4(-1, -1, -1, -1));
+  for (int i = 0; i < n_pitems; ++i)
+    for (int mm = 0; mm < pitems[i].len; ++mm) {
+      int4 &e = pslot[(size_t)mm * n_pitems + i];
+      if (pitems[i].offp >= 0) {
+        e.x = (int)idx[pitems[i].offp + mm];
+        e.z = k3slot[e.x];
+      }
+      if (pitems[i].offm >= 0) {
+        e.y = (int)idx[pitems[i].offm + mm];
+        e.w = k3slot[e.y];
+      }
+    }
+
+  // K1 tiles and their phase-table descriptors: q e^{-i s th_z} for the
+  // distinct segment starts, e^{-i m_y th_y} over the m_y range,
+  // 2 e^{-i |m_x| th_x} for the distinct |m_x| (linked along x), e^{-i th_z}
+  const int n_tiles = (n_pitems + K1_THREADS - 1) / K1_THREADS;
+  std::vector<int4> ptab(n_pitems);
   std::vector<int4> desc;
   std::vector<int> tile_off(n_tiles), tile_ts(n_tiles);
   int ts_max = 0;
   for (int t = 0; t < n_tiles; ++t) {
-    const int i0 = t * K1_THREADS, i1 = std::min(n_items, i0 + K1_THREADS);
-    const int r_lo = item_row[i0], r_hi = item_row[i1 - 1];
-    int my_lo = items[i0].my, my_hi = items[i0].my;
+    const int i0 = t * K1_THREADS, i1 = std::min(n_pitems, i0 + K1_THREADS);
+    std::vector<int> svals, axs;
+    int my_lo = pitems[i0].my, my_hi = pitems[i0].my;
     for (int i = i0; i < i1; ++i) {
-      my_lo = std::min(my_lo, items[i].my);
-      my_hi = std::max(my_hi, items[i].my);
+      svals.push_back(pitems[i].s);
+      axs.push_back(pitems[i].ax);
+      my_lo = std::min(my_lo, pitems[i].my);
+      my_hi = std::max(my_hi, pitems[i].my);
     }
-    const int n_r = r_hi - r_lo + 1, n_y = my_hi - my_lo + 1;
-    const int TS = n_r + n_y + 1;
+    std::sort(svals.begin(), svals.end());
+    svals.erase(std::unique(svals.begin(), svals.end()), svals.end());
+    std::sort(axs.begin(), axs.end());
+    axs.erase(std::unique(axs.begin(), axs.end()), axs.end());
+    const int n_z = (int)svals.size(), n_y = my_hi - my_lo + 1, n_x = (int)axs.size();
+    const int TS = n_z + n_y + n_x + 1;
     if (TS > 8192) return h->fail(EWB_EINVAL, "k-table too sparse for the tile planner");
     tile_off[t] = (int)desc.size();
     tile_ts[t] = TS;
     ts_max = std::max(ts_max, TS);
-    for (int r = r_lo; r <= r_hi; ++r) {
-      int fl = TF_QSCALE;
-      if (r > r_lo && rows[r].y == rows[r - 1].y && rows[r].x == rows[r - 1].x + 1)
-        fl |= TF_LINK | (0 << 2);
-      desc.push_back(make_int4(rows[r].x, 0, rows[r].y, fl));
-    }
+    for (int v : svals) desc.push_back(make_int4(0, 0, v, TF_QSCALE));
     for (int y = my_lo; y <= my_hi; ++y)
       desc.push_back(make_int4(0, y, 0, y > my_lo ? (TF_LINK | (1 << 2)) : 0));
+    for (int xi = 0; xi < n_x; ++xi)
+      desc.push_back(make_int4(axs[xi], 0, 0,
+                               TF_SCALE2 | ((xi > 0 && axs[xi] == axs[xi - 1] + 1) ? TF_LINK : 0)));
     desc.push_back(make_int4(0, 0, 1, 0));
-    for (int i = i0; i < i1; ++i) item_tab[i] = make_int2(item_row[i] - r_lo, n_r + items[i].my - my_lo);
+    for (int i = i0; i < i1; ++i) {
+      const int iz = (int)(std::lower_bound(svals.begin(), svals.end(), pitems[i].s) - svals.begin());
+      const int ix = (int)(std::lower_bound(axs.begin(), axs.end(), pitems[i].ax) - axs.begin());
+      ptab[i] = make_int4(iz, n_z + pitems[i].my - my_lo, n_z + n_y + ix, 0);
+    }
   }
 
   P.K = K;
   P.M = M;
   P.n_items = n_items;
   P.n_rows = n_rows;
+  P.M1 = M1;
+  P.n_pitems = n_pitems;
   P.n_tiles = n_tiles;
   P.ts_max = ts_max;
   P.pchunk = std::max(1, std::min(K1_PMAX, (K1_TAB_BYTES) / (16 * (ts_max | 1))));
   for (auto &c : P.ks_cache) c.second.release();
   P.ks_cache.clear();
   int rc;
-  if ((rc = upload(h, P.item_tab, item_tab))) return rc;
+  if ((rc = upload(h, P.pitem_tab, ptab))) return rc;
   if ((rc = upload(h, P.item_my, item_my))) return rc;
   if ((rc = upload(h, P.item_row, item_row))) return rc;
   if ((rc = upload(h, P.rows, rows))) return rc;
@@ -1512,6 +1742,10 @@ int build_plan(ewb_handle *h, const int64_t *m, int64_t K, const double *coeff) 
   if ((rc = upload(h, P.tile_ts, tile_ts))) return rc;
   if ((rc = upload(h, P.slot_k, slot_k))) return rc;
   if ((rc = upload(h, P.slot_coeff, slot_coeff))) return rc;
+  if ((rc = upload(h, P.pslot_map, pslot))) return rc;
+  // C*S for the gather: padding slots stay zero for the lifetime of the plan
+  CK(h->sp.ensure(n_slots * sizeof(double2)));
+  CK(cudaMemset(h->sp.p, 0, n_slots * sizeof(double2)));
   return EWB_OK;
 }
 
@@ -1587,16 +1821,16 @@ int occupancy_k1(ewb_handle *h, int M, size_t smem, int *occ_out) {
 // d_slots (if non-null) or left in h->spart with *n_part set.
 int stage_rho(ewb_handle *h, int64_t i0, int64_t i1, int *n_part_out) {
   Plan &P = h->plan;
-  const int M = P.M;
+  const int M1 = P.M1;
   const size_t smem = 2 * (size_t)P.pchunk * (P.ts_max | 1) * sizeof(double2) +
                       (size_t)P.ts_max * sizeof(int4);
   int occ = 1;
-  int rc = occupancy_k1(h, M, smem, &occ);
+  int rc = occupancy_k1(h, M1, smem, &occ);
   if (rc) return rc;
   const int64_t n = std::max<int64_t>(0, i1 - i0);
   // many short blocks (they desynchronise the table-build phases of
   // co-resident blocks), bounded by the partial-sum buffer size
-  const size_t slot_bytes = (size_t)M * P.n_items * sizeof(double2);
+  const size_t slot_bytes = (size_t)M1 * P.n_pitems * sizeof(double4);
   const int64_t slots1 = (int64_t)h->n_sm * occ;
   int64_t n_pc = std::max<int64_t>(1, (n + K1_PPB - 1) / K1_PPB);
   n_pc = std::min<int64_t>(n_pc, std::max<int64_t>(1, (int64_t)(K1_PART_BYTES / slot_bytes)));
@@ -1606,23 +1840,23 @@ int stage_rho(ewb_handle *h, int64_t i0, int64_t i1, int *n_part_out) {
     const int64_t fit = (waves * slots1) / P.n_tiles;
     if (fit >= 1) n_pc = std::min<int64_t>(fit, std::max<int64_t>(1, (int64_t)(K1_PART_BYTES / slot_bytes)));
   }
-  n_pc = std::min<int64_t>(n_pc, std::max<int64_t>(1, n));
+  n_pc = std::min<int64_t>(n_pc, std::max<int64_t>(1, n / K1_PMAX));  // >= one chunk per block
   int64_t ppb = (n + n_pc - 1) / std::max<int64_t>(1, n_pc);
   ppb = std::max<int64_t>(1, ppb);
   n_pc = std::max<int64_t>(1, (n + ppb - 1) / ppb);
-  const size_t n_slots = (size_t)M * P.n_items;
-  CK(h->spart.ensure((size_t)n_pc * n_slots * sizeof(double2)));
+  const size_t n_pslots = (size_t)M1 * P.n_pitems;
+  CK(h->spart.ensure((size_t)n_pc * n_pslots * sizeof(double4)));
   dim3 grid(P.n_tiles, (unsigned)n_pc);
-  k1_table(M)<<<grid, K1_THREADS, smem, h->stream>>>(
+  k1_table(M1)<<<grid, K1_THREADS, smem, h->stream>>>(
       h->frac.as<double4>(), h->base.as<double2>(), i0, std::max(i0, i1), ppb, P.pchunk,
-      P.item_tab.as<int2>(), P.n_items, P.tab_desc.as<int4>(), P.tile_off.as<int>(),
-      P.tile_ts.as<int>(), h->spart.as<double2>());
+      P.pitem_tab.as<int4>(), P.n_pitems, P.tab_desc.as<int4>(), P.tile_off.as<int>(),
+      P.tile_ts.as<int>(), h->spart.as<double4>());
   CKL();
   *n_part_out = (int)n_pc;
   return EWB_OK;
 }
 
-// finalize from n_part partial slot buffers in `src`
+// finalize from a gather-layout S (caller-supplied rho, ewb_long_range)
 int stage_finalize(ewb_handle *h, const double2 *src, int n_part, double *d_rho_out,
                    double *d_u_out) {
   Plan &P = h->plan;
@@ -1634,6 +1868,23 @@ int stage_finalize(ewb_handle *h, const double2 *src, int n_part, double *d_rho_
                                                  P.slot_coeff.as<double>(), P.K, d_rho_out,
                                                  nullptr, h->sp.as<double2>(),
                                                  h->eblk.as<double>(), 1);
+  CKL();
+  k_sum<<<1, 1024, 0, h->stream>>>(h->eblk.as<double>(), nb, 1.0, d_u_out);
+  CKL();
+  return EWB_OK;
+}
+
+// finalize from n_part pair-layout partials (the structure-factor output)
+int stage_finalize_pairs(ewb_handle *h, const double4 *src, int n_part, double *d_rho_out,
+                         double *d_u_out) {
+  Plan &P = h->plan;
+  const int64_t n_pslots = (int64_t)P.M1 * P.n_pitems;
+  const unsigned nb = blocks_for(n_pslots, RED_THREADS);
+  CK(h->eblk.ensure(nb * sizeof(double)));
+  k2p_finalize<<<nb, RED_THREADS, 0, h->stream>>>(src, n_part, n_pslots, P.pslot_map.as<int4>(),
+                                                  P.slot_coeff.as<double>(), P.K, d_rho_out,
+                                                  nullptr, h->sp.as<double2>(),
+                                                  h->eblk.as<double>(), 1);
   CKL();
   k_sum<<<1, 1024, 0, h->stream>>>(h->eblk.as<double>(), nb, 1.0, d_u_out);
   CKL();
@@ -1879,7 +2130,7 @@ int pipeline_seg(ewb_handle *h, int seg, const double *d_pos, const double *d_q,
     case 3: {
       int n_part = 0;
       if ((rc = stage_rho(h, 0, h->n, &n_part))) return rc;
-      return stage_finalize(h, h->spart.as<double2>(), n_part, d_rho_out, en + 1);
+      return stage_finalize_pairs(h, h->spart.as<double4>(), n_part, d_rho_out, en + 1);
     }
     default:
       if ((rc = stage_recip_forces(h, 0, h->n, d_force, false, nullptr))) return rc;
@@ -2052,6 +2303,14 @@ int ewb_set_stream(ewb_handle *h, uintptr_t stream) {
   return EWB_OK;
 }
 
+int ewb_set_max_pair_segment(ewb_handle *h, int mcap1) {
+  if (!h) return EWB_EINVAL;
+  ++h->gen;
+  if (mcap1 < 1 || mcap1 > MAXM1) return h->fail(EWB_EINVAL, "pair segment length must be in [1, 20]");
+  h->mcap1 = mcap1;
+  return EWB_OK;
+}
+
 int ewb_set_max_segment(ewb_handle *h, int mcap) {
   if (!h) return EWB_EINVAL;
   ++h->gen;
@@ -2106,14 +2365,16 @@ int ewb_set_kspace(ewb_handle *h, const int64_t *m_int, int64_t K, const double 
   return EWB_OK;
 }
 
-int ewb_kspace_info(const ewb_handle *h, int64_t *info6) {
-  if (!h || !info6) return EWB_EINVAL;
-  info6[0] = h->plan.K;
-  info6[1] = h->plan.n_items;
-  info6[2] = h->plan.M;
-  info6[3] = h->plan.n_rows;
-  info6[4] = h->plan.n_tiles;
-  info6[5] = h->plan.ts_max;
+int ewb_kspace_info(const ewb_handle *h, int64_t *info8) {
+  if (!h || !info8) return EWB_EINVAL;
+  info8[0] = h->plan.K;
+  info8[1] = h->plan.n_items;
+  info8[2] = h->plan.M;
+  info8[3] = h->plan.n_rows;
+  info8[4] = h->plan.n_tiles;
+  info8[5] = h->plan.ts_max;
+  info8[6] = h->plan.n_pitems;
+  info8[7] = h->plan.M1;
   return EWB_OK;
 }
 
@@ -2127,8 +2388,8 @@ int ewb_compute_rho_hat(ewb_handle *h, const double *pos, const double *q, int64
   CK(h->energy.ensure(8 * sizeof(double)));
   int n_part = 0;
   if ((rc = stage_rho(h, 0, n, &n_part))) return rc;
-  if ((rc = stage_finalize(h, h->spart.as<double2>(), n_part, h->rho.as<double>(),
-                           h->energy.as<double>() + 1)))
+  if ((rc = stage_finalize_pairs(h, h->spart.as<double4>(), n_part, h->rho.as<double>(),
+                                 h->energy.as<double>() + 1)))
     return rc;
   CK(cudaMemcpyAsync(rho_out, h->rho.p, 2 * h->plan.K * sizeof(double), cudaMemcpyDeviceToHost,
                      h->stream));
@@ -2248,7 +2509,7 @@ int ewb_dev_load(ewb_handle *h, const double *d_pos, const double *d_q, int64_t 
 
 int64_t ewb_dev_slot_doubles(const ewb_handle *h) {
   if (!h || !h->have_kspace) return -1;
-  return 2 * (int64_t)h->plan.M * h->plan.n_items;
+  return 4 * (int64_t)h->plan.M1 * h->plan.n_pitems;
 }
 
 int ewb_dev_rho_partial(ewb_handle *h, int64_t i0, int64_t i1, double *d_slots) {
@@ -2256,18 +2517,18 @@ int ewb_dev_rho_partial(ewb_handle *h, int64_t i0, int64_t i1, double *d_slots) 
   if (rc) return rc;
   if (i0 < 0 || i1 > h->n || i0 > i1) return h->fail(EWB_EINVAL, "bad particle range");
   CK(cudaSetDevice(h->device));
-  const int64_t n_slots = (int64_t)h->plan.M * h->plan.n_items;
+  const int64_t n_pslots = (int64_t)h->plan.M1 * h->plan.n_pitems;
   if (i1 == i0) {
-    CK(cudaMemsetAsync(d_slots, 0, n_slots * sizeof(double2), h->stream));
+    CK(cudaMemsetAsync(d_slots, 0, n_pslots * sizeof(double4), h->stream));
     return EWB_OK;
   }
   int n_part = 0;
   if ((rc = stage_rho(h, i0, i1, &n_part))) return rc;
-  const unsigned nb = blocks_for(n_slots, RED_THREADS);
-  k2_finalize<<<nb, RED_THREADS, 0, h->stream>>>(h->spart.as<double2>(), n_part, n_slots, nullptr,
-                                                 nullptr, h->plan.K, nullptr,
-                                                 reinterpret_cast<double2 *>(d_slots), nullptr,
-                                                 nullptr, 0);
+  const unsigned nb = blocks_for(n_pslots, RED_THREADS);
+  k2p_finalize<<<nb, RED_THREADS, 0, h->stream>>>(h->spart.as<double4>(), n_part, n_pslots,
+                                                  nullptr, nullptr, h->plan.K, nullptr,
+                                                  reinterpret_cast<double4 *>(d_slots), nullptr,
+                                                  nullptr, 0);
   CKL();
   return EWB_OK;
 }
@@ -2277,8 +2538,8 @@ int ewb_dev_kspace_finalize(ewb_handle *h, const double *d_slots, double *d_rho_
   if (rc) return rc;
   CK(cudaSetDevice(h->device));
   CK(h->energy.ensure(8 * sizeof(double)));
-  if ((rc = stage_finalize(h, reinterpret_cast<const double2 *>(d_slots), 1, d_rho_out,
-                           h->energy.as<double>() + 1)))
+  if ((rc = stage_finalize_pairs(h, reinterpret_cast<const double4 *>(d_slots), 1, d_rho_out,
+                                 h->energy.as<double>() + 1)))
     return rc;
   if (u_lr) {
     CK(cudaMemcpyAsync(u_lr, h->energy.as<double>() + 1, sizeof(double), cudaMemcpyDeviceToHost,

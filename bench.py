@@ -41,11 +41,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 # algorithmic FP64 flops per particle.k pair of this formulation
-# (DESIGN.md section 4): K1 2 DFMA + 2 DADD = 6; K3 4 DFMA + 1 DADD = 9
+# (DESIGN.md section 4): K1 (+-m_x pair items) 3 DFMA = 6; K3 4 DFMA + 1 DADD = 9
 FLOPS_K1 = 6.0
 FLOPS_K3 = 9.0
-# FP64 pipe instructions per pair (K1 4, K3 5)
-INSTR_K1 = 4.0
+# FP64 pipe instructions per pair (K1 3, K3 5)
+INSTR_K1 = 3.0
 INSTR_K3 = 5.0
 
 

@@ -94,6 +94,17 @@ int ewb_set_kspace(ewb_handle *h, const int64_t *m_int, int64_t K,
 /* plan summary: [K, n_items, M, n_rows, n_tiles, max_table, n_pair_items, M1] */
 int ewb_kspace_info(const ewb_handle *h, int64_t *info8);
 
+/* Force-field switches of the reference's ForceAssembler (driver.py:81-126):
+ * Coulomb (Ewald) on/off, and the energy-shifted 12-6 Lennard-Jones pair
+ * term fused into the real-space traversal.  LJ constants are the
+ * reference's lj_kernel consts (potentials.py:74-79): sigma^2, 4 eps,
+ * energy_shift(), 24 eps; rc2_lj = r_cutoff_lj**2 as computed by the caller. */
+int ewb_set_coulomb(ewb_handle *h, int on);
+int ewb_set_lj(ewb_handle *h, int on, double sigma2, double four_eps, double shift,
+               double tf_eps, double rc_lj, double rc2_lj);
+/* energies of the last evaluation: u_sr, u_lr, u_self, u_lj */
+int ewb_last_energies(ewb_handle *h, double *out4);
+
 /* ---- host-pointer entry points (reference-facing) ---- */
 int ewb_compute_rho_hat(ewb_handle *h, const double *pos, const double *q,
                         int64_t n, double *rho_out);
@@ -136,6 +147,13 @@ int ewb_dev_self_energy(ewb_handle *h, double *u_self);
 int ewb_dev_evaluate(ewb_handle *h, const double *d_pos, const double *d_q,
                      int64_t n, double *d_force, double *d_rho_out,
                      double *energies, double *timings);
+/* Device-resident velocity Verlet (driver.py:134-153), arrays (N,3)/(N,):
+ * kick_drift: v += dt/2 F/m, r += dt v, wrap into [0, L);
+ * kick: (if kick) v += dt/2 F/m, then kinetic = 0.5 sum m v.v. */
+int ewb_dev_md_kick_drift(ewb_handle *h, double *d_pos, double *d_vel, const double *d_force,
+                          const double *d_mass, int64_t n, double dt);
+int ewb_dev_md_kick(ewb_handle *h, double *d_vel, const double *d_force, const double *d_mass,
+                    int64_t n, double dt, int kick, double *kinetic);
 /* Sustained FP64 DFMA throughput of this device (TFLOP/s), measured with
  * independent fma chains; the FP64 roofline denominator. */
 int ewb_probe_fp64_peak(ewb_handle *h, double *tflops);

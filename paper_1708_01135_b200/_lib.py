@@ -67,6 +67,11 @@ SIGNATURES = {
     "ewb_dev_real_space": (_INT, [_P, _INT, _INT, _P, _P]),
     "ewb_dev_self_energy": (_INT, [_P, _P]),
     "ewb_dev_evaluate": (_INT, [_P, _P, _P, _I64, _P, _P, _P, _P]),
+    "ewb_set_coulomb": (_INT, [_P, _INT]),
+    "ewb_set_lj": (_INT, [_P, _INT, _D, _D, _D, _D, _D, _D]),
+    "ewb_last_energies": (_INT, [_P, _P]),
+    "ewb_dev_md_kick_drift": (_INT, [_P, _P, _P, _P, _P, _I64, _D]),
+    "ewb_dev_md_kick": (_INT, [_P, _P, _P, _P, _I64, _D, _INT, _P]),
     "ewb_probe_fp64_peak": (_INT, [_P, _P]),
     "ewb_launch_count": (_I64, [_P]),
 }
@@ -205,6 +210,32 @@ class Handle:
 
     def set_stream(self, stream_ptr):
         self._check(self.lib.ewb_set_stream(self.h, int(stream_ptr)))
+
+    def set_coulomb(self, on):
+        self._check(self.lib.ewb_set_coulomb(self.h, 1 if on else 0))
+
+    def set_lj(self, on, sigma2=0.0, four_eps=0.0, shift=0.0, tf_eps=0.0,
+               rc_lj=0.0):
+        rc_lj = float(rc_lj)
+        self._check(self.lib.ewb_set_lj(self.h, 1 if on else 0, float(sigma2),
+                                        float(four_eps), float(shift),
+                                        float(tf_eps), rc_lj, rc_lj**2))
+
+    def last_energies(self):
+        out = np.zeros(4)
+        self._check(self.lib.ewb_last_energies(self.h, _ptr(out)))
+        return out
+
+    def dev_md_kick_drift(self, d_pos, d_vel, d_force, d_mass, n, dt):
+        self._check(self.lib.ewb_dev_md_kick_drift(self.h, d_pos, d_vel, d_force,
+                                                   d_mass, int(n), float(dt)))
+
+    def dev_md_kick(self, d_vel, d_force, d_mass, n, dt, kick=True):
+        ke = ctypes.c_double(0.0)
+        self._check(self.lib.ewb_dev_md_kick(self.h, d_vel, d_force, d_mass, int(n),
+                                             float(dt), 1 if kick else 0,
+                                             ctypes.byref(ke)))
+        return ke.value
 
     def probe_fp64_peak(self):
         out = ctypes.c_double(0.0)

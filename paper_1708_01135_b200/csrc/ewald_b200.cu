@@ -845,6 +845,9 @@ struct RSParams {
   int jsplit;          // scan-all mode: candidate range split over this many warps
   int c_lo, c_hi;
   int64_t n;
+  int coul;            // screened Coulomb on pairs with r2 < rc2c
+  double rc2c;         // Coulomb cutoff^2 (rc2 = traversal cutoff^2 = max)
+  double rc2lj, lj_s2, lj_4e, lj_shift, lj_24e;  // shifted 12-6 LJ (potentials.py:21-45)
 };
 
 // dx exactly as the reference: fl(xi - xj) then one fold by +-L
@@ -878,11 +881,13 @@ constexpr int K6_LIST = 32 * K6_G + 32;  // pending pairs per warp
 #ifndef K6_MINB
 #define K6_MINB 4
 #endif
+template <bool LJ>
 __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
     k6_real_space(const double4 *__restrict__ sorted, const int *__restrict__ sorted_cell,
                   const int *__restrict__ order, const int *__restrict__ cell_start,
                   const int *__restrict__ row_ustart, RSParams P, double *__restrict__ force,
-                  double *__restrict__ eblk, int *__restrict__ err) {
+                  double *__restrict__ eblk, double *__restrict__ eblk_lj,
+                  int *__restrict__ err) {
   // A warp owns K6_G consecutive particles (centres) of one row of cells
   // (fixed cy, cz).  Lanes stream the candidates of the stencil rows --
   // contiguous runs of cells along x, so each 32-wide step is dense -- test
@@ -907,7 +912,7 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
   const int uw = blockIdx.x * K6_WARPS + warp;  // (unit, candidate split)
   const int u = u_lo + uw / P.jsplit;
   const int jpart = uw % P.jsplit;
-  double ue = 0.0;
+  double ue = 0.0, ue_lj = 0.0;
   if (u < u_hi) {
     int lo = r_lo, hi = r_hi - 1;
     while (lo < hi) {
@@ -949,13 +954,26 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
       const double r2 = zero ? 1.0 : r2raw;
       // sc = erfc(sqrt(alpha) r)/r, g = qq (sc + 2 sqrt(alpha/pi) e^{-alpha r^2})/r^2
       // (ewald.py:214-218), with one exp shared by erfc and the force
-      const double qq = zero ? 0.0 : pi.w * pj.w;
+      const bool coul = P.coul && r2raw < P.rc2c;
+      const double qq = (zero || !coul) ? 0.0 : pi.w * pj.w;
       const double inv_r = rsqrt_pos(r2);
       const double r = r2 * inv_r;
       const double ex = exp_neg(-P.al * r2);
       const double sc = erfc_from_exp(P.sa * r, ex, s_erfcx) * inv_r;
       ue = fma(P.half ? qq : 0.5 * qq, sc, ue);  // ordered pairs carry 1/2 (ewald.py:217)
-      gg = qq * fma(P.tsap, ex, sc) * (inv_r * inv_r);
+      const double inv_r2 = inv_r * inv_r;
+      gg = qq * fma(P.tsap, ex, sc) * inv_r2;
+      if (LJ) {
+        // shifted 12-6 (potentials.py:33-45): u = 4e (s12 - s6) - shift,
+        // g = 24e (2 s12 - s6) / r2, on pairs with r2 < rc_lj^2
+        const bool lj = !zero && r2raw < P.rc2lj;
+        const double s2 = P.lj_s2 * inv_r2;
+        const double s6 = s2 * s2 * s2;
+        const double s12 = s6 * s6;
+        const double ulj = fma(P.lj_4e, s12 - s6, -P.lj_shift);
+        ue_lj += lj ? (P.half ? ulj : 0.5 * ulj) : 0.0;
+        gg += lj ? P.lj_24e * fma(2.0, s12, -s6) * inv_r2 : 0.0;
+      }
     };
     auto accum = [&](const uint2 e, double dx, double dy, double dz, double gg) {
       const int g = (int)(e.y & 15u);
@@ -1194,6 +1212,17 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
     for (int w = 0; w < K6_WARPS; ++w) b += sh[w];
     eblk[blockIdx.x] = b;
   }
+  if (LJ) {
+    __syncthreads();
+    ue_lj = warp_sum(ue_lj);
+    if (lane == 0) sh[warp] = ue_lj;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b = 0.0;
+      for (int w = 0; w < K6_WARPS; ++w) b += sh[w];
+      eblk_lj[blockIdx.x] = b;
+    }
+  }
 }
 
 // Units per row of cells: row_ustart[r] = sum_{r'<r} ceil(count(r')/K6_G).
@@ -1298,6 +1327,57 @@ __global__ void __launch_bounds__(128)
     force[3 * i + 2] += a[2];
     eblk[i] = a[3];
   }
+}
+
+// ---------------------------------------------------------------------------
+// Device-resident velocity Verlet (velocity_verlet_step, driver.py:134-153):
+// v += 0.5 dt F/m; r += dt v; wrap into [0, L) (core.py:156-161); forces;
+// v += 0.5 dt F/m.  Kinetic energy 0.5 sum m v.v (driver.py:129-131).
+__global__ void k_md_kick_drift(double *__restrict__ pos, double *__restrict__ vel,
+                                const double *__restrict__ force, const double *__restrict__ mass,
+                                int64_t n, double dt, double L) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  // numpy's expression order, no contraction: v += ((0.5*dt)*F)*inv_m,
+  // r += dt*v, w = r - L*floor(r/L), w >= L -> w - L
+  const double inv_m = __ddiv_rn(1.0, mass[i]);
+  const double hdt = __dmul_rn(0.5, dt);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double v = __dadd_rn(vel[3 * i + a], __dmul_rn(__dmul_rn(hdt, force[3 * i + a]), inv_m));
+    vel[3 * i + a] = v;
+    const double r = __dadd_rn(pos[3 * i + a], __dmul_rn(dt, v));
+    double w = __dsub_rn(r, __dmul_rn(L, floor(__ddiv_rn(r, L))));
+    if (w >= L) w = __dsub_rn(w, L);
+    pos[3 * i + a] = w;
+  }
+}
+
+__global__ void __launch_bounds__(RED_THREADS)
+    k_md_kick(double *__restrict__ vel, const double *__restrict__ force,
+              const double *__restrict__ mass, int64_t n, double dt, int kick,
+              double *__restrict__ eblk) {
+  __shared__ double sh[RED_THREADS / 32];
+  const int64_t i = blockIdx.x * (int64_t)RED_THREADS + threadIdx.x;
+  double ke = 0.0;
+  if (i < n) {
+    const double m = mass[i];
+    const double inv_m = __ddiv_rn(1.0, m);
+    const double hdt = __dmul_rn(0.5, dt);
+    double vv = 0.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      double v = vel[3 * i + a];
+      if (kick) {
+        v = __dadd_rn(v, __dmul_rn(__dmul_rn(hdt, force[3 * i + a]), inv_m));
+        vel[3 * i + a] = v;
+      }
+      vv = fma(v, v, vv);
+    }
+    ke = m * vv;
+  }
+  const double b = block_sum<RED_THREADS>(ke, sh);
+  if (threadIdx.x == 0) eblk[blockIdx.x] = b;
 }
 
 // K7: sum q^2 (self energy) partials.
@@ -1440,6 +1520,10 @@ struct ewb_handle {
   // system
   bool have_system = false;
   double L = 0, alpha = 0, rc = 0, rc2 = 0;
+  // force-field switches (ForceAssembler, driver.py:81-126): Coulomb (Ewald)
+  // and the shifted 12-6 LJ fused into the real-space pair traversal
+  bool coul_on = true, lj_on = false;
+  double rc_lj = 0, rc2_lj = 0, lj_s2 = 0, lj_4e = 0, lj_shift = 0, lj_24e = 0;
   // k-space
   bool have_kspace = false;
   Plan plan;
@@ -1448,7 +1532,7 @@ struct ewb_handle {
   bool loaded = false;
   DBuf pos, q, force, rho;                   // host-API staging (caller layout)
   DBuf frac, base, xyzq;                     // derived
-  DBuf spart, sslot, sp, fpart, upart, eblk, eblk2, energy, errflag;
+  DBuf spart, sslot, sp, fpart, upart, eblk, eblk2, eblk_lj, energy, errflag;
   DBuf cell_of, slot, count, start, gstart, order_tmp, order, sorted, sorted_cell, row_ustart;
   // CUDA graph of the device pipeline (prep + real space + S(k) + forces +
   // self energy), captured on the second call with an unchanged key
@@ -1941,31 +2025,47 @@ int stage_recip_forces(ewb_handle *h, int64_t i0, int64_t i1, double *d_force, b
 // Cell list + real space for z-slab part/nparts; u_sr into d_u_out.
 constexpr int RS_CELLS = 1, RS_PAIRS = 2;
 int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, double *d_u_out,
-                     cudaEvent_t ev_cell, int which = RS_CELLS | RS_PAIRS) {
+                     cudaEvent_t ev_cell, int which = RS_CELLS | RS_PAIRS,
+                     double *d_ulj_out = nullptr) {
   const int64_t n = h->n;
-  if (!(h->rc > 0.0)) return h->fail(EWB_EINVAL, "cutoff must be positive");
-  if (h->rc > 0.5 * h->L) {
+  const bool coul_on = h->coul_on, lj_on = h->lj_on;
+  if (coul_on && !(h->rc > 0.0)) return h->fail(EWB_EINVAL, "cutoff must be positive");
+  const bool wide = coul_on && h->rc > 0.5 * h->L;
+  if (wide) {
     // r_c > L/2: the reference's image-shell path (ewald.py:553-576)
     if (h->rc > h->L)
       return h->fail(EWB_EBOX, "r_cutoff exceeds the box edge; a single image shell no longer "
                                "covers the interaction range");
     if (n > WIDE_MAX_N)
       return h->fail(EWB_ESIZE, "wide-cutoff real-space path is O(N^2); N exceeds the 4096 guard");
-    if (!(which & RS_PAIRS)) return EWB_OK;
-    if (part != 0) {  // not sharded: the first part owns every centre
-      CK(cudaMemsetAsync(d_u_out, 0, sizeof(double), h->stream));
-      return EWB_OK;
+    if (which & RS_PAIRS) {
+      if (part != 0) {  // not sharded: the first part owns every centre
+        CK(cudaMemsetAsync(d_u_out, 0, sizeof(double), h->stream));
+      } else {
+        CK(h->eblk.ensure(n * sizeof(double)));
+        k6w_wide<<<(unsigned)n, 128, 0, h->stream>>>(h->xyzq.as<double4>(), n, h->L, h->rc2,
+                                                     std::sqrt(h->alpha), h->alpha,
+                                                     2.0 * std::sqrt(h->alpha / M_PI), d_force,
+                                                     h->eblk.as<double>(), h->errflag.as<int>());
+        CKL();
+        k_sum<<<1, 1024, 0, h->stream>>>(h->eblk.as<double>(), n, 1.0, d_u_out);
+        CKL();
+      }
     }
-    CK(h->eblk.ensure(n * sizeof(double)));
-    k6w_wide<<<(unsigned)n, 128, 0, h->stream>>>(h->xyzq.as<double4>(), n, h->L, h->rc2,
-                                                 std::sqrt(h->alpha), h->alpha,
-                                                 2.0 * std::sqrt(h->alpha / M_PI), d_force,
-                                                 h->eblk.as<double>(), h->errflag.as<int>());
-    CKL();
-    k_sum<<<1, 1024, 0, h->stream>>>(h->eblk.as<double>(), n, 1.0, d_u_out);
-    CKL();
+  } else if ((which & RS_PAIRS) && !coul_on) {
+    CK(cudaMemsetAsync(d_u_out, 0, sizeof(double), h->stream));
+  }
+  if (!((coul_on && !wide) || lj_on)) {
+    if ((which & RS_PAIRS) && d_ulj_out) CK(cudaMemsetAsync(d_ulj_out, 0, sizeof(double), h->stream));
     return EWB_OK;
   }
+  if (lj_on && !(h->rc_lj > 0.0)) return h->fail(EWB_EINVAL, "cutoff must be positive");
+  if (lj_on && h->rc_lj > 0.5 * h->L)
+    return h->fail(EWB_ECUTOFF, "LJ cutoff exceeds L/2 (minimum-image bound)");
+  // one traversal at the larger cutoff; each term keeps its own exact predicate
+  const bool pair_coul = coul_on && !wide;
+  const double rc_t = std::max(pair_coul ? h->rc : 0.0, lj_on ? h->rc_lj : 0.0);
+  const double rc2_t = std::max(pair_coul ? h->rc2 : 0.0, lj_on ? h->rc2_lj : 0.0);
   // reference binning: cpd = floor(L / r_c), edge = L / cpd (celllist.py:96-98);
   // with cpd < 3 the 27-stencil folds onto every cell and the reference scans
   // all particles with a per-pair fold (engine.py:111-134) -- FOLD mode here.
@@ -1975,10 +2075,10 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
   // Any cell size whose stencil covers the cutoff sphere visits the same
   // pair set: the predicate, not the binning, decides membership.
   int rad = 2;
-  int cpd = (int)std::floor(2.0 * h->L / h->rc);
+  int cpd = (int)std::floor(2.0 * h->L / rc_t);
   if (cpd < 5 || h->stencil_rad == 1) {
     rad = 1;
-    cpd = (int)std::floor(h->L / h->rc);
+    cpd = (int)std::floor(h->L / rc_t);
   }
   if (cpd < 1) cpd = 1;
   if (cpd > 64) cpd = 64;  // edge stays >= r_c/rad; bounds the cell arrays
@@ -2034,7 +2134,14 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
   RSParams rp;
   rp.L = h->L;
   rp.hl = 0.5 * h->L;
-  rp.rc2 = h->rc2;
+  rp.rc2 = rc2_t;
+  rp.coul = pair_coul ? 1 : 0;
+  rp.rc2c = h->rc2;
+  rp.rc2lj = h->rc2_lj;
+  rp.lj_s2 = h->lj_s2;
+  rp.lj_4e = h->lj_4e;
+  rp.lj_shift = h->lj_shift;
+  rp.lj_24e = h->lj_24e;
   rp.sa = std::sqrt(h->alpha);
   rp.al = h->alpha;
   rp.tsap = 2.0 * std::sqrt(h->alpha / M_PI);
@@ -2060,16 +2167,31 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
   const unsigned nb = (unsigned)std::max<int64_t>(
       1, (units_max * rp.jsplit + K6_WARPS - 1) / K6_WARPS);
   CK(h->eblk.ensure(nb * sizeof(double)));
+  if (lj_on) CK(h->eblk_lj.ensure(nb * sizeof(double)));
   if (rows_slab <= 0) {
-    CK(cudaMemsetAsync(d_u_out, 0, sizeof(double), h->stream));
+    if (pair_coul) CK(cudaMemsetAsync(d_u_out, 0, sizeof(double), h->stream));
+    if (lj_on && d_ulj_out) CK(cudaMemsetAsync(d_ulj_out, 0, sizeof(double), h->stream));
     return EWB_OK;
   }
-  k6_real_space<<<nb, K6_WARPS * 32, 0, h->stream>>>(
-      h->sorted.as<double4>(), h->sorted_cell.as<int>(), h->order.as<int>(), h->start.as<int>(),
-      h->row_ustart.as<int>(), rp, d_force, h->eblk.as<double>(), h->errflag.as<int>());
+  if (lj_on)
+    k6_real_space<true><<<nb, K6_WARPS * 32, 0, h->stream>>>(
+        h->sorted.as<double4>(), h->sorted_cell.as<int>(), h->order.as<int>(), h->start.as<int>(),
+        h->row_ustart.as<int>(), rp, d_force, h->eblk.as<double>(), h->eblk_lj.as<double>(),
+        h->errflag.as<int>());
+  else
+    k6_real_space<false><<<nb, K6_WARPS * 32, 0, h->stream>>>(
+        h->sorted.as<double4>(), h->sorted_cell.as<int>(), h->order.as<int>(), h->start.as<int>(),
+        h->row_ustart.as<int>(), rp, d_force, h->eblk.as<double>(), nullptr,
+        h->errflag.as<int>());
   CKL();
-  k_sum<<<1, 1024, 0, h->stream>>>(h->eblk.as<double>(), nb, 1.0, d_u_out);
-  CKL();
+  if (pair_coul) {
+    k_sum<<<1, 1024, 0, h->stream>>>(h->eblk.as<double>(), nb, 1.0, d_u_out);
+    CKL();
+  }
+  if (lj_on && d_ulj_out) {
+    k_sum<<<1, 1024, 0, h->stream>>>(h->eblk_lj.as<double>(), nb, 1.0, d_ulj_out);
+    CKL();
+  }
   return EWB_OK;
 }
 
@@ -2126,13 +2248,21 @@ int pipeline_seg(ewb_handle *h, int seg, const double *d_pos, const double *d_q,
     case 1:
       return stage_real_space(h, 0, 1, d_force, en + 0, nullptr, RS_CELLS);
     case 2:
-      return stage_real_space(h, 0, 1, d_force, en + 0, nullptr, RS_PAIRS);
+      return stage_real_space(h, 0, 1, d_force, en + 0, nullptr, RS_PAIRS, en + 3);
     case 3: {
+      if (!h->coul_on) {
+        CK(cudaMemsetAsync(en + 1, 0, sizeof(double), h->stream));
+        return EWB_OK;
+      }
       int n_part = 0;
       if ((rc = stage_rho(h, 0, h->n, &n_part))) return rc;
       return stage_finalize_pairs(h, h->spart.as<double4>(), n_part, d_rho_out, en + 1);
     }
     default:
+      if (!h->coul_on) {
+        CK(cudaMemsetAsync(en + 2, 0, sizeof(double), h->stream));
+        return EWB_OK;
+      }
       if ((rc = stage_recip_forces(h, 0, h->n, d_force, false, nullptr))) return rc;
       return stage_self(h, en + 2);
   }
@@ -2281,7 +2411,8 @@ void ewb_destroy(ewb_handle *h) {
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   for (DBuf *b : {&h->pos, &h->q, &h->force, &h->rho, &h->frac, &h->base, &h->xyzq, &h->spart,
-                  &h->sslot, &h->sp, &h->fpart, &h->upart, &h->eblk, &h->eblk2, &h->energy,
+                  &h->sslot, &h->sp, &h->fpart, &h->upart, &h->eblk, &h->eblk2, &h->eblk_lj,
+                  &h->energy,
                   &h->errflag, &h->cell_of, &h->slot, &h->count, &h->start, &h->gstart,
                   &h->order_tmp, &h->order, &h->sorted, &h->sorted_cell, &h->row_ustart})
     b->release();
@@ -2324,6 +2455,70 @@ int ewb_set_stencil(ewb_handle *h, int rad) {
   ++h->gen;
   if (rad < 0 || rad > 2) return h->fail(EWB_EINVAL, "stencil radius must be 0 (auto), 1 or 2");
   h->stencil_rad = rad;
+  return EWB_OK;
+}
+
+int ewb_set_coulomb(ewb_handle *h, int on) {
+  if (!h) return EWB_EINVAL;
+  h->coul_on = on != 0;
+  ++h->gen;
+  return EWB_OK;
+}
+
+int ewb_set_lj(ewb_handle *h, int on, double sigma2, double four_eps, double shift,
+               double tf_eps, double rc_lj, double rc2_lj) {
+  if (!h) return EWB_EINVAL;
+  ++h->gen;
+  if (on && !(rc_lj > 0.0)) return h->fail(EWB_EINVAL, "cutoff must be positive");
+  h->lj_on = on != 0;
+  h->lj_s2 = sigma2;
+  h->lj_4e = four_eps;
+  h->lj_shift = shift;
+  h->lj_24e = tf_eps;
+  h->rc_lj = rc_lj;
+  h->rc2_lj = rc2_lj;
+  return EWB_OK;
+}
+
+int ewb_last_energies(ewb_handle *h, double *out4) {
+  if (!h || !out4) return EWB_EINVAL;
+  CK(cudaSetDevice(h->device));
+  CK(h->energy.ensure(8 * sizeof(double)));
+  CK(cudaMemcpyAsync(out4, h->energy.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return EWB_OK;
+}
+
+int ewb_dev_md_kick_drift(ewb_handle *h, double *d_pos, double *d_vel, const double *d_force,
+                          const double *d_mass, int64_t n, double dt) {
+  int rc = require_state(h, false, false);
+  if (rc) return rc;
+  if (n < 1) return h->fail(EWB_EINVAL, "particle count must be >= 1");
+  CK(cudaSetDevice(h->device));
+  k_md_kick_drift<<<blocks_for(n, 256), 256, 0, h->stream>>>(d_pos, d_vel, d_force, d_mass, n,
+                                                             dt, h->L);
+  CKL();
+  return EWB_OK;
+}
+
+int ewb_dev_md_kick(ewb_handle *h, double *d_vel, const double *d_force, const double *d_mass,
+                    int64_t n, double dt, int kick, double *kinetic) {
+  if (!h) return EWB_EINVAL;
+  if (n < 1) return h->fail(EWB_EINVAL, "particle count must be >= 1");
+  CK(cudaSetDevice(h->device));
+  const unsigned nb = blocks_for(n, RED_THREADS);
+  CK(h->eblk2.ensure(nb * sizeof(double)));
+  CK(h->energy.ensure(8 * sizeof(double)));
+  k_md_kick<<<nb, RED_THREADS, 0, h->stream>>>(d_vel, d_force, d_mass, n, dt, kick ? 1 : 0,
+                                               h->eblk2.as<double>());
+  CKL();
+  k_sum<<<1, 1024, 0, h->stream>>>(h->eblk2.as<double>(), nb, 0.5, h->energy.as<double>() + 4);
+  CKL();
+  if (kinetic) {
+    CK(cudaMemcpyAsync(kinetic, h->energy.as<double>() + 4, sizeof(double), cudaMemcpyDeviceToHost,
+                       h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+  }
   return EWB_OK;
 }
 
@@ -2471,16 +2666,17 @@ int ewb_self_energy(ewb_handle *h, const double *q, int64_t n, double *u_self) {
 
 int ewb_evaluate(ewb_handle *h, const double *pos, const double *q, int64_t n,
                  double *force_inout, double *rho_out, double *energies, double *timings) {
-  int rc = require_state(h, true, false);
+  int rc = require_state(h, h && h->coul_on, false);
   if (rc) return rc;
   CK(cudaSetDevice(h->device));
-  if (!(h->rc > 0.0)) return h->fail(EWB_EINVAL, "cutoff must be positive");
+  if (h->coul_on && !(h->rc > 0.0)) return h->fail(EWB_EINVAL, "cutoff must be positive");
   if (!pos || !q) return h->fail(EWB_EINVAL, "null particle arrays");
   if (n < 1) return h->fail(EWB_EINVAL, "particle count must be >= 1");
   CK(h->pos.ensure(n * 3 * sizeof(double)));
   CK(h->q.ensure(n * sizeof(double)));
   CK(h->force.ensure(n * 3 * sizeof(double)));
-  if (rho_out) CK(h->rho.ensure(2 * h->plan.K * sizeof(double)));
+  if (rho_out && h->coul_on) CK(h->rho.ensure(2 * h->plan.K * sizeof(double)));
+  if (!h->coul_on) rho_out = nullptr;
   CK(cudaMemcpyAsync(h->pos.p, pos, n * 3 * sizeof(double), cudaMemcpyHostToDevice, h->stream));
   CK(cudaMemcpyAsync(h->q.p, q, n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
   CK(cudaMemcpyAsync(h->force.p, force_inout, n * 3 * sizeof(double), cudaMemcpyHostToDevice,
@@ -2490,7 +2686,9 @@ int ewb_evaluate(ewb_handle *h, const double *pos, const double *q, int64_t n,
     return rc;
   double en[3];
   CK(cudaMemcpyAsync(en, h->energy.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-  if ((rc = check_errflag(h, (h->rc > 0.5 * h->L ? 0 : ERR_UNWRAPPED) | ERR_COINCIDENT)))
+  if ((rc = check_errflag(
+           h, ((h->coul_on && h->rc > 0.5 * h->L && !h->lj_on) ? 0 : ERR_UNWRAPPED) |
+                  ERR_COINCIDENT)))
     return rc;
   CK(cudaMemcpy(force_inout, h->force.p, n * 3 * sizeof(double), cudaMemcpyDeviceToHost));
   if (rho_out)
@@ -2589,14 +2787,17 @@ int ewb_dev_self_energy(ewb_handle *h, double *u_self) {
 
 int ewb_dev_evaluate(ewb_handle *h, const double *d_pos, const double *d_q, int64_t n,
                      double *d_force, double *d_rho_out, double *energies, double *timings) {
-  int rc = require_state(h, true, false);
+  int rc = require_state(h, h && h->coul_on, false);
   if (rc) return rc;
   CK(cudaSetDevice(h->device));
-  if (!(h->rc > 0.0)) return h->fail(EWB_EINVAL, "cutoff must be positive");
+  if (h->coul_on && !(h->rc > 0.0)) return h->fail(EWB_EINVAL, "cutoff must be positive");
+  if (!h->coul_on) d_rho_out = nullptr;
   if ((rc = run_eval(h, d_pos, d_q, n, d_force, d_rho_out, timings != nullptr))) return rc;
   double en[3];
   CK(cudaMemcpyAsync(en, h->energy.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-  if ((rc = check_errflag(h, (h->rc > 0.5 * h->L ? 0 : ERR_UNWRAPPED) | ERR_COINCIDENT)))
+  if ((rc = check_errflag(
+           h, ((h->coul_on && h->rc > 0.5 * h->L && !h->lj_on) ? 0 : ERR_UNWRAPPED) |
+                  ERR_COINCIDENT)))
     return rc;
   if (energies) std::memcpy(energies, en, sizeof en);
   return read_timings(h, timings);

@@ -166,10 +166,46 @@ def config_case(name):
          **extra)
 
 
+def md_cases():
+    """Reference ForceAssembler (Coulomb + LJ, LJ only) and a short NVE run."""
+    from ewaldmd.driver import ForceAssembler
+    rng = np.random.default_rng(77)
+    ps = em.init_rocksalt(2, 3.5)            # N=64, L=14
+    ps.position += 0.15 * rng.standard_normal(ps.position.shape)
+    ps.wrap()
+    pos0 = ps.position.copy()
+    for tag, coul in (("md_fa_coul_lj", True), ("md_fa_lj", False)):
+        cfg = em.SimConfig(n_particles=64, box_edge=14.0, tolerance=1e-6,
+                           coulomb_on=coul, lj_on=True, threads=WORKERS,
+                           lj=em.LJParams(epsilon_lj=1.0, sigma=2.5, r_cutoff_lj=6.25))
+        ps.position[:] = pos0
+        fa = ForceAssembler(ps, cfg)
+        pe = fa(ps)
+        save(tag, pos=pos0, q=ps.charge.copy(), L=14.0, pe=pe,
+             u_coulomb=fa.last["u_coulomb"], u_lj=fa.last["u_lj"],
+             force=ps.force.copy())
+    # NVE trajectory
+    cfg = em.SimConfig(n_particles=64, box_edge=14.0, tolerance=1e-6, dt=0.01,
+                       n_steps=8, velocity_scale=0.05, threads=WORKERS, seed=1,
+                       lj_on=True,
+                       lj=em.LJParams(epsilon_lj=1.0, sigma=2.5, r_cutoff_lj=6.25))
+    ps = em.init_rocksalt(2, 3.5)
+    ps.position += 0.15 * np.random.default_rng(78).standard_normal(ps.position.shape)
+    ps.wrap()
+    pos0 = ps.position.copy()
+    m = em.run(cfg, ps)
+    save("md_run", pos0=pos0, q=ps.charge.copy(), L=14.0,
+         energy_trace=np.array(m.energy_trace), pos_final=ps.position.copy(),
+         vel_final=ps.velocity.copy(), alpha=m.alpha, r_cutoff=m.r_cutoff,
+         max_disp=m.max_step_displacement)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["small", "c1", "c2", "c3", "c4", "c5"]
     for w in which:
         if w == "small":
             small_cases()
+        elif w == "md":
+            md_cases()
         else:
             config_case(w)

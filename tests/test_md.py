@@ -1,0 +1,139 @@
+"""§8(f) rows 1-2: the fused LJ term, the force assembler and the
+device-resident velocity-Verlet run against the reference driver's golden
+vectors (tests/golden/md_*.npz, from ewaldmd.driver.ForceAssembler / run)."""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import f_rms, golden, rel
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def md():
+    from paper_1708_01135_b200 import md
+    return md
+
+
+def _ps(pos, q, L):
+    import paper_1708_01135_b200 as ew
+    ps = ew.create_particle_set(pos.shape[0], ew.SimulationBox(L))
+    ps.position[:] = pos
+    ps.charge[:] = q
+    return ps
+
+
+@pytest.mark.parametrize("name,coul", [("md_fa_coul_lj", True), ("md_fa_lj", False)])
+def test_force_assembler_matches_reference(md, name, coul):
+    g = golden(name)
+    ps = _ps(g["pos"], g["q"], float(g["L"]))
+    cfg = md.SimConfig(n_particles=64, box_edge=14.0, tolerance=1e-6, coulomb_on=coul,
+                       lj_on=True, lj=md.LJParams(1.0, 2.5, 6.25))
+    fa = md.ForceAssembler(ps, cfg)
+    pe = fa(ps)
+    assert rel(fa.last["u_lj"], float(g["u_lj"])) <= 1e-10
+    if coul:
+        assert rel(fa.last["u_coulomb"], float(g["u_coulomb"])) <= 1e-10
+    else:
+        assert fa.last["u_coulomb"] == 0.0
+    assert rel(pe, float(g["pe"])) <= 1e-10
+    assert np.abs(ps.force - g["force"]).max() <= 1e-9 * f_rms(g["force"])
+    # zeroes forces each call (test_driver.py:181-193)
+    fa(ps)
+    assert np.abs(ps.force - g["force"]).max() <= 1e-9 * f_rms(g["force"])
+
+
+class TestLJPair:
+    P = None
+
+    def _pair(self, md, sep, params):
+        ps = _ps(np.array([[0.0, 0.0, 0.0], [sep, 0.0, 0.0]]), np.zeros(2), 30.0)
+        cfg = md.SimConfig(n_particles=2, box_edge=30.0, coulomb_on=False, lj_on=True,
+                           lj=params)
+        fa = md.ForceAssembler(ps, cfg)
+        fa(ps)
+        return fa.last["u_lj"], ps.force.copy(), -ps.force[0, 0]
+
+    def test_zero_crossing_and_minimum(self, md):
+        p = md.LJParams(1.0, 2.5, 6.25)
+        u, _, radial = self._pair(md, 2.5, p)
+        assert u == pytest.approx(-p.energy_shift(), rel=1e-12)
+        assert radial > 0.0
+        u, _, radial = self._pair(md, md.wca_cutoff(2.5), p)
+        assert u == pytest.approx(-1.0 - p.energy_shift(), rel=1e-12)
+        assert abs(radial) < 1e-12
+
+    def test_force_matches_analytic_and_third_law(self, md):
+        p = md.LJParams(1.0, 2.5, 6.25)
+        u, f, radial = self._pair(md, 3.1, p)
+        assert radial == pytest.approx(md.lj_pair_force(3.1, p), rel=1e-12)
+        assert u == pytest.approx(md.lj_pair_energy(3.1, p), rel=1e-12)
+        np.testing.assert_allclose(f[0], -f[1], rtol=1e-14)
+
+    def test_outside_cutoff_and_coincident(self, md):
+        import paper_1708_01135_b200 as ew
+        wca = md.LJParams(1.0, 2.5, md.wca_cutoff(2.5))
+        u, f, _ = self._pair(md, 3.5, wca)
+        assert u == 0.0 and np.all(f == 0.0)
+        with pytest.raises(ew.CoincidentParticlesError):
+            self._pair(md, 0.0, md.LJParams(1.0, 2.5, 6.25))
+
+
+def test_velocity_verlet_kinematics(md):
+    import paper_1708_01135_b200 as ew
+
+    class Constant:
+        def __init__(self, f):
+            self.f = np.asarray(f, dtype=float)
+
+        def __call__(self, ps):
+            ps.force[:] = self.f
+            return 0.0
+
+    ps = ew.create_particle_set(4, ew.SimulationBox(10.0))
+    ps.position[:] = 2.0
+    before = ps.position.copy()
+    md.velocity_verlet_step(ps, 0.1, Constant((0.0, 0.0, 0.0)))
+    np.testing.assert_array_equal(ps.position, before)
+    ps = ew.create_particle_set(1, ew.SimulationBox(10.0))
+    ps.position[:] = 5.0
+    ps.mass[:] = 2.0
+    a = Constant((0.4, 0.0, 0.0))
+    a(ps)
+    md.velocity_verlet_step(ps, 0.01, a)
+    assert ps.position[0, 0] == pytest.approx(5.0 + 0.5 * 0.2 * 1e-4, rel=1e-12)
+
+
+def test_device_run_matches_reference_trajectory(md):
+    g = golden("md_run")
+    ps = _ps(g["pos0"], g["q"], float(g["L"]))
+    cfg = md.SimConfig(n_particles=64, box_edge=14.0, tolerance=1e-6, dt=0.01, n_steps=8,
+                       velocity_scale=0.05, seed=1, lj_on=True,
+                       lj=md.LJParams(1.0, 2.5, 6.25))
+    m = md.run(cfg, ps)
+    et = np.array(m.energy_trace)
+    ref = g["energy_trace"]
+    assert et.shape == ref.shape
+    scale = np.abs(ref).max()
+    assert np.abs(et - ref).max() <= 1e-9 * scale
+    assert np.abs(ps.position - g["pos_final"]).max() <= 1e-10
+    assert np.abs(ps.velocity - g["vel_final"]).max() <= 1e-10 * np.abs(g["vel_final"]).max()
+    assert m.alpha == pytest.approx(float(g["alpha"]), rel=1e-15)
+    assert m.max_step_displacement == pytest.approx(float(g["max_disp"]), rel=1e-9)
+    assert m.drift < 1e-3
+    assert len(m.step_wall) == 8
+
+
+def test_run_zero_steps_and_determinism(md):
+    cfg = md.SimConfig(n_particles=64, box_edge=14.0, tolerance=1e-6, dt=0.01, n_steps=0,
+                       velocity_scale=0.05, seed=1, lj_on=False)
+    m = md.run(cfg)
+    assert len(m.energy_trace) == 1 and m.step_wall == [] and m.n_k > 0
+    cfg.n_steps = 3
+    e1 = md.run(cfg).total_energies
+    e2 = md.run(cfg).total_energies
+    for a, b in zip(e1, e2):
+        assert abs(a - b) <= 1e-10 * abs(a)

@@ -72,6 +72,11 @@ int ewb_set_max_pair_segment(ewb_handle *h, int mcap1);
  * per edge), 1 = r_c cells with the 3^3 stencil (the reference's grid). */
 int ewb_set_stencil(ewb_handle *h, int rad);
 
+/* Force gather with C*S in the constant bank (uniform-register operands)
+ * for systems with >= 2 particle blocks per SM (default on).  The constant
+ * bank is per process: handles must not run evaluations concurrently on
+ * different streams of the same device. */
+int ewb_set_const_gather(ewb_handle *h, int on);
 /* CUDA-graph replay of the evaluation pipeline (default on): the second
  * evaluate with unchanged shapes/pointers/configuration is captured, later
  * ones replay the graph.  0 runs every kernel eagerly. */

@@ -51,6 +51,7 @@ SIGNATURES = {
     "ewb_set_stencil": (_INT, [_P, _INT]),
     "ewb_set_deterministic": (_INT, [_P, _INT]),
     "ewb_set_graphs": (_INT, [_P, _INT]),
+    "ewb_set_const_gather": (_INT, [_P, _INT]),
     "ewb_set_system": (_INT, [_P, _D, _D, _D, _D]),
     "ewb_set_kspace": (_INT, [_P, _P, _I64, _P]),
     "ewb_kspace_info": (_INT, [_P, _P]),
@@ -192,6 +193,9 @@ class Handle:
     def set_max_pair_segment(self, mcap1):
         self._check(self.lib.ewb_set_max_pair_segment(self.h, int(mcap1)))
         self.kspace_key = None
+
+    def set_const_gather(self, on):
+        self._check(self.lib.ewb_set_const_gather(self.h, 1 if on else 0))
 
     def set_graphs(self, on):
         self._check(self.lib.ewb_set_graphs(self.h, 1 if on else 0))

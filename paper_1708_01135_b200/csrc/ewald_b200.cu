@@ -66,6 +66,9 @@ constexpr size_t K1_PART_BYTES = (size_t)512 << 20;  // cap of the partial S(k) 
 #ifndef K3_WAVES
 #define K3_WAVES 4
 #endif
+#ifndef K3C_MIN_WAVES
+#define K3C_MIN_WAVES 2           // constant-bank K3 when >= this many blocks per SM
+#endif
 constexpr int K3_THREADS = 128;
 constexpr int K3_PPT = 2;         // particles per thread in the gather
 constexpr int K3_CH = 32;         // k-items per shared-memory chunk
@@ -471,10 +474,7 @@ __global__ void __launch_bounds__(K3_THREADS, K3_MINB)
 #pragma unroll
       for (int u = 0; u < NPT; ++u) {
         const int t = threadIdx.x + u * K3_THREADS;
-        if (t < nc * M) {
-          const int m = t / nc, itc = t - m * nc;
-          stage_sp[u] = sp[(size_t)m * n_items + c0 + itc];
-        }
+        if (t < nc * M) stage_sp[u] = sp[(size_t)c0 * M + t];
       }
       if (threadIdx.x < nc) {
         stage_my = item_my[c0 + threadIdx.x];
@@ -486,10 +486,7 @@ __global__ void __launch_bounds__(K3_THREADS, K3_MINB)
 #pragma unroll
       for (int u = 0; u < NPT; ++u) {
         const int t = threadIdx.x + u * K3_THREADS;
-        if (t < nc * M) {
-          const int m = t / nc, itc = t - m * nc;
-          s_spb[b][itc * M + m] = stage_sp[u];
-        }
+        if (t < nc * M) s_spb[b][t] = stage_sp[u];
       }
       if (threadIdx.x < nc) {
         s_myb[b][threadIdx.x] = stage_my;
@@ -597,6 +594,143 @@ __global__ void __launch_bounds__(K3_THREADS, K3_MINB)
       fp[n_local + pi[q]] = Fy[q];
       fp[2 * n_local + pi[q]] = Fz[q];
       if (ENERGY) upart[(size_t)ks * n_local + pi[q]] = U[q];
+    }
+  }
+}
+
+// K3c: the force gather with C*S and the item metadata in the CONSTANT bank.
+// Every thread of a warp reads the same C*S entry, so with a warp-uniform
+// constant-bank index the operand lives in uniform registers (LDCU -> DFMA
+// ..., URx, ...), relieving the vector register file, whose operand
+// bandwidth bounds the shared-memory variant (measured: +27% FP64
+// throughput on the K3 inner loop, tools/micro/fp64uniform.cu).  The
+// k-space is walked in chunks of <= K3C_CAP slots, one launch per chunk
+// (copy-to-symbol is stream ordered); partial rows are flushed at chunk
+// ends and forces accumulate across launches.
+// Two buffers (A/B) on two streams: consecutive chunks alternate, so one
+// launch's partial last wave overlaps the next launch.
+constexpr int K3C_CAP = 1700;    // C*S slots per chunk buffer (27.2 KB)
+constexpr int K3C_ITEMS = 160;   // items per chunk (metadata)
+__constant__ double2 c_k3sp[2][K3C_CAP];
+__constant__ int4 c_k3meta[2][K3C_ITEMS];  // (m_x, s, m_y, flags: 1 new row, 2 m_y jump)
+
+template <int M, bool ENERGY, int BUF>
+__global__ void __launch_bounds__(K3_THREADS, K3_MINB)
+    k3c_force_gather(const double4 *__restrict__ frac, const double2 *__restrict__ base,
+                     int64_t p_begin, int64_t p_end, int nc, int first,
+                     double *__restrict__ fpart, double *__restrict__ upart) {
+  const int64_t n_local = p_end - p_begin;
+  int64_t pi[K3_PPT];
+  double tx[K3_PPT], ty[K3_PPT], tz[K3_PPT], c2z[K3_PPT];
+  double2 ey[K3_PPT], ez[K3_PPT], P[K3_PPT];
+  double Fx[K3_PPT], Fy[K3_PPT], Fz[K3_PPT], U[K3_PPT], SG[K3_PPT], SY[K3_PPT], SH[K3_PPT];
+#pragma unroll
+  for (int q = 0; q < K3_PPT; ++q) {
+    pi[q] = (int64_t)blockIdx.x * (K3_THREADS * K3_PPT) + q * K3_THREADS + threadIdx.x;
+    const int64_t g = p_begin + (pi[q] < n_local ? pi[q] : 0);
+    const double4 f = frac[g];
+    tx[q] = f.x;
+    ty[q] = f.y;
+    tz[q] = f.z;
+    const double2 by = base[3 * g + 1], bz = base[3 * g + 2];
+    ey[q] = make_double2(by.x, -by.y);
+    ez[q] = make_double2(bz.x, -bz.y);
+    c2z[q] = bz.x + bz.x;
+    Fx[q] = Fy[q] = Fz[q] = U[q] = SG[q] = SY[q] = SH[q] = 0.0;
+    P[q] = make_double2(1.0, 0.0);
+  }
+  int cmx = 0, cs = 0;
+  for (int itc = 0; itc < nc; ++itc) {
+    const int4 mt = c_k3meta[BUF][itc];
+    const int my = mt.z;
+    if (itc == 0 || (mt.w & 1)) {
+      if (itc > 0) {
+#pragma unroll
+        for (int q = 0; q < K3_PPT; ++q) {
+          Fx[q] = fma((double)cmx, SG[q], Fx[q]);
+          Fy[q] += SY[q];
+          Fz[q] += fma((double)(cs + M), SG[q], -SH[q]);
+          SG[q] = SY[q] = SH[q] = 0.0;
+        }
+      }
+      cmx = mt.x;
+      cs = mt.y;
+#pragma unroll
+      for (int q = 0; q < K3_PPT; ++q) P[q] = phase_plus(cmx, my, cs, tx[q], ty[q], tz[q]);
+    } else if (mt.w & 2) {
+#pragma unroll
+      for (int q = 0; q < K3_PPT; ++q) P[q] = phase_plus(cmx, my, cs, tx[q], ty[q], tz[q]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < K3_PPT; ++q) P[q] = cmul(P[q], ey[q]);
+    }
+    const double2 *spi = c_k3sp[BUF] + itc * M;
+    double2 Ap[K3_PPT], Ac[K3_PPT];
+    double G[K3_PPT], H[K3_PPT];
+    {
+      const double2 s0 = spi[0];
+#pragma unroll
+      for (int q = 0; q < K3_PPT; ++q) {
+        Ap[q] = P[q];
+        G[q] = fma(Ap[q].x, s0.y, Ap[q].y * s0.x);
+        H[q] = G[q];
+        if (ENERGY) U[q] = fma(Ap[q].x, s0.x, fma(-Ap[q].y, s0.y, U[q]));
+      }
+    }
+    if (M > 1) {
+      const double2 s1 = spi[1];
+#pragma unroll
+      for (int q = 0; q < K3_PPT; ++q) {
+        Ac[q] = cmul(P[q], ez[q]);
+        G[q] = fma(Ac[q].x, s1.y, fma(Ac[q].y, s1.x, G[q]));
+        H[q] += G[q];
+        if (ENERGY) U[q] = fma(Ac[q].x, s1.x, fma(-Ac[q].y, s1.y, U[q]));
+      }
+#pragma unroll
+      for (int m = 2; m < M; ++m) {
+        const double2 sm = spi[m];
+#pragma unroll
+        for (int q = 0; q < K3_PPT; ++q) {
+          const double2 An = make_double2(fma(c2z[q], Ac[q].x, -Ap[q].x),
+                                          fma(c2z[q], Ac[q].y, -Ap[q].y));
+          Ap[q] = Ac[q];
+          Ac[q] = An;
+          G[q] = fma(An.x, sm.y, fma(An.y, sm.x, G[q]));
+          H[q] += G[q];
+          if (ENERGY) U[q] = fma(An.x, sm.x, fma(-An.y, sm.y, U[q]));
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < K3_PPT; ++q) {
+      SG[q] += G[q];
+      SY[q] = fma((double)my, G[q], SY[q]);
+      SH[q] += H[q];
+    }
+  }
+  if (nc > 0) {
+#pragma unroll
+    for (int q = 0; q < K3_PPT; ++q) {
+      Fx[q] = fma((double)cmx, SG[q], Fx[q]);
+      Fy[q] += SY[q];
+      Fz[q] += fma((double)(cs + M), SG[q], -SH[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < K3_PPT; ++q) {
+    if (pi[q] < n_local) {
+      double *fx = fpart + pi[q], *fy = fpart + n_local + pi[q], *fz = fpart + 2 * n_local + pi[q];
+      if (first) {
+        *fx = Fx[q];
+        *fy = Fy[q];
+        *fz = Fz[q];
+        if (ENERGY) upart[pi[q]] = U[q];
+      } else {
+        *fx += Fx[q];
+        *fy += Fy[q];
+        *fz += Fz[q];
+        if (ENERGY) upart[pi[q]] += U[q];
+      }
     }
   }
 }
@@ -1437,6 +1571,20 @@ k1_fn k1_table(int M) {
   return nullptr;
 }
 
+typedef void (*k3c_fn)(const double4 *, const double2 *, int64_t, int64_t, int, int, double *,
+                       double *);
+k3c_fn k3c_table(int M, bool energy, int buf) {
+  switch (M) {
+#define X(m)                                                                        \
+  case m:                                                                           \
+    return buf ? (energy ? k3c_force_gather<m, true, 1> : k3c_force_gather<m, false, 1>) \
+               : (energy ? k3c_force_gather<m, true, 0> : k3c_force_gather<m, false, 0>);
+    EWB_M_CASES(X)
+#undef X
+  }
+  return nullptr;
+}
+
 k3_fn k3_table(int M, bool energy) {
   switch (M) {
 #define X(m) \
@@ -1488,14 +1636,14 @@ struct Plan {
   // K3 (force gather) layout: items = z-segments of <= M k-vectors
   int M = 0, n_items = 0, n_rows = 0;
   std::vector<int> row_item_prefix;  // n_rows+1
-  DBuf item_my, item_row, rows, slot_k, slot_coeff;
+  DBuf item_my, item_row, rows, slot_k, slot_coeff, k3meta;
   // K1 (structure factor) layout: pair items = the +m_x and -m_x segments of
   // one (|m_x|, m_y, m_z-run) sharing one z recurrence
   int M1 = 0, n_pitems = 0, n_tiles = 0, ts_max = 0, pchunk = K1_PMAX;
   DBuf pitem_tab, tab_desc, tile_off, tile_ts, pslot_map;  // pslot_map: int4 (kp, km, k3p, k3m)
   std::vector<std::pair<int, DBuf>> ks_cache;  // n_ks -> row boundaries
   void release() {
-    for (DBuf *b : {&item_my, &item_row, &rows, &slot_k, &slot_coeff, &pitem_tab, &tab_desc,
+    for (DBuf *b : {&item_my, &item_row, &rows, &slot_k, &slot_coeff, &k3meta, &pitem_tab, &tab_desc,
                     &tile_off, &tile_ts, &pslot_map})
       b->release();
     for (auto &c : ks_cache) c.second.release();
@@ -1510,12 +1658,15 @@ struct ewb_handle {
   int n_sm = 148;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
+  cudaStream_t aux_stream = nullptr;  // second stream of the constant-bank gather
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev[6] = {};
   std::string err;
   int mcap = 28;   // K3 segment cap
   int mcap1 = 20;  // K1 pair segment cap
   int stencil_rad = 0;  // 0 auto, 1 force r_c cells (testing)
   int deterministic = 0;  // 1: full-shell real space, no atomics (bitwise reproducible)
+  int k3_const = 1;       // constant-bank force gather for large systems
   int64_t launches = 0;
   // system
   bool have_system = false;
@@ -1661,18 +1812,24 @@ int build_plan(ewb_handle *h, const int64_t *m, int64_t K, const double *coeff) 
     item_my[i] = items[i].my;
   }
   const int n_rows = (int)rows.size();
+  std::vector<int4> k3meta(n_items);
+  for (int i = 0; i < n_items; ++i) {
+    const bool new_row = i == 0 || item_row[i] != item_row[i - 1];
+    const bool jump = !new_row && items[i].my != items[i - 1].my + 1;
+    k3meta[i] = make_int4(items[i].mx, items[i].s, items[i].my, (new_row ? 1 : 0) | (jump ? 2 : 0));
+  }
   P.row_item_prefix.assign(n_rows + 1, 0);
   for (int r = 0; r < n_rows; ++r) P.row_item_prefix[r + 1] = P.row_item_prefix[r] + rows[r].w;
 
-  // slots (slot-major layout: slot = m * n_items + item)
+  // gather slots (item-major layout: slot = item * M + m)
   const size_t n_slots = (size_t)M * n_items;
   std::vector<int> slot_k(n_slots, -1);
   std::vector<double> slot_coeff(n_slots, 0.0);
   for (int i = 0; i < n_items; ++i)
     for (int mm = 0; mm < items[i].len; ++mm) {
       const int64_t k = idx[items[i].off + mm];
-      slot_k[(size_t)mm * n_items + i] = (int)k;
-      slot_coeff[(size_t)mm * n_items + i] = coeff ? coeff[k] : 0.0;
+      slot_k[(size_t)i * M + mm] = (int)k;  // item-major: a k-chunk is contiguous
+      slot_coeff[(size_t)i * M + mm] = coeff ? coeff[k] : 0.0;
     }
 
   // ---- K1 pair plan (own segmentation, cap mcap1) ----
@@ -1827,6 +1984,7 @@ int build_plan(ewb_handle *h, const int64_t *m, int64_t K, const double *coeff) 
   if ((rc = upload(h, P.slot_k, slot_k))) return rc;
   if ((rc = upload(h, P.slot_coeff, slot_coeff))) return rc;
   if ((rc = upload(h, P.pslot_map, pslot))) return rc;
+  if ((rc = upload(h, P.k3meta, k3meta))) return rc;
   // C*S for the gather: padding slots stay zero for the lifetime of the plan
   CK(h->sp.ensure(n_slots * sizeof(double2)));
   CK(cudaMemset(h->sp.p, 0, n_slots * sizeof(double2)));
@@ -1991,9 +2149,58 @@ int stage_recip_forces(ewb_handle *h, int64_t i0, int64_t i1, double *d_force, b
     occ = std::max(1, occ);
   }
   const int64_t ptiles = (n_local + K3_THREADS * K3_PPT - 1) / (K3_THREADS * K3_PPT);
+  const int64_t slots3 = (int64_t)h->n_sm * occ;
+  const unsigned nbc = blocks_for(n_local, RED_THREADS);
+  if (h->k3_const && ptiles >= K3C_MIN_WAVES * (int64_t)h->n_sm) {
+    // constant-bank variant: enough particles to fill the GPU without
+    // k-splits; walk the k-space in constant-bank chunks
+    const int cap = std::max(1, std::min(K3C_ITEMS, K3C_CAP / M));
+    CK(h->fpart.ensure((size_t)2 * 3 * n_local * sizeof(double)));
+    if (energy) CK(h->upart.ensure((size_t)2 * n_local * sizeof(double)));
+    const int n_chunks = (P.n_items + cap - 1) / cap;
+    cudaStream_t st[2] = {h->stream, h->aux_stream};
+    // fork the auxiliary stream off the main one (graph-capture safe)
+    CK(cudaEventRecord(h->ev_fork, h->stream));
+    CK(cudaStreamWaitEvent(h->aux_stream, h->ev_fork, 0));
+    if (n_chunks < 2) {  // the second accumulator must still be defined
+      CK(cudaMemsetAsync(h->fpart.as<double>() + 3 * n_local, 0, 3 * n_local * sizeof(double),
+                         h->aux_stream));
+      if (energy)
+        CK(cudaMemsetAsync(h->upart.as<double>() + n_local, 0, n_local * sizeof(double),
+                           h->aux_stream));
+    }
+    for (int c = 0; c < n_chunks; ++c) {
+      const int it0 = c * cap, nc = std::min(cap, P.n_items - it0), b = c & 1;
+      CK(cudaMemcpyToSymbolAsync(c_k3sp, h->sp.as<double2>() + (size_t)it0 * M,
+                                 (size_t)nc * M * sizeof(double2),
+                                 (size_t)b * K3C_CAP * sizeof(double2), cudaMemcpyDeviceToDevice,
+                                 st[b]));
+      CK(cudaMemcpyToSymbolAsync(c_k3meta, P.k3meta.as<int4>() + it0, (size_t)nc * sizeof(int4),
+                                 (size_t)b * K3C_ITEMS * sizeof(int4), cudaMemcpyDeviceToDevice,
+                                 st[b]));
+      k3c_table(M, energy, b)<<<(unsigned)ptiles, K3_THREADS, 0, st[b]>>>(
+          h->frac.as<double4>(), h->base.as<double2>(), i0, i1, nc, c < 2 ? 1 : 0,
+          h->fpart.as<double>() + (size_t)b * 3 * n_local,
+          energy ? h->upart.as<double>() + (size_t)b * n_local : nullptr);
+      CKL();
+    }
+    // join
+    CK(cudaEventRecord(h->ev_join, h->aux_stream));
+    CK(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
+    if (energy) CK(h->eblk2.ensure(nbc * sizeof(double)));
+    k3_combine<<<nbc, RED_THREADS, 0, h->stream>>>(
+        h->fpart.as<double>(), energy ? h->upart.as<double>() : nullptr, 2, i0, n_local,
+        h->frac.as<double4>(), 4.0 * M_PI / h->L, d_force,
+        energy ? h->eblk2.as<double>() : nullptr, energy ? 1 : 0);
+    CKL();
+    if (energy) {
+      k_sum<<<1, 1024, 0, h->stream>>>(h->eblk2.as<double>(), nbc, 1.0, d_u_out);
+      CKL();
+    }
+    return EWB_OK;
+  }
   // enough k-splits for K3_WAVES waves of resident blocks (short blocks
   // balance the tail), each split keeping >= 2 rows
-  const int64_t slots3 = (int64_t)h->n_sm * occ;
   int n_ks = (int)std::max<int64_t>(1, (K3_WAVES * slots3 + ptiles - 1) / ptiles);
   n_ks = std::max(1, std::min(n_ks, std::max(1, P.n_rows / 2)));
   int rc = EWB_OK;
@@ -2397,6 +2604,12 @@ int ewb_create(int device, ewb_handle **out) {
     return EWB_ECUDA;
   }
   h->stream = h->own_stream;
+  if (cudaStreamCreateWithFlags(&h->aux_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+    delete h;
+    return EWB_ECUDA;
+  }
   for (auto &ev : h->ev)
     if (cudaEventCreate(&ev) != cudaSuccess) {
       delete h;
@@ -2421,6 +2634,9 @@ void ewb_destroy(ewb_handle *h) {
     if (ge) cudaGraphExecDestroy(ge);
   for (auto &ev : h->ev)
     if (ev) cudaEventDestroy(ev);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
+  if (h->aux_stream) cudaStreamDestroy(h->aux_stream);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   delete h;
 }
@@ -2519,6 +2735,13 @@ int ewb_dev_md_kick(ewb_handle *h, double *d_vel, const double *d_force, const d
                        h->stream));
     CK(cudaStreamSynchronize(h->stream));
   }
+  return EWB_OK;
+}
+
+int ewb_set_const_gather(ewb_handle *h, int on) {
+  if (!h) return EWB_EINVAL;
+  h->k3_const = on ? 1 : 0;
+  ++h->gen;
   return EWB_OK;
 }
 

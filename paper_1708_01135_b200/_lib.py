@@ -52,6 +52,7 @@ SIGNATURES = {
     "ewb_set_deterministic": (_INT, [_P, _INT]),
     "ewb_set_graphs": (_INT, [_P, _INT]),
     "ewb_set_const_gather": (_INT, [_P, _INT]),
+    "ewb_set_tensor_cores": (_INT, [_P, _INT]),
     "ewb_set_system": (_INT, [_P, _D, _D, _D, _D]),
     "ewb_set_kspace": (_INT, [_P, _P, _I64, _P]),
     "ewb_kspace_info": (_INT, [_P, _P]),
@@ -196,6 +197,9 @@ class Handle:
 
     def set_const_gather(self, on):
         self._check(self.lib.ewb_set_const_gather(self.h, 1 if on else 0))
+
+    def set_tensor_cores(self, on):
+        self._check(self.lib.ewb_set_tensor_cores(self.h, 1 if on else 0))
 
     def set_graphs(self, on):
         self._check(self.lib.ewb_set_graphs(self.h, 1 if on else 0))

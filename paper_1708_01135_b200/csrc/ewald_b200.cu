@@ -1545,6 +1545,8 @@ __global__ void __launch_bounds__(256) k_fp64_probe(double *__restrict__ out, in
   if (s == 1.2345) out[0] = s;  // keep the chains alive
 }
 
+#include "k1_tc.cuh"
+
 // ---------------------------------------------------------------------------
 // template dispatch tables
 #define EWB_M_CASES(X)                                                                           \
@@ -1641,10 +1643,16 @@ struct Plan {
   // one (|m_x|, m_y, m_z-run) sharing one z recurrence
   int M1 = 0, n_pitems = 0, n_tiles = 0, ts_max = 0, pchunk = K1_PMAX;
   DBuf pitem_tab, tab_desc, tile_off, tile_ts, pslot_map;  // pslot_map: int4 (kp, km, k3p, k3m)
+  // tensor-core structure factor (k1_tc.cuh): M tiles of 8 (m_z, m_y-run)
+  // runs, a-chunks of <= TC_NMAX X columns, (tile, pair, a) -> pair slots
+  bool tc_ok = false;
+  int tc_A = 0, tc_mtiles = 0, tc_nchunks = 0, tc_npad_max = 0;
+  int tc_ymin = 0, tc_ny = 0, tc_zmin = 0, tc_nz = 0;
+  DBuf tc_runs, tc_map, tc_chunks;
   std::vector<std::pair<int, DBuf>> ks_cache;  // n_ks -> row boundaries
   void release() {
     for (DBuf *b : {&item_my, &item_row, &rows, &slot_k, &slot_coeff, &k3meta, &pitem_tab, &tab_desc,
-                    &tile_off, &tile_ts, &pslot_map})
+                    &tile_off, &tile_ts, &pslot_map, &tc_runs, &tc_map, &tc_chunks})
       b->release();
     for (auto &c : ks_cache) c.second.release();
     ks_cache.clear();
@@ -1667,6 +1675,9 @@ struct ewb_handle {
   int stencil_rad = 0;  // 0 auto, 1 force r_c cells (testing)
   int deterministic = 0;  // 1: full-shell real space, no atomics (bitwise reproducible)
   int k3_const = 1;       // constant-bank force gather for large systems
+  int use_tc = 1;         // structure factor on the int8 tensor cores (k1_tc.cuh)
+  DBuf tc_qmax, tc_ytab, tc_ztab, tc_xsl;
+  void *tc_spart_zeroed = nullptr;  // spart buffer whose unmapped slots were zeroed
   int64_t launches = 0;
   // system
   bool have_system = false;
@@ -1920,6 +1931,66 @@ int build_plan(ewb_handle *h, const int64_t *m, int64_t K, const double *coeff) 
       }
     }
 
+  // ---- tensor-core structure factor plan ----
+  std::vector<int4> tc_runs;
+  std::vector<int2> tc_map;
+  std::vector<TCChunk> tc_chunks;
+  int tc_A = 0, tc_ymin = 0, tc_ymax = 0, tc_zmin = 0, tc_zmax = 0, tc_mtiles = 0, tc_npad_max = 16;
+  {
+    std::map<int, std::vector<int>> by_z;  // m_z -> distinct m_y
+    tc_ymin = tc_ymax = (int)m[1];
+    tc_zmin = tc_zmax = (int)m[2];
+    for (int64_t k = 0; k < K; ++k) {
+      const int mx = (int)m[3 * k], my = (int)m[3 * k + 1], mz = (int)m[3 * k + 2];
+      tc_A = std::max(tc_A, std::abs(mx));
+      tc_ymin = std::min(tc_ymin, my);
+      tc_ymax = std::max(tc_ymax, my);
+      tc_zmin = std::min(tc_zmin, mz);
+      tc_zmax = std::max(tc_zmax, mz);
+      by_z[mz].push_back(my);
+    }
+    std::map<std::pair<int, int>, int> row_of;  // (m_y, m_z) -> tile*64 + p
+    int n_runs = 0;
+    for (auto &kv : by_z) {
+      auto &v = kv.second;
+      std::sort(v.begin(), v.end());
+      v.erase(std::unique(v.begin(), v.end()), v.end());
+      size_t i = 0;
+      while (i < v.size()) {
+        size_t e = i + 1;
+        while (e < v.size() && e - i < 8 && v[e] == v[e - 1] + 1) ++e;
+        tc_runs.push_back(make_int4(kv.first, v[i], (int)(e - i), 0));
+        for (size_t u = i; u < e; ++u)
+          row_of[std::make_pair(v[u], kv.first)] = (n_runs / 8) * 64 + (n_runs % 8) * 8 + (int)(u - i);
+        ++n_runs;
+        i = e;
+      }
+    }
+    tc_mtiles = (n_runs + 7) / 8;
+    tc_runs.resize((size_t)tc_mtiles * 8, make_int4(0, 0, 0, 0));
+    const int A1 = tc_A + 1;
+    tc_map.assign((size_t)tc_mtiles * 64 * A1, make_int2(-1, -1));
+    for (int i = 0; i < n_pitems; ++i)
+      for (int mm = 0; mm < pitems[i].len; ++mm) {
+        const int r = row_of.at(std::make_pair(pitems[i].my, pitems[i].s + mm));
+        int2 &e = tc_map[(size_t)r * A1 + pitems[i].ax];
+        const int slot = mm * n_pitems + i;
+        if (e.x < 0) e.x = slot; else e.y = slot;
+      }
+    // a-chunks: Xr columns then Xs columns, <= TC_NMAX in total
+    int a0 = 0;
+    while (a0 <= tc_A) {
+      int a1 = a0;
+      auto ncols = [&](int lo, int hi) { return (hi - lo + 1) + std::max(0, hi - std::max(lo, 1) + 1); };
+      while (a1 + 1 <= tc_A && ncols(a0, a1 + 1) <= TC_NMAX) ++a1;
+      const int nc = ncols(a0, a1);
+      const int npad = ((nc + 15) / 16) * 16;
+      tc_chunks.push_back(TCChunk{a0, a1, a1 - a0 + 1, npad});
+      tc_npad_max = std::max(tc_npad_max, npad);
+      a0 = a1 + 1;
+    }
+  }
+
   // K1 tiles and their phase-table descriptors: q e^{-i s th_z} for the
   // distinct segment starts, e^{-i m_y th_y} over the m_y range,
   // 2 e^{-i |m_x| th_x} for the distinct |m_x| (linked along x), e^{-i th_z}
@@ -1974,6 +2045,19 @@ int build_plan(ewb_handle *h, const int64_t *m, int64_t K, const double *coeff) 
   for (auto &c : P.ks_cache) c.second.release();
   P.ks_cache.clear();
   int rc;
+  P.tc_A = tc_A;
+  P.tc_mtiles = tc_mtiles;
+  P.tc_nchunks = (int)tc_chunks.size();
+  P.tc_npad_max = tc_npad_max;
+  P.tc_ymin = tc_ymin;
+  P.tc_ny = tc_ymax - tc_ymin + 1;
+  P.tc_zmin = tc_zmin;
+  P.tc_nz = tc_zmax - tc_zmin + 1;
+  if ((rc = upload(h, P.tc_runs, tc_runs))) return rc;
+  if ((rc = upload(h, P.tc_map, tc_map))) return rc;
+  if ((rc = upload(h, P.tc_chunks, tc_chunks))) return rc;
+  P.tc_ok = true;
+  h->tc_spart_zeroed = nullptr;
   if ((rc = upload(h, P.pitem_tab, ptab))) return rc;
   if ((rc = upload(h, P.item_my, item_my))) return rc;
   if ((rc = upload(h, P.item_row, item_row))) return rc;
@@ -2061,8 +2145,57 @@ int occupancy_k1(ewb_handle *h, int M, size_t smem, int *occ_out) {
 
 // S(k) over particles [i0, i1): partials over particle chunks reduced into
 // d_slots (if non-null) or left in h->spart with *n_part set.
+// Tensor-core structure factor (k1_tc.cuh): same pair-layout partials as K1.
+int stage_rho_tc(ewb_handle *h, int64_t i0, int64_t i1, int *n_part_out) {
+  Plan &P = h->plan;
+  const int64_t n = std::max<int64_t>(0, i1 - i0);
+  const size_t n_pslots = (size_t)P.M1 * P.n_pitems;
+  const int64_t np = std::max<int64_t>(TC_KB, ((n + TC_KB - 1) / TC_KB) * TC_KB);
+  const int64_t nkb = np / TC_KB;
+  const int T = P.tc_mtiles * P.tc_nchunks;
+  const int64_t kb_cap = TC_MAXP / TC_KB;
+  const int64_t ns_min = (nkb + kb_cap - 1) / kb_cap;
+  const int64_t waves = std::max<int64_t>(1, (T * ns_min + h->n_sm - 1) / h->n_sm);
+  int64_t ns = std::max<int64_t>(ns_min, (waves * h->n_sm) / std::max(1, T));
+  ns = std::min<int64_t>(ns, nkb);
+  const int64_t kbps = (nkb + ns - 1) / ns;
+  ns = (nkb + kbps - 1) / kbps;
+  const int xsl_b = tc_xsl_bytes(P.tc_npad_max);
+  CK(h->tc_qmax.ensure(sizeof(double)));
+  CK(h->tc_ytab.ensure((size_t)P.tc_ny * np * sizeof(double2)));
+  CK(h->tc_ztab.ensure((size_t)P.tc_nz * np * sizeof(double2)));
+  CK(h->tc_xsl.ensure((size_t)P.tc_nchunks * nkb * TC_S * xsl_b));
+  CK(h->spart.ensure((size_t)ns * n_pslots * sizeof(double4)));
+  if (h->tc_spart_zeroed != h->spart.p) {  // slots no k maps to stay zero
+    CK(cudaMemsetAsync(h->spart.p, 0, h->spart.cap, h->stream));
+    h->tc_spart_zeroed = h->spart.p;
+  }
+  CK(cudaMemsetAsync(h->tc_qmax.p, 0, sizeof(double), h->stream));
+  if (n > 0) {
+    k_absmax_q<<<(unsigned)std::min<int64_t>(1184, (n + 255) / 256), 256, 0, h->stream>>>(
+        h->frac.as<double4>(), i0, i1, h->tc_qmax.as<unsigned long long>());
+    CKL();
+  }
+  k1t_prep<<<(unsigned)((np / 4 + 127) / 128), 128, 0, h->stream>>>(
+      h->frac.as<double4>(), i0, std::max(i0, i1), np, h->tc_qmax.as<double>(), P.tc_ymin, P.tc_ny,
+      P.tc_zmin, P.tc_nz, P.tc_chunks.as<TCChunk>(), P.tc_nchunks, P.tc_npad_max,
+      h->tc_ytab.as<double2>(), h->tc_ztab.as<double2>(), h->tc_xsl.as<uint8_t>());
+  CKL();
+  const size_t smem = 2 * (size_t)tc_stage_bytes(P.tc_npad_max);
+  CK(cudaFuncSetAttribute(k1t_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k1t_gemm<<<dim3(P.tc_mtiles, P.tc_nchunks, (unsigned)ns), TC_THREADS, smem, h->stream>>>(
+      h->tc_ytab.as<double2>(), h->tc_ztab.as<double2>(), h->base.as<double2>(),
+      h->tc_xsl.as<uint8_t>(), P.tc_chunks.as<TCChunk>(), P.tc_runs.as<int4>(),
+      P.tc_map.as<int2>(), h->tc_qmax.as<double>(), i0, std::max(i0, i1), np, kbps * TC_KB,
+      P.tc_ymin, P.tc_zmin, P.tc_A, P.tc_npad_max, (int64_t)n_pslots, h->spart.as<double4>());
+  CKL();
+  *n_part_out = (int)ns;
+  return EWB_OK;
+}
+
 int stage_rho(ewb_handle *h, int64_t i0, int64_t i1, int *n_part_out) {
   Plan &P = h->plan;
+  if (h->use_tc && P.tc_ok) return stage_rho_tc(h, i0, i1, n_part_out);
   const int M1 = P.M1;
   const size_t smem = 2 * (size_t)P.pchunk * (P.ts_max | 1) * sizeof(double2) +
                       (size_t)P.ts_max * sizeof(int4);
@@ -2741,6 +2874,13 @@ int ewb_dev_md_kick(ewb_handle *h, double *d_vel, const double *d_force, const d
 int ewb_set_const_gather(ewb_handle *h, int on) {
   if (!h) return EWB_EINVAL;
   h->k3_const = on ? 1 : 0;
+  ++h->gen;
+  return EWB_OK;
+}
+
+int ewb_set_tensor_cores(ewb_handle *h, int on) {
+  if (!h) return EWB_EINVAL;
+  h->use_tc = on ? 1 : 0;
   ++h->gen;
   return EWB_OK;
 }

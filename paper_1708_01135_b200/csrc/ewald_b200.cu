@@ -33,6 +33,7 @@
 #include <type_traits>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <numeric>
@@ -1676,6 +1677,7 @@ struct ewb_handle {
   int deterministic = 0;  // 1: full-shell real space, no atomics (bitwise reproducible)
   int k3_const = 1;       // constant-bank force gather for large systems
   int use_tc = 1;         // structure factor on the int8 tensor cores (k1_tc.cuh)
+  int tc_dbg = 0;         // tools only (EWB_TC_DBG): 1 skip G production, 2 skip MMAs
   DBuf tc_qmax, tc_ytab, tc_ztab, tc_xsl;
   void *tc_spart_zeroed = nullptr;  // spart buffer whose unmapped slots were zeroed
   int64_t launches = 0;
@@ -2181,13 +2183,14 @@ int stage_rho_tc(ewb_handle *h, int64_t i0, int64_t i1, int *n_part_out) {
       P.tc_zmin, P.tc_nz, P.tc_chunks.as<TCChunk>(), P.tc_nchunks, P.tc_npad_max,
       h->tc_ytab.as<double2>(), h->tc_ztab.as<double2>(), h->tc_xsl.as<uint8_t>());
   CKL();
-  const size_t smem = 2 * (size_t)tc_stage_bytes(P.tc_npad_max);
+  const size_t smem = (size_t)tc_smem_bytes(P.tc_npad_max);
   CK(cudaFuncSetAttribute(k1t_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k1t_gemm<<<dim3(P.tc_mtiles, P.tc_nchunks, (unsigned)ns), TC_THREADS, smem, h->stream>>>(
+  k1t_gemm<<<dim3(P.tc_mtiles, P.tc_nchunks, (unsigned)ns), TC_NTHREADS, smem, h->stream>>>(
       h->tc_ytab.as<double2>(), h->tc_ztab.as<double2>(), h->base.as<double2>(),
       h->tc_xsl.as<uint8_t>(), P.tc_chunks.as<TCChunk>(), P.tc_runs.as<int4>(),
       P.tc_map.as<int2>(), h->tc_qmax.as<double>(), i0, std::max(i0, i1), np, kbps * TC_KB,
-      P.tc_ymin, P.tc_zmin, P.tc_A, P.tc_npad_max, (int64_t)n_pslots, h->spart.as<double4>());
+      P.tc_ymin, P.tc_zmin, P.tc_A, P.tc_npad_max, (int64_t)n_pslots, h->spart.as<double4>(),
+      h->tc_dbg);
   CKL();
   *n_part_out = (int)ns;
   return EWB_OK;
@@ -2737,6 +2740,7 @@ int ewb_create(int device, ewb_handle **out) {
     return EWB_ECUDA;
   }
   h->stream = h->own_stream;
+  if (const char *d = getenv("EWB_TC_DBG")) h->tc_dbg = atoi(d);
   if (cudaStreamCreateWithFlags(&h->aux_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) {

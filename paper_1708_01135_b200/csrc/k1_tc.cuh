@@ -49,7 +49,8 @@ constexpr int TC_MAXP = 16384;              // particles per CTA (int32 exactnes
 constexpr double TC_SC = 140185576636287.0;              // 0x7F7F7F7F7F7F
 constexpr double TC_MAGIC = 6755399441055744.0 + 141289400074368.0;  // 1.5*2^52 + 0x8080..80
 
-__host__ __device__ constexpr int tc_xsl_bytes(int npad) { return (npad / 8) * TC_SBO; }
+// one X slice (fixed stride for every chunk: compile-time MMA descriptors)
+__host__ __device__ constexpr int tc_xsl_bytes(int) { return (TC_NMAX / 8) * TC_SBO; }
 __host__ __device__ constexpr int tc_stage_bytes(int npad) {
   return TC_S * TC_GSL + TC_S * tc_xsl_bytes(npad);
 }
@@ -252,20 +253,46 @@ __global__ void __launch_bounds__(128)
   }
 }
 
-// k1t_gemm: grid (M tiles, a-chunks, particle splits); 256 threads.
+// k1t_gemm: grid (M tiles, a-chunks, particle splits); warp-specialised:
+//   warps 0-7 (256 threads): produce the G slices of a K-block (2 stages),
+//   warp 8 lane 0: issues the MMAs, warp 9 lane 0: bulk-copies the X slices
+//   (TC_XS-deep ring).  Stages hand over through mbarriers: G full (8
+//   producer-warp arrivals) / empty (tcgen05.commit), X full (complete_tx) /
+//   empty (tcgen05.commit).
 //   runs[tile*8 + g] = (m_z, m_y0, len, 0): rows 8g..8g+len-1 of the tile are
 //   the pairs (m_y0 + i, m_z); Re G in rows 0..63, Im G in rows 64..127.
 //   tmap[(tile*64 + p) * (A+1) + a] = pair slots (x, y; -1 = none) of
 //   (a, m_y, m_z) in the K1 pair layout (k2p_finalize input).
-__global__ void __launch_bounds__(TC_THREADS, 1)
+constexpr int TC_XS = 4;                      // X ring depth
+constexpr int TC_NTHREADS = TC_THREADS + 64;  // + MMA warp + loader warp
+__host__ __device__ constexpr int tc_smem_bytes(int npad_max) {
+  return 2 * TC_S * TC_GSL + TC_XS * TC_S * tc_xsl_bytes(npad_max);
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes,
+                                         uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst),
+      "l"(src), "r"(bytes), "r"(mbar)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(TC_NTHREADS, 1)
     k1t_gemm(const double2 *__restrict__ ytab, const double2 *__restrict__ ztab,
              const double2 *__restrict__ base, const uint8_t *__restrict__ xsl,
              const TCChunk *__restrict__ chunks, const int4 *__restrict__ runs,
              const int2 *__restrict__ tmap, const double *__restrict__ qmax_p, int64_t p_begin,
              int64_t p_end, int64_t np, int64_t ppb, int ymin, int zmin, int A, int npad_max,
-             int64_t n_pslots, double4 *__restrict__ spart) {
+             int64_t n_pslots, double4 *__restrict__ spart, int dbg) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t mbar[2];
+  __shared__ uint64_t g_full[2], g_empty[2], x_full[TC_XS], x_empty[TC_XS], acc_full;
   __shared__ uint32_t tmem_base_s;
   __shared__ int4 s_runs[8];
   const int tile = blockIdx.x, ch = blockIdx.y, split = blockIdx.z;
@@ -273,7 +300,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const TCChunk C = chunks[ch];
   const int npad = C.npad;
   const int xsl_b = tc_xsl_bytes(npad_max);
-  const int stage_b = TC_S * TC_GSL + TC_S * xsl_b;
+  const int xblk = TC_S * xsl_b;  // bytes of one K-block's X slices
+  uint8_t *gbuf = smem;
+  uint8_t *xbuf = smem + 2 * TC_S * TC_GSL;
   const int64_t n_kb_all = np / TC_KB;
   const int64_t kb0 = (int64_t)split * (ppb / TC_KB);
   const int64_t kb1 = min(n_kb_all, kb0 + ppb / TC_KB);
@@ -281,8 +310,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   if (threadIdx.x < 8) s_runs[threadIdx.x] = runs[tile * 8 + threadIdx.x];
   if (threadIdx.x == 0) {
-    mbar_init(smem_u32(&mbar[0]), 1);
-    mbar_init(smem_u32(&mbar[1]), 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(&g_full[i]), TC_THREADS / 32);
+      mbar_init(smem_u32(&g_empty[i]), 1);
+    }
+    for (int i = 0; i < TC_XS; ++i) {
+      mbar_init(smem_u32(&x_full[i]), 1);
+      mbar_init(smem_u32(&x_empty[i]), 1);
+    }
+    mbar_init(smem_u32(&acc_full), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -296,97 +332,124 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = tmem_base_s;
 
-  // producer role: core column c (16 particles), row half h, run g, quad qd
-  const int pc = warp & 3, ph = warp >> 2, g = lane >> 2, qd = lane & 3;
-  const int4 run = s_runs[g];
-  const int kin = pc * 16 + qd * 4;  // particle offset in the K-block
-  const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(npad >> 3) << 17) |
-                         (8u << 24);
-
-  for (int it = 0; it < nkb; ++it) {
-    const int st = it & 1;
-    uint8_t *sb = smem + st * stage_b;
-    if (it >= 2) mbar_wait(smem_u32(&mbar[st]), ((it - 2) >> 1) & 1);
-    const int64_t kb = kb0 + it;
-    // X slices: contiguous copy of the pre-split block
-    {
-      const uint8_t *src = xsl + ((int64_t)ch * n_kb_all + kb) * (int64_t)(TC_S * xsl_b);
-      const uint32_t dst = smem_u32(sb + TC_S * TC_GSL);
-      const int nbytes = TC_S * xsl_b;
-      for (int o = threadIdx.x * 16; o < nbytes; o += TC_THREADS * 16) cp_async16(dst + o, src + o);
+  if (warp == 9) {
+    // ---- X loader ----
+    if (lane == 0) {
+      for (int it = 0; it < nkb; ++it) {
+        const int xs = it % TC_XS;
+        if (it >= TC_XS) mbar_wait(smem_u32(&x_empty[xs]), ((it / TC_XS) - 1) & 1);
+        const uint8_t *src = xsl + ((int64_t)ch * n_kb_all + kb0 + it) * (int64_t)xblk;
+        const uint32_t fb = smem_u32(&x_full[xs]);
+        mbar_expect_tx(fb, (uint32_t)xblk);
+        bulk_g2s(smem_u32(xbuf + xs * xblk), src, (uint32_t)xblk, fb);
+      }
     }
-    // G slices: rows (8g + 4ph + i) and +64, particles kin..kin+3
-    {
-      const int64_t j = kb * TC_KB + kin;  // relative to p_begin
-      double2 cur[4], e1[4];
-      const int myl = run.y + 4 * ph;
-      const bool active = 4 * ph < run.z;  // rows of this half exist in the run
+  } else if (warp == 8) {
+    // ---- MMA issuer ----
+    if (lane == 0) {
+      const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) |
+                             ((uint32_t)(npad >> 3) << 17) | (8u << 24);
+      for (int it = 0; it < nkb; ++it) {
+        const int gs = it & 1, xs = it % TC_XS;
+        mbar_wait(smem_u32(&g_full[gs]), (it >> 1) & 1);
+        mbar_wait(smem_u32(&x_full[xs]), (it / TC_XS) & 1);
+        tc_fence_after();
+        if (!(dbg & 2)) {
+          const uint64_t gd = tc_desc(smem_u32(gbuf + gs * TC_S * TC_GSL));
+          const uint64_t xd = tc_desc(smem_u32(xbuf + xs * xblk));
+          const uint32_t acc0 = it > 0 ? 1u : 0u;
+          constexpr int XSL = tc_xsl_bytes(0);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (active) {
-          const double2 yv = ytab[(int64_t)(myl - ymin) * np + j + u];
-          const double2 zv = ztab[(int64_t)(run.x - zmin) * np + j + u];
-          cur[u] = cmul(yv, zv);
-          e1[u] = base[3 * min(p_begin + j + u, p_end - 1) + 1];
+          for (int l = 0; l < TC_NL; ++l) {
+            constexpr int dummy = 0;
+            (void)dummy;
+            const int w = TC_W0 + l;
+            const int s_lo = w - (TC_S - 1) > 0 ? w - (TC_S - 1) : 0;
+#pragma unroll
+            for (int s = 0; s < TC_S; ++s) {
+              const int t = w - s;
+              if (t < 0 || t >= TC_S) continue;
+#pragma unroll
+              for (int ks = 0; ks < TC_KB / 32; ++ks)
+                tc_mma(tmem + (uint32_t)(l * npad), gd + (uint64_t)((s * TC_GSL + ks * 256) >> 4),
+                       xd + (uint64_t)((t * XSL + ks * 256) >> 4), idesc,
+                       (s > s_lo || ks > 0) ? 1u : acc0);
+            }
+          }
+          tc_commit(smem_u32(&g_empty[gs]));
+          tc_commit(smem_u32(&x_empty[xs]));
         } else {
-          cur[u] = e1[u] = make_double2(0.0, 0.0);
+          mbar_arrive(smem_u32(&g_empty[gs]));
+          mbar_arrive(smem_u32(&x_empty[xs]));
         }
       }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int r = 4 * ph + i;
-        const bool valid = r < run.z;
-        uint2 br[4], bi[4];
+      if (!(dbg & 2) && nkb > 0)
+        tc_commit(smem_u32(&acc_full));
+      else
+        mbar_arrive(smem_u32(&acc_full));
+    }
+  } else {
+    // ---- G producers: core column pc (16 particles), row half ph, run g, quad qd ----
+    const int pc = warp & 3, ph = warp >> 2, g = lane >> 2, qd = lane & 3;
+    const int4 run = s_runs[g];
+    const int kin = pc * 16 + qd * 4;  // particle offset in the K-block
+    const int myl = run.y + 4 * ph;
+    const bool active = 4 * ph < run.z;  // rows of this half exist in the run
+    for (int it = 0; it < nkb; ++it) {
+      const int gs = it & 1;
+      uint8_t *sb = gbuf + gs * TC_S * TC_GSL;
+      if (it >= 2) mbar_wait(smem_u32(&g_empty[gs]), ((it >> 1) - 1) & 1);
+      if (!(dbg & 1)) {
+        const int64_t j = (kb0 + it) * TC_KB + kin;  // relative to p_begin
+        double2 cur[4], e1[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          br[u] = tc_bits(valid ? cur[u].x : 0.0);
-          bi[u] = tc_bits(valid ? cur[u].y : 0.0);
-          if (i < 3) cur[u] = cmul(cur[u], e1[u]);
-        }
-        uint32_t w[TC_S];
-        const int row = 8 * g + r;
-        tc_digits4(br[0], br[1], br[2], br[3], w);
-        const int off = tc_off(row, kin);
-#pragma unroll
-        for (int s = 0; s < TC_S; ++s) *reinterpret_cast<uint32_t *>(sb + s * TC_GSL + off) = w[s];
-        tc_digits4(bi[0], bi[1], bi[2], bi[3], w);
-        const int offi = tc_off(row + 64, kin);
-#pragma unroll
-        for (int s = 0; s < TC_S; ++s) *reinterpret_cast<uint32_t *>(sb + s * TC_GSL + offi) = w[s];
-      }
-    }
-    cp_async_wait_all();
-    fence_async_smem();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      tc_fence_after();
-      const uint32_t gb = smem_u32(sb), xb = smem_u32(sb + TC_S * TC_GSL);
-#pragma unroll 1
-      for (int l = 0; l < TC_NL; ++l) {
-        const int w = TC_W0 + l;
-        for (int s = max(0, w - (TC_S - 1)); s <= min(TC_S - 1, w); ++s) {
-          const int t = w - s;
-#pragma unroll
-          for (int ks = 0; ks < TC_KB / 32; ++ks) {
-            const uint32_t acc = (it > 0 || s > max(0, w - (TC_S - 1)) || ks > 0) ? 1u : 0u;
-            tc_mma(tmem + (uint32_t)(l * npad), tc_desc(gb + s * TC_GSL + ks * 256),
-                   tc_desc(xb + t * xsl_b + ks * 256), idesc, acc);
+          if (active) {
+            const double2 yv = ytab[(int64_t)(myl - ymin) * np + j + u];
+            const double2 zv = ztab[(int64_t)(run.x - zmin) * np + j + u];
+            cur[u] = cmul(yv, zv);
+            e1[u] = base[3 * min(p_begin + j + u, p_end - 1) + 1];
+          } else {
+            cur[u] = e1[u] = make_double2(0.0, 0.0);
           }
         }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = 4 * ph + i;
+          const bool valid = r < run.z;
+          uint2 br[4], bi[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            br[u] = tc_bits(valid ? cur[u].x : 0.0);
+            bi[u] = tc_bits(valid ? cur[u].y : 0.0);
+            if (i < 3) cur[u] = cmul(cur[u], e1[u]);
+          }
+          uint32_t w[TC_S];
+          const int row = 8 * g + r;
+          tc_digits4(br[0], br[1], br[2], br[3], w);
+          const int off = tc_off(row, kin);
+#pragma unroll
+          for (int s = 0; s < TC_S; ++s) *reinterpret_cast<uint32_t *>(sb + s * TC_GSL + off) = w[s];
+          tc_digits4(bi[0], bi[1], bi[2], bi[3], w);
+          const int offi = tc_off(row + 64, kin);
+#pragma unroll
+          for (int s = 0; s < TC_S; ++s)
+            *reinterpret_cast<uint32_t *>(sb + s * TC_GSL + offi) = w[s];
+        }
       }
-      tc_commit(smem_u32(&mbar[st]));
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&g_full[gs]));
     }
-    __syncwarp();
   }
 
-  // epilogue: combine the levels, exchange Re/Im rows through shared memory
+  // ---- epilogue: combine the levels, exchange Re/Im rows through smem ----
   double *E = reinterpret_cast<double *>(smem);
   const int ES = npad + 1;
-  if (nkb > 0) {
-    const int last = nkb - 1;
-    mbar_wait(smem_u32(&mbar[last & 1]), (last >> 1) & 1);
-    if (nkb >= 2) mbar_wait(smem_u32(&mbar[(last - 1) & 1]), ((last - 1) >> 1) & 1);
-    tc_fence_after();
+  mbar_wait(smem_u32(&acc_full), 0);
+  tc_fence_after();
+  __syncthreads();  // every producer/loader is done with the stage buffers
+  if (warp < 8 && nkb > 0) {
     const double scale = 2.0 * (*qmax_p) / (TC_SC * TC_SC);  // x2: pair layout A = 2 P
     const int row = 32 * (warp & 3) + lane;
     const int half = npad / 2;
@@ -417,7 +480,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   // write the pair-layout partials (2P1, 2P3, 2P4, 2P2) of every mapped slot
   const int na = C.a1 - C.a0 + 1;
   const int sa0 = max(C.a0, 1);
-  for (int item = threadIdx.x; item < 64 * na; item += TC_THREADS) {
+  for (int item = threadIdx.x; item < 64 * na; item += TC_NTHREADS) {
     const int p = item / na, a = C.a0 + item % na;
     const int2 sl = tmap[((int64_t)tile * 64 + p) * (A + 1) + a];
     if (sl.x < 0 && sl.y < 0) continue;

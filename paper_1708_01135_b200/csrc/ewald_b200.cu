@@ -32,6 +32,7 @@
 #include <tuple>
 #include <type_traits>
 #include <cmath>
+#include <climits>
 #include <cstdint>
 #include <cstdlib>
 #include <cstdio>
@@ -1547,6 +1548,7 @@ __global__ void __launch_bounds__(256) k_fp64_probe(double *__restrict__ out, in
 }
 
 #include "k1_tc.cuh"
+#include "k3_tc.cuh"
 
 // ---------------------------------------------------------------------------
 // template dispatch tables
@@ -1650,10 +1652,15 @@ struct Plan {
   int tc_A = 0, tc_mtiles = 0, tc_nchunks = 0, tc_npad_max = 0;
   int tc_ymin = 0, tc_ny = 0, tc_zmin = 0, tc_nz = 0;
   DBuf tc_runs, tc_map, tc_chunks;
+  // tensor-core force gather (k3_tc.cuh): A rows (a, type), K pairs, slot map
+  bool t3_ok = false;
+  int t3_rows = 0, t3_mtiles = 0, t3_npairs = 0, t3_nkb = 0;
+  DBuf t3_rowtab, t3_pair_yz, t3_slotmap;
   std::vector<std::pair<int, DBuf>> ks_cache;  // n_ks -> row boundaries
   void release() {
     for (DBuf *b : {&item_my, &item_row, &rows, &slot_k, &slot_coeff, &k3meta, &pitem_tab, &tab_desc,
-                    &tile_off, &tile_ts, &pslot_map, &tc_runs, &tc_map, &tc_chunks})
+                    &tile_off, &tile_ts, &pslot_map, &tc_runs, &tc_map, &tc_chunks, &t3_rowtab,
+                    &t3_pair_yz, &t3_slotmap})
       b->release();
     for (auto &c : ks_cache) c.second.release();
     ks_cache.clear();
@@ -1679,6 +1686,7 @@ struct ewb_handle {
   int use_tc = 1;         // structure factor on the int8 tensor cores (k1_tc.cuh)
   int tc_dbg = 0;         // tools only (EWB_TC_DBG): 1 skip G production, 2 skip MMAs
   DBuf tc_qmax, tc_ytab, tc_ztab, tc_xsl;
+  DBuf t3_wsl, t3_rscale;
   void *tc_spart_zeroed = nullptr;  // spart buffer whose unmapped slots were zeroed
   int64_t launches = 0;
   // system
@@ -1993,6 +2001,31 @@ int build_plan(ewb_handle *h, const int64_t *m, int64_t K, const double *coeff) 
     }
   }
 
+  // ---- tensor-core force-gather plan ----
+  std::vector<T3Row> t3_rows;
+  std::vector<int2> t3_pair_yz;
+  std::vector<int> t3_slotmap;
+  {
+    for (int t = 1; t <= tc_A; ++t)
+      for (int ty = 0; ty < 6; ++ty) t3_rows.push_back(T3Row{t, ty});
+    t3_rows.push_back(T3Row{0, 2});
+    t3_rows.push_back(T3Row{0, 4});
+    const int n_runs_all = (int)tc_runs.size();
+    const int npp = ((n_runs_all * 8 + 31) / 32) * 32;
+    t3_pair_yz.assign(npp, make_int2(INT_MIN, INT_MIN));
+    for (int r = 0; r < n_runs_all; ++r)
+      for (int i = 0; i < tc_runs[r].z; ++i)
+        t3_pair_yz[r * 8 + i] = make_int2(tc_runs[r].y + i, tc_runs[r].x);
+    std::map<std::pair<int, int>, int> p_of;
+    for (int p = 0; p < npp; ++p)
+      if (t3_pair_yz[p].x != INT_MIN) p_of[std::make_pair(t3_pair_yz[p].x, t3_pair_yz[p].y)] = p;
+    t3_slotmap.assign((size_t)(2 * tc_A + 1) * npp, -1);
+    for (int64_t k = 0; k < K; ++k) {
+      const int p = p_of.at(std::make_pair((int)m[3 * k + 1], (int)m[3 * k + 2]));
+      t3_slotmap[(size_t)(m[3 * k] + tc_A) * npp + p] = k3slot[k];
+    }
+  }
+
   // K1 tiles and their phase-table descriptors: q e^{-i s th_z} for the
   // distinct segment starts, e^{-i m_y th_y} over the m_y range,
   // 2 e^{-i |m_x| th_x} for the distinct |m_x| (linked along x), e^{-i th_z}
@@ -2059,6 +2092,14 @@ int build_plan(ewb_handle *h, const int64_t *m, int64_t K, const double *coeff) 
   if ((rc = upload(h, P.tc_map, tc_map))) return rc;
   if ((rc = upload(h, P.tc_chunks, tc_chunks))) return rc;
   P.tc_ok = true;
+  P.t3_rows = (int)t3_rows.size();
+  P.t3_mtiles = (P.t3_rows + 127) / 128;
+  P.t3_npairs = (int)t3_pair_yz.size();
+  P.t3_nkb = 2 * P.t3_npairs / TC_KB;
+  if ((rc = upload(h, P.t3_rowtab, t3_rows))) return rc;
+  if ((rc = upload(h, P.t3_pair_yz, t3_pair_yz))) return rc;
+  if ((rc = upload(h, P.t3_slotmap, t3_slotmap))) return rc;
+  P.t3_ok = true;
   h->tc_spart_zeroed = nullptr;
   if ((rc = upload(h, P.pitem_tab, ptab))) return rc;
   if ((rc = upload(h, P.item_my, item_my))) return rc;
@@ -2269,6 +2310,52 @@ int stage_finalize_pairs(ewb_handle *h, const double4 *src, int n_part, double *
   return EWB_OK;
 }
 
+// Tensor-core force gather (k3_tc.cuh); forces only (the per-particle
+// energy of the foreign-rho API stays on the FP64 gather).
+int stage_recip_tc(ewb_handle *h, int64_t i0, int64_t i1, double *d_force) {
+  Plan &P = h->plan;
+  const int64_t n_local = i1 - i0;
+  const int nkb = P.t3_nkb;
+  CK(h->t3_wsl.ensure((size_t)P.t3_mtiles * nkb * TC_S * TC_GSL));
+  CK(h->t3_rscale.ensure((size_t)P.t3_mtiles * 128 * sizeof(double)));
+  k3t_wprep<<<P.t3_mtiles * 128, 256, 0, h->stream>>>(
+      h->sp.as<double2>(), P.t3_slotmap.as<int>(), P.tc_A, P.t3_pair_yz.as<int2>(), P.t3_npairs,
+      P.t3_rowtab.as<T3Row>(), P.t3_rows, nkb, h->t3_rscale.as<double>(), h->t3_wsl.as<uint8_t>());
+  CKL();
+  const int64_t ptiles = (n_local + T3_NP - 1) / T3_NP;
+  const int64_t T = ptiles * P.t3_mtiles;
+  const int kb_cap = T3_KMAX / TC_KB;
+  const int ns_min = std::max(1, (nkb + kb_cap - 1) / kb_cap);
+  // splits: least (waves x per-CTA work), at least 4 K-blocks per CTA
+  int ns = ns_min;
+  double best = 1e300;
+  for (int c = ns_min; c <= ns_min + 3 && (c == ns_min || nkb / c >= 4); ++c) {
+    const double waves = (double)((T * c + h->n_sm - 1) / h->n_sm);
+    const double cost = waves * ((nkb + c - 1) / c) + 0.02 * c * nkb;
+    if (cost < best) {
+      best = cost;
+      ns = c;
+    }
+  }
+  const int kbps = (nkb + ns - 1) / ns;
+  ns = (nkb + kbps - 1) / kbps;
+  const int n_ks = ns * P.t3_mtiles;
+  CK(h->fpart.ensure((size_t)n_ks * 3 * n_local * sizeof(double)));
+  const size_t smem = (size_t)t3_smem_bytes();
+  CK(cudaFuncSetAttribute(k3t_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k3t_gemm<<<dim3((unsigned)ptiles, P.t3_mtiles, ns), TC_NTHREADS, smem, h->stream>>>(
+      h->frac.as<double4>(), h->base.as<double2>(), h->t3_wsl.as<uint8_t>(),
+      h->t3_rscale.as<double>(), P.t3_rowtab.as<T3Row>(), P.t3_rows, P.t3_pair_yz.as<int2>(), nkb,
+      kbps, i0, i1, h->fpart.as<double>(), h->tc_dbg);
+  CKL();
+  const unsigned nbc = blocks_for(n_local, RED_THREADS);
+  k3_combine<<<nbc, RED_THREADS, 0, h->stream>>>(h->fpart.as<double>(), nullptr, n_ks, i0, n_local,
+                                                  h->frac.as<double4>(), 4.0 * M_PI / h->L,
+                                                  d_force, nullptr, 0);
+  CKL();
+  return EWB_OK;
+}
+
 int stage_recip_forces(ewb_handle *h, int64_t i0, int64_t i1, double *d_force, bool energy,
                        double *d_u_out) {
   Plan &P = h->plan;
@@ -2277,6 +2364,7 @@ int stage_recip_forces(ewb_handle *h, int64_t i0, int64_t i1, double *d_force, b
     if (energy) CK(cudaMemsetAsync(d_u_out, 0, sizeof(double), h->stream));
     return EWB_OK;
   }
+  if (!energy && h->use_tc && P.t3_ok) return stage_recip_tc(h, i0, i1, d_force);
   const int M = P.M;
   k3_fn fn = k3_table(M, energy);
   int &occ = h->occ_k3[M][energy ? 1 : 0];

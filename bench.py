@@ -15,9 +15,13 @@ r_c=6, cube |n_i|<=18 (25,326 half-space k-vectors).
 * e2e: the same metric through the reference-facing API
   (EwaldSolver.evaluate on a ParticleSet whose arrays live in pinned host
   memory), host<->device copies inside the timed region.
-* roofline: FP64-bound; the kernel with the largest share of the step is
-  reported against the FP64 DFMA peak measured on this device by
-  ewb_probe_fp64_peak (MEASURED_PEAKS.json has no FP64 figure).
+* roofline: the stage with the largest share of the step.  S(k) and the
+  reciprocal forces run on the int8 tensor cores (k1t_gemm, k3t_gemm):
+  executed MMA ops against the int8 peak measured by ewb_probe_i8_peak;
+  real space (k6) is FP64-bound: in-cutoff pairs x 64 flops against the
+  FP64 DFMA peak measured by ewb_probe_fp64_peak (MEASURED_PEAKS.json has
+  neither figure).  The SURVEY 8(d) FP64-equivalent of the reciprocal work
+  (22 flops per particle.k pair) is reported beside it.
 * cpu_baseline: the oracle (C restatement of the reference, OpenMP over all
   host cores) on one full evaluation of the same config, rank 0 at N=1.
 
@@ -47,6 +51,12 @@ FLOPS_K3 = 9.0
 # FP64 pipe instructions per pair (K1 3, K3 5)
 INSTR_K1 = 3.0
 INSTR_K3 = 5.0
+# SURVEY.md 8(d) convention for the reciprocal work: 22 FP64 flops per pair
+FLOPS_SURVEY = 22.0
+# one real-space pair evaluation (k6 pair_eval + accumulation): 6 adds (dx),
+# 5 (r^2), rsqrt refinement 7, exp 18, erfc 16, energy/force scalars 6,
+# two force updates 6 -> 64 FP64 operations
+FLOPS_PAIR_RS = 64.0
 
 
 def parse():
@@ -271,6 +281,7 @@ def run_ours(args):
     h.set_system(cfg["L"], params.alpha, params.r_cutoff)
     h.set_kspace(rs.m_int, rs.coeff)
     fp64_peak = h.probe_fp64_peak()
+    i8_peak = h.probe_i8_peak()
 
     pos_d = torch.from_numpy(cfg["pos"]).to(dev)
     q_d = torch.from_numpy(cfg["q"]).to(dev)
@@ -369,38 +380,57 @@ def run_ours(args):
     pairs = float(n) * K
     if world == 1 and args.steps > 0:
         mean = stage / args.steps
-        t_real = mean[1]
-        t_k1 = mean[2]
-        t_k3 = mean[3]
-        cands = {"k6_real_space": t_real, "k1_structure_factor": t_k1,
-                 "k3_force_gather": t_k3}
-        dom = max(cands, key=cands.get)
-        if dom == "k6_real_space":
-            # report the reciprocal pair throughput too; real space roofline
-            # uses the same FP64 denominator with pair-evaluation flops
-            pass
-        k_flops = {"k1_structure_factor": FLOPS_K1 * pairs,
-                   "k3_force_gather": FLOPS_K3 * pairs}
-        k_instr = {"k1_structure_factor": INSTR_K1 * pairs,
-                   "k3_force_gather": INSTR_K3 * pairs}
-        recip_dom = max(("k1_structure_factor", "k3_force_gather"),
-                        key=lambda k: cands[k])
-        ach = k_flops[recip_dom] / cands[recip_dom] / 1e12
-        sm_peak_instr = fp64_peak / 2.0  # DFMA: 2 flops per pipe slot
+        t_real, t_k1, t_k3 = mean[1], mean[2], mean[3]
+        tci = h.tc_info()
+        rs_pairs = h.last_pair_count()  # unordered in-cutoff pairs (half shell)
+        np64 = ((n + 63) // 64) * 64
+        # executed int8 tensor ops (2 per MAC) of the two GEMM kernels
+        ops_k1 = 2.0 * tci["pairs_per_kstep"] * 128 * tci["k1_npad_sum"] * np64 * tci["k1_mtiles"]
+        ops_k3 = 2.0 * tci["pairs_per_kstep"] * 128 * tci["k3_K"] * np64 * tci["k3_mtiles"]
+        fp64_equiv = pairs * FLOPS_SURVEY / (t_k1 + t_k3) / 1e12
+        kern = {
+            "k1t_gemm": {
+                "stage_ms": 1e3 * t_k1, "bound": "tensor", "unit": "TOP/s (int8)",
+                "achieved": ops_k1 / t_k1 / 1e12, "peak": i8_peak,
+                "frac": ops_k1 / t_k1 / 1e12 / i8_peak,
+                "ops_per_launch": ops_k1,
+                "note": "S(k): executed int8 MMA ops (26 slice pairs x 2 per MAC) over the "
+                        "alg1 stage time (k_absmax_q + k1t_prep + k1t_gemm + k2p_finalize)"},
+            "k3t_gemm": {
+                "stage_ms": 1e3 * t_k3, "bound": "tensor", "unit": "TOP/s (int8)",
+                "achieved": ops_k3 / t_k3 / 1e12, "peak": i8_peak,
+                "frac": ops_k3 / t_k3 / 1e12 / i8_peak,
+                "ops_per_launch": ops_k3,
+                "note": "forces: executed int8 MMA ops over the alg2 stage time "
+                        "(k3t_wprep + k3t_gemm + k3_combine)"},
+            "k6_real_space": {
+                "stage_ms": 1e3 * t_real, "bound": "fp64", "unit": "TFLOP/s",
+                "pairs": rs_pairs,
+                "achieved": rs_pairs * FLOPS_PAIR_RS / t_real / 1e12, "peak": fp64_peak,
+                "frac": rs_pairs * FLOPS_PAIR_RS / t_real / 1e12 / fp64_peak,
+                "pair_evals_per_s": rs_pairs / t_real,
+                "note": f"in-cutoff pairs x {FLOPS_PAIR_RS:.0f} FP64 flops per pair evaluation "
+                        "(erfc+exp+rsqrt, both forces); stage t_sr incl. binning"},
+        }
+        dom = max(kern, key=lambda k: kern[k]["stage_ms"])
+        d = kern[dom]
         roof = {
-            "bound": "fp64", "kernel": recip_dom,
-            "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
-            "frac": ach / fp64_peak,
-            "fp64_pipe_frac": k_instr[recip_dom] / cands[recip_dom] / 1e12 / sm_peak_instr,
-            "peak_source": "measured (ewb_probe_fp64_peak, DFMA chains, this run)",
-            "traffic": None,
-            "step_share": {k: v / float(mean[1] + mean[2] + mean[3]) for k, v in cands.items()},
-            "dominant_kernel_of_step": dom,
-            "stage_ms": {"t_cell": 1e3 * mean[0], "t_sr": 1e3 * mean[1],
-                         "t_alg1": 1e3 * mean[2], "t_alg2": 1e3 * mean[3]},
-            "pairs_per_s": pairs / (mean[2] + mean[3]),
-            "flops_per_pair": {"k1": FLOPS_K1, "k3": FLOPS_K3,
-                               "survey_convention": 22.0},
+            "bound": d["bound"], "kernel": dom, "achieved": d["achieved"], "peak": d["peak"],
+            "unit": d["unit"], "frac": d["frac"], "traffic": None,
+            "peak_source": ("measured int8 tcgen05.mma probe (ewb_probe_i8_peak, M128 N256 K32, "
+                            "this run)" if d["bound"] == "tensor" else
+                            "measured FP64 DFMA probe (ewb_probe_fp64_peak, this run)"),
+            "kernels": kern,
+            "step_share": {k: v["stage_ms"] / (1e3 * float(t_real + t_k1 + t_k3))
+                           for k, v in kern.items()},
+            "reciprocal_fp64_equivalent": {
+                "pairs_per_s": pairs / (t_k1 + t_k3),
+                "achieved_tflops": fp64_equiv, "fp64_peak": fp64_peak,
+                "frac": fp64_equiv / fp64_peak,
+                "convention": "SURVEY 8(d): 22 FP64 flops per particle.k pair; > 1 means the "
+                              "reciprocal work runs beyond the FP64 roofline (tensor cores)"},
+            "stage_ms": {"t_cell": 1e3 * mean[0], "t_sr": 1e3 * t_real,
+                         "t_alg1": 1e3 * t_k1, "t_alg2": 1e3 * t_k3},
         }
 
     cpu = None
@@ -430,6 +460,7 @@ def run_ours(args):
             "gpu_launches": int(launches), "clocks": clocks,
             "energies": [float(x) for x in en],
             "fp64_peak_tflops_measured": fp64_peak,
+            "i8_peak_tops_measured": i8_peak,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -167,6 +167,18 @@ int ewb_dev_md_kick(ewb_handle *h, double *d_vel, const double *d_force, const d
 /* Sustained FP64 DFMA throughput of this device (TFLOP/s), measured with
  * independent fma chains; the FP64 roofline denominator. */
 int ewb_probe_fp64_peak(ewb_handle *h, double *tflops);
+/* Roofline denominator of the tensor-core kernels: dense int8 tcgen05.mma
+ * (M=128, N=256, K=32, shared-memory operands) issued back to back on every
+ * SM; *tops = measured int8 TOP/s. */
+int ewb_probe_i8_peak(ewb_handle *h, double *tops);
+/* Tensor-core plan of the current k-table (for MMA-work accounting):
+ * info8 = {enabled, S(k) M tiles, sum of padded X columns, force M tiles,
+ *          force GEMM K, levels, slice-pair MMAs per K step, max |m_x|}. */
+int ewb_tc_info(const ewb_handle *h, int64_t *info8);
+/* Pairs inside the traversal cutoff visited by the last real-space pass
+ * (unordered pairs in the default half-shell mode, ordered pairs in the
+ * deterministic full-shell mode); synchronises the handle's stream. */
+int ewb_last_pair_count(ewb_handle *h, int64_t *pairs);
 /* Kernels launched by this handle since creation (evidence counter). */
 int64_t ewb_launch_count(const ewb_handle *h);
 

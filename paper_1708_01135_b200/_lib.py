@@ -75,6 +75,9 @@ SIGNATURES = {
     "ewb_dev_md_kick_drift": (_INT, [_P, _P, _P, _P, _P, _I64, _D]),
     "ewb_dev_md_kick": (_INT, [_P, _P, _P, _P, _I64, _D, _INT, _P]),
     "ewb_probe_fp64_peak": (_INT, [_P, _P]),
+    "ewb_probe_i8_peak": (_INT, [_P, _P]),
+    "ewb_tc_info": (_INT, [_P, _P]),
+    "ewb_last_pair_count": (_INT, [_P, _P]),
     "ewb_launch_count": (_I64, [_P]),
 }
 
@@ -248,6 +251,22 @@ class Handle:
     def probe_fp64_peak(self):
         out = ctypes.c_double(0.0)
         self._check(self.lib.ewb_probe_fp64_peak(self.h, ctypes.byref(out)))
+        return out.value
+
+    def probe_i8_peak(self):
+        out = ctypes.c_double(0.0)
+        self._check(self.lib.ewb_probe_i8_peak(self.h, ctypes.byref(out)))
+        return out.value
+
+    def tc_info(self):
+        info = np.zeros(8, dtype=np.int64)
+        self._check(self.lib.ewb_tc_info(self.h, _ptr(info)))
+        return dict(zip(("enabled", "k1_mtiles", "k1_npad_sum", "k3_mtiles", "k3_K",
+                         "levels", "pairs_per_kstep", "A"), info.tolist()))
+
+    def last_pair_count(self):
+        out = ctypes.c_int64(0)
+        self._check(self.lib.ewb_last_pair_count(self.h, ctypes.byref(out)))
         return out.value
 
     def launch_count(self):

@@ -1023,7 +1023,7 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
                   const int *__restrict__ order, const int *__restrict__ cell_start,
                   const int *__restrict__ row_ustart, RSParams P, double *__restrict__ force,
                   double *__restrict__ eblk, double *__restrict__ eblk_lj,
-                  int *__restrict__ err) {
+                  int *__restrict__ err, unsigned long long *__restrict__ pair_count) {
   // A warp owns K6_G consecutive particles (centres) of one row of cells
   // (fixed cy, cz).  Lanes stream the candidates of the stencil rows --
   // contiguous runs of cells along x, so each 32-wide step is dense -- test
@@ -1068,6 +1068,7 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
     for (int g = 0; g < K6_G; ++g) s_f[warp][g][lane] = make_double3(0.0, 0.0, 0.0);
     __syncwarp();
     int cnt = 0;  // pending pairs (warp-uniform)
+    int accepted = 0;  // pairs inside the traversal cutoff (warp-uniform)
     bool coincident = false;
 
     // Each accepted pair stores, per axis, which image the reference's fold
@@ -1252,6 +1253,7 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
               s_list[warp][cnt + __popc(bal & lt_mask)] = make_uint2((uint32_t)j, t);
             }
             cnt += __popc(bal);
+            accepted += __popc(bal);
           }
         }
 #endif
@@ -1322,6 +1324,7 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
     __syncwarp();
     if (cnt > 0) round(0, cnt);
     if (coincident) atomicOr(err, ERR_COINCIDENT);
+    if (lane == 0 && pair_count) atomicAdd(pair_count, (unsigned long long)accepted);
     __syncwarp();
     for (int g = 0; g < gi; ++g) {
       const double3 f = s_f[warp][g][lane];
@@ -1652,6 +1655,7 @@ struct Plan {
   int tc_A = 0, tc_mtiles = 0, tc_nchunks = 0, tc_npad_max = 0;
   int tc_ymin = 0, tc_ny = 0, tc_zmin = 0, tc_nz = 0;
   DBuf tc_runs, tc_map, tc_chunks;
+  std::vector<TCChunk> tc_chunks_host;
   // tensor-core force gather (k3_tc.cuh): A rows (a, type), K pairs, slot map
   bool t3_ok = false;
   int t3_rows = 0, t3_mtiles = 0, t3_npairs = 0, t3_nkb = 0;
@@ -1687,6 +1691,7 @@ struct ewb_handle {
   int tc_dbg = 0;         // tools only (EWB_TC_DBG): 1 skip G production, 2 skip MMAs
   DBuf tc_qmax, tc_ytab, tc_ztab, tc_xsl;
   DBuf t3_wsl, t3_rscale;
+  DBuf pairc;  // in-cutoff pairs visited by the last real-space pass
   void *tc_spart_zeroed = nullptr;  // spart buffer whose unmapped slots were zeroed
   int64_t launches = 0;
   // system
@@ -2092,6 +2097,7 @@ int build_plan(ewb_handle *h, const int64_t *m, int64_t K, const double *coeff) 
   if ((rc = upload(h, P.tc_map, tc_map))) return rc;
   if ((rc = upload(h, P.tc_chunks, tc_chunks))) return rc;
   P.tc_ok = true;
+  P.tc_chunks_host = tc_chunks;
   P.t3_rows = (int)t3_rows.size();
   P.t3_mtiles = (P.t3_rows + 127) / 128;
   P.t3_npairs = (int)t3_pair_yz.size();
@@ -2604,16 +2610,18 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
     if (lj_on && d_ulj_out) CK(cudaMemsetAsync(d_ulj_out, 0, sizeof(double), h->stream));
     return EWB_OK;
   }
+  CK(h->pairc.ensure(sizeof(unsigned long long)));
+  if (part == 0) CK(cudaMemsetAsync(h->pairc.p, 0, sizeof(unsigned long long), h->stream));
   if (lj_on)
     k6_real_space<true><<<nb, K6_WARPS * 32, 0, h->stream>>>(
         h->sorted.as<double4>(), h->sorted_cell.as<int>(), h->order.as<int>(), h->start.as<int>(),
         h->row_ustart.as<int>(), rp, d_force, h->eblk.as<double>(), h->eblk_lj.as<double>(),
-        h->errflag.as<int>());
+        h->errflag.as<int>(), h->pairc.as<unsigned long long>());
   else
     k6_real_space<false><<<nb, K6_WARPS * 32, 0, h->stream>>>(
         h->sorted.as<double4>(), h->sorted_cell.as<int>(), h->order.as<int>(), h->start.as<int>(),
         h->row_ustart.as<int>(), rp, d_force, h->eblk.as<double>(), nullptr,
-        h->errflag.as<int>());
+        h->errflag.as<int>(), h->pairc.as<unsigned long long>());
   CKL();
   if (pair_coul) {
     k_sum<<<1, 1024, 0, h->stream>>>(h->eblk.as<double>(), nb, 1.0, d_u_out);
@@ -3278,6 +3286,59 @@ int ewb_probe_fp64_peak(ewb_handle *h, double *tflops) {
   CK(cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]));
   const double flops = 2.0 * 8.0 * iters * 256.0 * blocks * reps;
   *tflops = flops / (ms * 1e-3) / 1e12;
+  return EWB_OK;
+}
+
+int ewb_probe_i8_peak(ewb_handle *h, double *tops) {
+  if (!h || !tops) return EWB_EINVAL;
+  CK(cudaSetDevice(h->device));
+  CK(h->eblk2.ensure(64));
+  const int iters = 16384;
+  const unsigned blocks = (unsigned)h->n_sm;
+  const size_t smem = (size_t)(16 + 32) * TC_SBO;
+  CK(cudaFuncSetAttribute(k_i8_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_i8_probe<<<blocks, 128, smem, h->stream>>>(iters, h->eblk2.as<int>());
+  CKL();
+  CK(cudaEventRecord(h->ev[0], h->stream));
+  const int reps = 3;
+  for (int r = 0; r < reps; ++r) {
+    k_i8_probe<<<blocks, 128, smem, h->stream>>>(iters, h->eblk2.as<int>());
+    CKL();
+  }
+  CK(cudaEventRecord(h->ev[1], h->stream));
+  CK(cudaEventSynchronize(h->ev[1]));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]));
+  const double ops = 2.0 * 128.0 * 256.0 * 32.0 * iters * blocks * reps;
+  *tops = ops / (ms * 1e-3) / 1e12;
+  return EWB_OK;
+}
+
+int ewb_tc_info(const ewb_handle *h, int64_t *info8) {
+  if (!h || !info8) return EWB_EINVAL;
+  if (!h->have_kspace) return EWB_ESTATE;
+  const Plan &P = h->plan;
+  int64_t npad_sum = 0;
+  for (const auto &c : P.tc_chunks_host) npad_sum += c.npad;
+  info8[0] = P.tc_ok && h->use_tc ? 1 : 0;
+  info8[1] = P.tc_mtiles;
+  info8[2] = npad_sum;         // sum of padded X columns over the a-chunks
+  info8[3] = P.t3_mtiles;
+  info8[4] = 2 * P.t3_npairs;  // K of the force GEMM
+  info8[5] = TC_NL;            // levels
+  info8[6] = 26;               // slice-pair MMAs per K step
+  info8[7] = P.tc_A;
+  return EWB_OK;
+}
+
+int ewb_last_pair_count(ewb_handle *h, int64_t *pairs) {
+  if (!h || !pairs) return EWB_EINVAL;
+  *pairs = 0;
+  if (!h->pairc.p) return EWB_OK;
+  unsigned long long v = 0;
+  CK(cudaStreamSynchronize(h->stream));
+  CK(cudaMemcpy(&v, h->pairc.p, sizeof(v), cudaMemcpyDeviceToHost));
+  *pairs = (int64_t)v;
   return EWB_OK;
 }
 

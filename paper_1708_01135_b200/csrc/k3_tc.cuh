@@ -308,3 +308,50 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
     fpart[(size_t)ks_index * 3 * n_local + (size_t)c * n_local + i] = s;
   }
 }
+
+// k_i8_probe: the roofline denominator for the tensor-core kernels.  One CTA
+// per SM issues `iters` back-to-back int8 MMAs (M=128, N=256, K=32, both
+// operands in shared memory, the same no-swizzle K-major layout as the
+// kernels above) into TMEM and waits for them.
+__global__ void __launch_bounds__(128, 1) k_i8_probe(int iters, int *__restrict__ sink) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t done;
+  __shared__ uint32_t tmem_base_s;
+  for (int i = threadIdx.x; i < (16 + 32) * TC_SBO / 4; i += blockDim.x)
+    reinterpret_cast<uint32_t *>(smem)[i] = 0x01010101u * (uint32_t)(i & 3);
+  if (threadIdx.x == 0) {
+    mbar_init(smem_u32(&done), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if ((threadIdx.x >> 5) == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+                     smem_u32(&tmem_base_s))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_s;
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) | (8u << 24);
+    const uint64_t ad = tc_desc(smem_u32(smem)), bd = tc_desc(smem_u32(smem + 16 * TC_SBO));
+    for (int i = 0; i < iters; ++i) tc_mma(tmem, ad + (uint64_t)((i & 1) * 16), bd, idesc, i > 0 ? 1u : 0u);
+    tc_commit(smem_u32(&done));
+  }
+  mbar_wait(smem_u32(&done), 0);
+  tc_fence_after();
+  if ((threadIdx.x >> 5) == 0) {
+    int r[8];
+    tc_ld8(tmem + ((uint32_t)(32 * 0) << 16), r);
+    tc_wait_ld();
+    if (r[0] == 123456789) sink[0] = r[1];
+  }
+  tc_fence_before();
+  __syncthreads();
+  if ((threadIdx.x >> 5) == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+  }
+}

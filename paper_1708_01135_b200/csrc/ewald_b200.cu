@@ -890,11 +890,14 @@ __global__ void k_iota(int *__restrict__ v, int64_t n) {
 
 __global__ void k5_gather(const int *__restrict__ order, const double4 *__restrict__ xyzq,
                           const int *__restrict__ cell_of, int64_t n,
-                          double4 *__restrict__ sorted, int *__restrict__ sorted_cell) {
+                          double4 *__restrict__ sorted, float4 *__restrict__ sorted_f,
+                          int *__restrict__ sorted_cell) {
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= n) return;
   const int o = order[p];
-  sorted[p] = xyzq[o];
+  const double4 v = xyzq[o];
+  sorted[p] = v;
+  sorted_f[p] = make_float4((float)v.x, (float)v.y, (float)v.z, 0.0f);
   sorted_cell[p] = cell_of[o];
 }
 
@@ -984,6 +987,7 @@ struct RSParams {
   int coul;            // screened Coulomb on pairs with r2 < rc2c
   double rc2c;         // Coulomb cutoff^2 (rc2 = traversal cutoff^2 = max)
   double rc2lj, lj_s2, lj_4e, lj_shift, lj_24e;  // shifted 12-6 LJ (potentials.py:21-45)
+  float rc2f;  // FP32 candidate prefilter bound (>= rc2 plus the rounding margin)
 };
 
 // dx exactly as the reference: fl(xi - xj) then one fold by +-L
@@ -1019,7 +1023,8 @@ constexpr int K6_LIST = 32 * K6_G + 32;  // pending pairs per warp
 #endif
 template <bool LJ>
 __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
-    k6_real_space(const double4 *__restrict__ sorted, const int *__restrict__ sorted_cell,
+    k6_real_space(const double4 *__restrict__ sorted, const float4 *__restrict__ sorted_f,
+                  const int *__restrict__ sorted_cell,
                   const int *__restrict__ order, const int *__restrict__ cell_start,
                   const int *__restrict__ row_ustart, RSParams P, double *__restrict__ force,
                   double *__restrict__ eblk, double *__restrict__ eblk_lj,
@@ -1033,6 +1038,7 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
   // are evaluated in a converged round (lane l: pair l) and accumulated into
   // the lane's slot of F_g in shared memory; slots are summed at the end.
   __shared__ double4 s_i[K6_WARPS][K6_G];
+  __shared__ float4 s_cf[K6_WARPS][K6_G];  // centres + the piece's image shift, FP32
   __shared__ uint2 s_list[K6_WARPS][K6_LIST];
   __shared__ double3 s_f[K6_WARPS][K6_G][32];
   __shared__ double sh[K6_WARPS];
@@ -1174,6 +1180,38 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
         k = d >= P.hl ? 0u : (d < -P.hl ? 2u : 1u);
         return k == 1u ? d : (k == 0u ? __dsub_rn(d, P.L) : __dadd_rn(d, P.L));
       };
+      if constexpr (!FX && !FYZ) {
+        // FP32 prefilter: a conservative superset of the reference's
+        // predicate (rc2f includes the rounding bound); the exact FP64 r^2 <
+        // r_c^2 decides inside pair_eval, so results are unchanged
+        __syncwarp();
+        if (lane < gi) {
+          const double4 pi = s_i[warp][lane];
+          s_cf[warp][lane] = make_float4((float)(pi.x + sx), (float)(pi.y + sy),
+                                         (float)(pi.z + sz), 0.0f);
+        }
+        __syncwarp();
+        for (int j0 = jb; j0 < je; j0 += 32) {
+          const int j = j0 + lane;
+          const bool vj = j < je;
+          const float4 pj = sorted_f[vj ? j : jb];
+#pragma unroll
+          for (int g = 0; g < K6_G; ++g) {
+            if (g < gi) {
+              const float4 c = s_cf[warp][g];
+              const float dx = c.x - pj.x, dy = c.y - pj.y, dz = c.z - pj.z;
+              const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+              const bool acc = vj && (r2 < P.rc2f) && (after ? j > first + g : j != first + g);
+              const unsigned bal = __ballot_sync(0xffffffffu, acc);
+              if (acc) s_list[warp][cnt + __popc(bal & lt_mask)] = make_uint2((uint32_t)j, tag | (uint32_t)g);
+              cnt += __popc(bal);
+              accepted += __popc(bal);
+            }
+          }
+          if (cnt >= 32) drain();
+        }
+        return;
+      }
       for (int j0 = jb; j0 < je; j0 += 32) {
         const int j = j0 + lane;
         const bool vj = j < je;
@@ -1711,6 +1749,7 @@ struct ewb_handle {
   DBuf frac, base, xyzq;                     // derived
   DBuf spart, sslot, sp, fpart, upart, eblk, eblk2, eblk_lj, energy, errflag;
   DBuf cell_of, slot, count, start, gstart, order_tmp, order, sorted, sorted_cell, row_ustart;
+  DBuf sorted_f;  // FP32 copy of the sorted positions (candidate prefilter)
   // CUDA graph of the device pipeline (prep + real space + S(k) + forces +
   // self energy), captured on the second call with an unchanged key
   struct GKey {
@@ -2532,6 +2571,7 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
   CK(h->order_tmp.ensure(n * sizeof(int)));
   CK(h->order.ensure(n * sizeof(int)));
   CK(h->sorted.ensure(n * sizeof(double4)));
+  CK(h->sorted_f.ensure(n * sizeof(float4)));
   CK(cudaMemsetAsync(h->count.p, 0, (n_cells + 1) * sizeof(int), h->stream));
   k4_bin_count<<<blocks_for(n, 256), 256, 0, h->stream>>>(h->xyzq.as<double4>(), n, edge, cpd_eff,
                                                           h->cell_of.as<int>(), h->slot.as<int>(),
@@ -2556,6 +2596,7 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
   k5_gather<<<blocks_for(n, 256), 256, 0, h->stream>>>(h->order.as<int>(), h->xyzq.as<double4>(),
                                                        h->cell_of.as<int>(), n,
                                                        h->sorted.as<double4>(),
+                                                       h->sorted_f.as<float4>(),
                                                        h->sorted_cell.as<int>());
   CKL();
   // units: K6_G consecutive particles of one row of cells (fixed cy, cz)
@@ -2579,6 +2620,14 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
   rp.lj_4e = h->lj_4e;
   rp.lj_shift = h->lj_shift;
   rp.lj_24e = h->lj_24e;
+  {
+    // |error of the FP32 r^2| <= 2^-24 (14 L r_c + 3 r_c^2) for |x| < L,
+    // |shift| <= L (positions, shifted centres, differences and the FMA
+    // chain rounded once each); doubled and rounded up
+    const double rc_t = std::sqrt(rc2_t);
+    const double margin = std::ldexp(2.0 * (16.0 * h->L * rc_t + 8.0 * rc2_t), -24);
+    rp.rc2f = std::nextafter((float)(rc2_t + margin), INFINITY);
+  }
   rp.sa = std::sqrt(h->alpha);
   rp.al = h->alpha;
   rp.tsap = 2.0 * std::sqrt(h->alpha / M_PI);
@@ -2614,12 +2663,12 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
   if (part == 0) CK(cudaMemsetAsync(h->pairc.p, 0, sizeof(unsigned long long), h->stream));
   if (lj_on)
     k6_real_space<true><<<nb, K6_WARPS * 32, 0, h->stream>>>(
-        h->sorted.as<double4>(), h->sorted_cell.as<int>(), h->order.as<int>(), h->start.as<int>(),
+        h->sorted.as<double4>(), h->sorted_f.as<float4>(), h->sorted_cell.as<int>(), h->order.as<int>(), h->start.as<int>(),
         h->row_ustart.as<int>(), rp, d_force, h->eblk.as<double>(), h->eblk_lj.as<double>(),
         h->errflag.as<int>(), h->pairc.as<unsigned long long>());
   else
     k6_real_space<false><<<nb, K6_WARPS * 32, 0, h->stream>>>(
-        h->sorted.as<double4>(), h->sorted_cell.as<int>(), h->order.as<int>(), h->start.as<int>(),
+        h->sorted.as<double4>(), h->sorted_f.as<float4>(), h->sorted_cell.as<int>(), h->order.as<int>(), h->start.as<int>(),
         h->row_ustart.as<int>(), rp, d_force, h->eblk.as<double>(), nullptr,
         h->errflag.as<int>(), h->pairc.as<unsigned long long>());
   CKL();
@@ -2860,7 +2909,9 @@ void ewb_destroy(ewb_handle *h) {
                   &h->sslot, &h->sp, &h->fpart, &h->upart, &h->eblk, &h->eblk2, &h->eblk_lj,
                   &h->energy,
                   &h->errflag, &h->cell_of, &h->slot, &h->count, &h->start, &h->gstart,
-                  &h->order_tmp, &h->order, &h->sorted, &h->sorted_cell, &h->row_ustart})
+                  &h->order_tmp, &h->order, &h->sorted, &h->sorted_cell, &h->row_ustart,
+                  &h->sorted_f, &h->tc_qmax, &h->tc_ytab, &h->tc_ztab, &h->tc_xsl, &h->t3_wsl,
+                  &h->t3_rscale, &h->pairc})
     b->release();
   h->plan.release();
   for (auto &ge : h->gexec)

@@ -385,8 +385,8 @@ def run_ours(args):
         rs_pairs = h.last_pair_count()  # unordered in-cutoff pairs (half shell)
         np64 = ((n + 63) // 64) * 64
         # executed int8 tensor ops (2 per MAC) of the two GEMM kernels
-        ops_k1 = 2.0 * tci["pairs_per_kstep"] * 128 * tci["k1_npad_sum"] * np64 * tci["k1_mtiles"]
-        ops_k3 = 2.0 * tci["pairs_per_kstep"] * 128 * tci["k3_K"] * np64 * tci["k3_mtiles"]
+        ops_k1 = 2.0 * tci["k1_pairs_per_kstep"] * 128 * tci["k1_npad_sum"] * np64 * tci["k1_mtiles"]
+        ops_k3 = 2.0 * tci["k3_pairs_per_kstep"] * 128 * tci["k3_K"] * np64 * tci["k3_mtiles"]
         fp64_equiv = pairs * FLOPS_SURVEY / (t_k1 + t_k3) / 1e12
         kern = {
             "k1t_gemm": {
@@ -394,14 +394,14 @@ def run_ours(args):
                 "achieved": ops_k1 / t_k1 / 1e12, "peak": i8_peak,
                 "frac": ops_k1 / t_k1 / 1e12 / i8_peak,
                 "ops_per_launch": ops_k1,
-                "note": "S(k): executed int8 MMA ops (26 slice pairs x 2 per MAC) over the "
+                "note": "S(k): executed int8 MMA ops (26 slice pairs of six 8-bit slices, 2 per MAC) over the "
                         "alg1 stage time (k_absmax_q + k1t_prep + k1t_gemm + k2p_finalize)"},
             "k3t_gemm": {
                 "stage_ms": 1e3 * t_k3, "bound": "tensor", "unit": "TOP/s (int8)",
                 "achieved": ops_k3 / t_k3 / 1e12, "peak": i8_peak,
                 "frac": ops_k3 / t_k3 / 1e12 / i8_peak,
                 "ops_per_launch": ops_k3,
-                "note": "forces: executed int8 MMA ops over the alg2 stage time "
+                "note": "forces: executed int8 MMA ops (15 slice pairs of five slices) over the alg2 stage time "
                         "(k3t_wprep + k3t_gemm + k3_combine)"},
             "k6_real_space": {
                 "stage_ms": 1e3 * t_real, "bound": "fp64", "unit": "TFLOP/s",

@@ -76,6 +76,7 @@ SIGNATURES = {
     "ewb_dev_md_kick": (_INT, [_P, _P, _P, _P, _I64, _D, _INT, _P]),
     "ewb_probe_fp64_peak": (_INT, [_P, _P]),
     "ewb_probe_i8_peak": (_INT, [_P, _P]),
+    "ewb_probe_i8_shape": (_INT, [_P, _INT, _P]),
     "ewb_tc_info": (_INT, [_P, _P]),
     "ewb_last_pair_count": (_INT, [_P, _P]),
     "ewb_launch_count": (_I64, [_P]),
@@ -258,11 +259,16 @@ class Handle:
         self._check(self.lib.ewb_probe_i8_peak(self.h, ctypes.byref(out)))
         return out.value
 
+    def probe_i8_shape(self, n_mma):
+        out = ctypes.c_double(0.0)
+        self._check(self.lib.ewb_probe_i8_shape(self.h, int(n_mma), ctypes.byref(out)))
+        return out.value
+
     def tc_info(self):
         info = np.zeros(8, dtype=np.int64)
         self._check(self.lib.ewb_tc_info(self.h, _ptr(info)))
         return dict(zip(("enabled", "k1_mtiles", "k1_npad_sum", "k3_mtiles", "k3_K",
-                         "levels", "pairs_per_kstep", "A"), info.tolist()))
+                         "k3_pairs_per_kstep", "k1_pairs_per_kstep", "A"), info.tolist()))
 
     def last_pair_count(self):
         out = ctypes.c_int64(0)

@@ -1697,12 +1697,12 @@ struct Plan {
   // tensor-core force gather (k3_tc.cuh): A rows (a, type), K pairs, slot map
   bool t3_ok = false;
   int t3_rows = 0, t3_mtiles = 0, t3_npairs = 0, t3_nkb = 0;
-  DBuf t3_rowtab, t3_pair_yz, t3_slotmap;
+  DBuf t3_rowtab, t3_pair_yz, t3_slotmap, t3_comp;
   std::vector<std::pair<int, DBuf>> ks_cache;  // n_ks -> row boundaries
   void release() {
     for (DBuf *b : {&item_my, &item_row, &rows, &slot_k, &slot_coeff, &k3meta, &pitem_tab, &tab_desc,
                     &tile_off, &tile_ts, &pslot_map, &tc_runs, &tc_map, &tc_chunks, &t3_rowtab,
-                    &t3_pair_yz, &t3_slotmap})
+                    &t3_pair_yz, &t3_slotmap, &t3_comp})
       b->release();
     for (auto &c : ks_cache) c.second.release();
     ks_cache.clear();
@@ -2047,13 +2047,29 @@ int build_plan(ewb_handle *h, const int64_t *m, int64_t K, const double *coeff) 
 
   // ---- tensor-core force-gather plan ----
   std::vector<T3Row> t3_rows;
+  std::vector<int4> t3_comp;
   std::vector<int2> t3_pair_yz;
   std::vector<int> t3_slotmap;
   {
-    for (int t = 1; t <= tc_A; ++t)
-      for (int ty = 0; ty < 6; ++ty) t3_rows.push_back(T3Row{t, ty});
-    t3_rows.push_back(T3Row{0, 2});
-    t3_rows.push_back(T3Row{0, 4});
+    // rows ordered by force component (x: types 0,1; y: 2,3 and a=0; z: 4,5
+    // and a=0) so that each component is a contiguous row range per M tile
+    for (int c = 0; c < 3; ++c) {
+      if (c > 0) t3_rows.push_back(T3Row{0, 2 * c});
+      for (int t = 1; t <= tc_A; ++t)
+        for (int ty = 2 * c; ty < 2 * c + 2; ++ty) t3_rows.push_back(T3Row{t, ty});
+    }
+    const int n_t3 = (int)t3_rows.size();
+    for (int mt = 0; mt < (n_t3 + 127) / 128; ++mt) {
+      int4 cr = make_int4(0, 0, 0, 0);
+      int *ends[3] = {&cr.x, &cr.y, &cr.z};
+      for (int c = 0; c < 3; ++c) {
+        int e = 0;
+        for (int r = 0; r < 128 && mt * 128 + r < n_t3; ++r)
+          if ((t3_rows[mt * 128 + r].type >> 1) <= c) e = r + 1;
+        *ends[c] = e;
+      }
+      t3_comp.push_back(cr);
+    }
     const int n_runs_all = (int)tc_runs.size();
     const int npp = ((n_runs_all * 8 + 31) / 32) * 32;
     t3_pair_yz.assign(npp, make_int2(INT_MIN, INT_MIN));
@@ -2142,9 +2158,12 @@ int build_plan(ewb_handle *h, const int64_t *m, int64_t K, const double *coeff) 
   P.t3_npairs = (int)t3_pair_yz.size();
   P.t3_nkb = 2 * P.t3_npairs / TC_KB;
   if ((rc = upload(h, P.t3_rowtab, t3_rows))) return rc;
+  if ((rc = upload(h, P.t3_comp, t3_comp))) return rc;
   if ((rc = upload(h, P.t3_pair_yz, t3_pair_yz))) return rc;
   if ((rc = upload(h, P.t3_slotmap, t3_slotmap))) return rc;
-  P.t3_ok = true;
+  // the epilogue's shared X table must fit next to the level sums
+  P.t3_ok = 128 * (T3_NP + 1) * (int)sizeof(double) + T3_NP * (tc_A + 1) * (int)sizeof(double2) <=
+            t3_smem_bytes();
   h->tc_spart_zeroed = nullptr;
   if ((rc = upload(h, P.pitem_tab, ptab))) return rc;
   if ((rc = upload(h, P.item_my, item_my))) return rc;
@@ -2264,7 +2283,9 @@ int stage_rho_tc(ewb_handle *h, int64_t i0, int64_t i1, int *n_part_out) {
         h->frac.as<double4>(), i0, i1, h->tc_qmax.as<unsigned long long>());
     CKL();
   }
-  k1t_prep<<<(unsigned)((np / 4 + 127) / 128), 128, 0, h->stream>>>(
+  k1t_prep<<<dim3((unsigned)((np + 127) / 128),
+                  (P.tc_ny + 7) / 8 + (P.tc_nz + 7) / 8 + P.tc_nchunks * ((P.tc_npad_max + 7) / 8)),
+             128, 0, h->stream>>>(
       h->frac.as<double4>(), i0, std::max(i0, i1), np, h->tc_qmax.as<double>(), P.tc_ymin, P.tc_ny,
       P.tc_zmin, P.tc_nz, P.tc_chunks.as<TCChunk>(), P.tc_nchunks, P.tc_npad_max,
       h->tc_ytab.as<double2>(), h->tc_ztab.as<double2>(), h->tc_xsl.as<uint8_t>());
@@ -2361,12 +2382,20 @@ int stage_recip_tc(ewb_handle *h, int64_t i0, int64_t i1, double *d_force) {
   Plan &P = h->plan;
   const int64_t n_local = i1 - i0;
   const int nkb = P.t3_nkb;
-  CK(h->t3_wsl.ensure((size_t)P.t3_mtiles * nkb * TC_S * TC_GSL));
+  CK(h->t3_wsl.ensure((size_t)P.t3_mtiles * nkb * T3_S * TC_GSL));
   CK(h->t3_rscale.ensure((size_t)P.t3_mtiles * 128 * sizeof(double)));
-  k3t_wprep<<<P.t3_mtiles * 128, 256, 0, h->stream>>>(
-      h->sp.as<double2>(), P.t3_slotmap.as<int>(), P.tc_A, P.t3_pair_yz.as<int2>(), P.t3_npairs,
-      P.t3_rowtab.as<T3Row>(), P.t3_rows, nkb, h->t3_rscale.as<double>(), h->t3_wsl.as<uint8_t>());
-  CKL();
+  {
+    const unsigned kparts = (unsigned)std::max(1, std::min(16, (2 * P.t3_npairs + 1023) / 1024));
+    CK(cudaMemsetAsync(h->t3_rscale.p, 0, (size_t)P.t3_mtiles * 128 * sizeof(double), h->stream));
+    k3t_wmax<<<dim3(P.t3_rows, kparts), 256, 0, h->stream>>>(
+        h->sp.as<double2>(), P.t3_slotmap.as<int>(), P.tc_A, P.t3_pair_yz.as<int2>(), P.t3_npairs,
+        P.t3_rowtab.as<T3Row>(), P.t3_rows, h->t3_rscale.as<unsigned long long>());
+    CKL();
+    k3t_wprep<<<dim3(P.t3_mtiles * 128, kparts), 256, 0, h->stream>>>(
+        h->sp.as<double2>(), P.t3_slotmap.as<int>(), P.tc_A, P.t3_pair_yz.as<int2>(), P.t3_npairs,
+        P.t3_rowtab.as<T3Row>(), P.t3_rows, nkb, h->t3_rscale.as<double>(), h->t3_wsl.as<uint8_t>());
+    CKL();
+  }
   const int64_t ptiles = (n_local + T3_NP - 1) / T3_NP;
   const int64_t T = ptiles * P.t3_mtiles;
   const int kb_cap = T3_KMAX / TC_KB;
@@ -2388,11 +2417,30 @@ int stage_recip_tc(ewb_handle *h, int64_t i0, int64_t i1, double *d_force) {
   CK(h->fpart.ensure((size_t)n_ks * 3 * n_local * sizeof(double)));
   const size_t smem = (size_t)t3_smem_bytes();
   CK(cudaFuncSetAttribute(k3t_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k3t_gemm<<<dim3((unsigned)ptiles, P.t3_mtiles, ns), TC_NTHREADS, smem, h->stream>>>(
-      h->frac.as<double4>(), h->base.as<double2>(), h->t3_wsl.as<uint8_t>(),
-      h->t3_rscale.as<double>(), P.t3_rowtab.as<T3Row>(), P.t3_rows, P.t3_pair_yz.as<int2>(), nkb,
-      kbps, i0, i1, h->fpart.as<double>(), h->tc_dbg);
-  CKL();
+  {
+    // clusters of T3_CL particle tiles share the A loads (padding tiles
+    // carry no particles)
+    const int64_t ptiles_pad = ((ptiles + T3_CL - 1) / T3_CL) * T3_CL;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)ptiles_pad, P.t3_mtiles, ns);
+    lc.blockDim = dim3(TC_NTHREADS);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = h->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = T3_CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&lc, k3t_gemm, (const double4 *)h->frac.as<double4>(),
+                          (const double2 *)h->base.as<double2>(), (const uint8_t *)h->t3_wsl.as<uint8_t>(),
+                          (const double *)h->t3_rscale.as<double>(),
+                          (const T3Row *)P.t3_rowtab.as<T3Row>(), P.t3_rows,
+                          (const int2 *)P.t3_pair_yz.as<int2>(), nkb, kbps, i0, i1, P.tc_A,
+                          (const int4 *)P.t3_comp.as<int4>(), h->fpart.as<double>(), h->tc_dbg));
+    ++h->launches;
+  }
   const unsigned nbc = blocks_for(n_local, RED_THREADS);
   k3_combine<<<nbc, RED_THREADS, 0, h->stream>>>(h->fpart.as<double>(), nullptr, n_ks, i0, n_local,
                                                   h->frac.as<double4>(), 4.0 * M_PI / h->L,
@@ -3340,30 +3388,32 @@ int ewb_probe_fp64_peak(ewb_handle *h, double *tflops) {
   return EWB_OK;
 }
 
-int ewb_probe_i8_peak(ewb_handle *h, double *tops) {
-  if (!h || !tops) return EWB_EINVAL;
+int ewb_probe_i8_shape(ewb_handle *h, int n_mma, double *tops) {
+  if (!h || !tops || n_mma < 16 || n_mma > 256 || n_mma % 16) return EWB_EINVAL;
   CK(cudaSetDevice(h->device));
   CK(h->eblk2.ensure(64));
   const int iters = 16384;
   const unsigned blocks = (unsigned)h->n_sm;
   const size_t smem = (size_t)(16 + 32) * TC_SBO;
   CK(cudaFuncSetAttribute(k_i8_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_i8_probe<<<blocks, 128, smem, h->stream>>>(iters, h->eblk2.as<int>());
+  k_i8_probe<<<blocks, 128, smem, h->stream>>>(iters, n_mma, h->eblk2.as<int>());
   CKL();
   CK(cudaEventRecord(h->ev[0], h->stream));
   const int reps = 3;
   for (int r = 0; r < reps; ++r) {
-    k_i8_probe<<<blocks, 128, smem, h->stream>>>(iters, h->eblk2.as<int>());
+    k_i8_probe<<<blocks, 128, smem, h->stream>>>(iters, n_mma, h->eblk2.as<int>());
     CKL();
   }
   CK(cudaEventRecord(h->ev[1], h->stream));
   CK(cudaEventSynchronize(h->ev[1]));
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]));
-  const double ops = 2.0 * 128.0 * 256.0 * 32.0 * iters * blocks * reps;
+  const double ops = 2.0 * 128.0 * n_mma * 32.0 * iters * blocks * reps;
   *tops = ops / (ms * 1e-3) / 1e12;
   return EWB_OK;
 }
+
+int ewb_probe_i8_peak(ewb_handle *h, double *tops) { return ewb_probe_i8_shape(h, 256, tops); }
 
 int ewb_tc_info(const ewb_handle *h, int64_t *info8) {
   if (!h || !info8) return EWB_EINVAL;
@@ -3376,8 +3426,8 @@ int ewb_tc_info(const ewb_handle *h, int64_t *info8) {
   info8[2] = npad_sum;         // sum of padded X columns over the a-chunks
   info8[3] = P.t3_mtiles;
   info8[4] = 2 * P.t3_npairs;  // K of the force GEMM
-  info8[5] = TC_NL;            // levels
-  info8[6] = 26;               // slice-pair MMAs per K step
+  info8[5] = T3_PAIRS;         // slice-pair MMAs per K step of the force GEMM
+  info8[6] = 26;               // slice-pair MMAs per K step of the S(k) GEMM
   info8[7] = P.tc_A;
   return EWB_OK;
 }

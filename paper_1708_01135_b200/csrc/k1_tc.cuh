@@ -119,6 +119,14 @@ __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
 }
+// one lane of a converged warp (PTX elect.sync)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
 __device__ __forceinline__ void tc_commit(uint32_t mbar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    mbar)
@@ -149,107 +157,95 @@ struct TCChunk {
 //   ytab[(my - ymin) * np + j]  = e^{-i 2pi my f_y}
 //   ztab[(mz - zmin) * np + j]  = (q_j / qmax) e^{-i 2pi mz f_z}
 //   xsl: per (chunk, K-block) the six X slices in the shared-memory image
-// One thread per particle quad (tables: per particle; X: 4 particles packed
-// per 32-bit word).  Phases by recurrence with a fresh sincospi every 8 steps.
+// grid (particles / 128, tasks): task < nyt: 8 m_y values per particle,
+// then 8 m_z values, then one a-chunk of X slices per particle quad.  Each
+// run of 8 starts with a sincospi and continues by recurrence.
 __global__ void __launch_bounds__(128)
     k1t_prep(const double4 *__restrict__ frac, int64_t p_begin, int64_t p_end, int64_t np,
              const double *__restrict__ qmax_p, int ymin, int ny, int zmin, int nz,
              const TCChunk *__restrict__ chunks, int n_chunks, int npad_max,
              double2 *__restrict__ ytab, double2 *__restrict__ ztab, uint8_t *__restrict__ xsl) {
-  const int64_t quad = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t j0 = 4 * quad;
-  if (j0 >= np) return;
-  const double inv_qmax = 1.0 / fmax(*qmax_p, 1e-300);
-  double fx[4], fy[4], fz[4], qs[4];
+  const int task = blockIdx.y;
+  const int nyt = (ny + 7) / 8, nzt = (nz + 7) / 8;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (task < nyt + nzt) {
+    const int64_t j = t;
+    if (j >= np) return;
+    const bool ok = p_begin + j < p_end;
+    const double4 f = ok ? frac[p_begin + j] : make_double4(0.0, 0.0, 0.0, 0.0);
+    const bool is_y = task < nyt;
+    const int t0 = 8 * (is_y ? task : task - nyt);
+    const int m0 = (is_y ? ymin : zmin) + t0, cnt = min(8, (is_y ? ny : nz) - t0);
+    const double fr = is_y ? f.y : f.z;
+    const double sc = is_y ? 1.0 : (ok ? f.w / fmax(*qmax_p, 1e-300) : 0.0);
+    double s, c;
+    sincospi(2.0 * fr, &s, &c);
+    const double2 e1 = make_double2(c, -s);
+    sincospi(2.0 * ((double)m0 * fr), &s, &c);
+    double2 cur = make_double2(c, -s);
+    double2 *dst = (is_y ? ytab : ztab) + (int64_t)t0 * np + j;
+    for (int u = 0; u < cnt; ++u) {
+      dst[(int64_t)u * np] = make_double2(sc * cur.x, sc * cur.y);
+      cur = cmul(cur, e1);
+    }
+    return;
+  }
+  // X slices: column c of chunk ch: Xr(a0 + c) for c < nr, Xs(max(a0,1) + c - nr),
+  // zero above; one task per (chunk, 8 consecutive columns)
+  const int xt = task - nyt - nzt;
+  const int segs = (npad_max + 7) / 8;
+  const int ch = xt / segs, c0 = 8 * (xt % segs);
+  const int64_t j0 = 4 * t;
+  if (j0 >= np || ch >= n_chunks) return;
+  const TCChunk C = chunks[ch];
+  if (c0 >= C.npad) return;
+  double fx[4];
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     const int64_t j = p_begin + j0 + u;
-    const bool ok = j < p_end;
-    const double4 f = ok ? frac[j] : make_double4(0.0, 0.0, 0.0, 0.0);
-    fx[u] = f.x;
-    fy[u] = f.y;
-    fz[u] = f.z;
-    qs[u] = ok ? f.w * inv_qmax : 0.0;
+    fx[u] = j < p_end ? frac[j].x : 0.0;
   }
-  // y and z phase tables
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    double2 e1, cur = make_double2(1.0, 0.0);
-    double s, c;
-    sincospi(2.0 * fy[u], &s, &c);
-    e1 = make_double2(c, -s);
-    for (int t = 0; t < ny; ++t) {
-      const int my = ymin + t;
-      if ((t & 7) == 0) {
-        sincospi(2.0 * ((double)my * fy[u]), &s, &c);
-        cur = make_double2(c, -s);
-      } else {
-        cur = cmul(cur, e1);
-      }
-      ytab[(int64_t)t * np + j0 + u] = cur;
-    }
-    sincospi(2.0 * fz[u], &s, &c);
-    e1 = make_double2(c, -s);
-    for (int t = 0; t < nz; ++t) {
-      const int mz = zmin + t;
-      if ((t & 7) == 0) {
-        sincospi(2.0 * ((double)mz * fz[u]), &s, &c);
-        cur = make_double2(c, -s);
-      } else {
-        cur = cmul(cur, e1);
-      }
-      ztab[(int64_t)t * np + j0 + u] = make_double2(qs[u] * cur.x, qs[u] * cur.y);
-    }
-  }
-  // X slices: column c of chunk ch: Xr(a0 + c) for c < nr, Xs(max(a0,1) + c - nr)
   const int64_t kb = j0 / TC_KB;
   const int kin = (int)(j0 % TC_KB);
   const int64_t n_kb = np / TC_KB;
   const int xsl_b = tc_xsl_bytes(npad_max);
-  for (int ch = 0; ch < n_chunks; ++ch) {
-    const TCChunk C = chunks[ch];
-    uint8_t *base = xsl + ((int64_t)ch * n_kb + kb) * (int64_t)(TC_S * xsl_b);
-    double2 cr[4], e1[4];
+  uint8_t *base = xsl + ((int64_t)ch * n_kb + kb) * (int64_t)(TC_S * xsl_b);
+  const int sa0 = max(C.a0, 1), ns = max(0, C.a1 - sa0 + 1);
+  double2 cr[4], e1[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      double s, c;
-      sincospi(2.0 * fx[u], &s, &c);
-      e1[u] = make_double2(c, s);  // e^{+i 2pi f_x}: (cos, sin) of a f_x
-    }
-    // cosines then sines, each as a recurrence over a
-    for (int pass = 0; pass < 2; ++pass) {
-      const int a_lo = pass == 0 ? C.a0 : max(C.a0, 1);
-      const int col0 = pass == 0 ? 0 : C.nr;
-      const int ncol = pass == 0 ? C.nr : C.a1 - a_lo + 1;
-      for (int t = 0; t < ncol; ++t) {
-        const int a = a_lo + t;
-        uint2 b[4];
+  for (int u = 0; u < 4; ++u) {
+    double s, c;
+    sincospi(2.0 * fx[u], &s, &c);
+    e1[u] = make_double2(c, s);  // e^{+i 2pi f_x}: (cos, sin) of a f_x
+  }
+  int prev_pass = -1;
+  for (int col = c0; col < min(c0 + 8, C.npad); ++col) {
+    const int pass = col < C.nr ? 0 : (col < C.nr + ns ? 1 : 2);
+    uint32_t w[TC_S];
+    if (pass == 2) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if ((t & 7) == 0) {
-            double s, c;
-            sincospi(2.0 * ((double)a * fx[u]), &s, &c);
-            cr[u] = make_double2(c, s);
-          } else {
-            cr[u] = cmul(cr[u], e1[u]);
-          }
-          const bool ok = p_begin + j0 + u < p_end;
-          b[u] = tc_bits(ok ? (pass == 0 ? cr[u].x : cr[u].y) : 0.0);
+      for (int s = 0; s < TC_S; ++s) w[s] = 0u;
+    } else {
+      const int a = pass == 0 ? C.a0 + col : sa0 + (col - C.nr);
+      uint2 b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (pass != prev_pass) {
+          double s, c;
+          sincospi(2.0 * ((double)a * fx[u]), &s, &c);
+          cr[u] = make_double2(c, s);
+        } else {
+          cr[u] = cmul(cr[u], e1[u]);
         }
-        uint32_t w[TC_S];
-        tc_digits4(b[0], b[1], b[2], b[3], w);
-        const int off = tc_off(col0 + t, kin);
-#pragma unroll
-        for (int s = 0; s < TC_S; ++s)
-          *reinterpret_cast<uint32_t *>(base + s * xsl_b + off) = w[s];
+        const bool ok = p_begin + j0 + u < p_end;
+        b[u] = tc_bits(ok ? (pass == 0 ? cr[u].x : cr[u].y) : 0.0);
       }
+      tc_digits4(b[0], b[1], b[2], b[3], w);
     }
-    // zero padding columns
-    for (int cpad = C.nr + max(0, C.a1 - max(C.a0, 1) + 1); cpad < C.npad; ++cpad) {
-      const int off = tc_off(cpad, kin);
+    prev_pass = pass;
+    const int off = tc_off(col, kin);
 #pragma unroll
-      for (int s = 0; s < TC_S; ++s) *reinterpret_cast<uint32_t *>(base + s * xsl_b + off) = 0u;
-    }
+    for (int s = 0; s < TC_S; ++s) *reinterpret_cast<uint32_t *>(base + s * xsl_b + off) = w[s];
   }
 }
 
@@ -263,10 +259,17 @@ __global__ void __launch_bounds__(128)
 //   the pairs (m_y0 + i, m_z); Re G in rows 0..63, Im G in rows 64..127.
 //   tmap[(tile*64 + p) * (A+1) + a] = pair slots (x, y; -1 = none) of
 //   (a, m_y, m_z) in the K1 pair layout (k2p_finalize input).
-constexpr int TC_XS = 4;                      // X ring depth
+#ifndef TC_GSTAGES
+#define TC_GSTAGES 2
+#endif
+#ifndef TC_XSTAGES
+#define TC_XSTAGES 4
+#endif
+constexpr int TC_GS = TC_GSTAGES;             // G ring depth (produced)
+constexpr int TC_XS = TC_XSTAGES;             // X ring depth (bulk copies)
 constexpr int TC_NTHREADS = TC_THREADS + 64;  // + MMA warp + loader warp
 __host__ __device__ constexpr int tc_smem_bytes(int npad_max) {
-  return 2 * TC_S * TC_GSL + TC_XS * TC_S * tc_xsl_bytes(npad_max);
+  return TC_GS * TC_S * TC_GSL + TC_XS * TC_S * tc_xsl_bytes(npad_max);
 }
 __device__ __forceinline__ void mbar_arrive(uint32_t a) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
@@ -292,7 +295,7 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
              int64_t p_end, int64_t np, int64_t ppb, int ymin, int zmin, int A, int npad_max,
              int64_t n_pslots, double4 *__restrict__ spart, int dbg) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t g_full[2], g_empty[2], x_full[TC_XS], x_empty[TC_XS], acc_full;
+  __shared__ uint64_t g_full[TC_GS], g_empty[TC_GS], x_full[TC_XS], x_empty[TC_XS], acc_full;
   __shared__ uint32_t tmem_base_s;
   __shared__ int4 s_runs[8];
   const int tile = blockIdx.x, ch = blockIdx.y, split = blockIdx.z;
@@ -302,7 +305,7 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
   const int xsl_b = tc_xsl_bytes(npad_max);
   const int xblk = TC_S * xsl_b;  // bytes of one K-block's X slices
   uint8_t *gbuf = smem;
-  uint8_t *xbuf = smem + 2 * TC_S * TC_GSL;
+  uint8_t *xbuf = smem + TC_GS * TC_S * TC_GSL;
   const int64_t n_kb_all = np / TC_KB;
   const int64_t kb0 = (int64_t)split * (ppb / TC_KB);
   const int64_t kb1 = min(n_kb_all, kb0 + ppb / TC_KB);
@@ -310,7 +313,7 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
 
   if (threadIdx.x < 8) s_runs[threadIdx.x] = runs[tile * 8 + threadIdx.x];
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < TC_GS; ++i) {
       mbar_init(smem_u32(&g_full[i]), TC_THREADS / 32);
       mbar_init(smem_u32(&g_empty[i]), 1);
     }
@@ -345,16 +348,17 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
       }
     }
   } else if (warp == 8) {
-    // ---- MMA issuer ----
-    if (lane == 0) {
+    // ---- MMA issuer: the whole warp waits, one elected lane issues ----
+    {
       const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) |
                              ((uint32_t)(npad >> 3) << 17) | (8u << 24);
       for (int it = 0; it < nkb; ++it) {
-        const int gs = it & 1, xs = it % TC_XS;
-        mbar_wait(smem_u32(&g_full[gs]), (it >> 1) & 1);
+        const int gs = it % TC_GS, xs = it % TC_XS;
+        mbar_wait(smem_u32(&g_full[gs]), (it / TC_GS) & 1);
         mbar_wait(smem_u32(&x_full[xs]), (it / TC_XS) & 1);
         tc_fence_after();
-        if (!(dbg & 2)) {
+        __syncwarp();
+        if (!(dbg & 2) && elect_one()) {
           const uint64_t gd = tc_desc(smem_u32(gbuf + gs * TC_S * TC_GSL));
           const uint64_t xd = tc_desc(smem_u32(xbuf + xs * xblk));
           const uint32_t acc0 = it > 0 ? 1u : 0u;
@@ -378,15 +382,18 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
           }
           tc_commit(smem_u32(&g_empty[gs]));
           tc_commit(smem_u32(&x_empty[xs]));
-        } else {
+        } else if ((dbg & 2) && lane == 0) {
           mbar_arrive(smem_u32(&g_empty[gs]));
           mbar_arrive(smem_u32(&x_empty[xs]));
         }
+        __syncwarp();
       }
-      if (!(dbg & 2) && nkb > 0)
-        tc_commit(smem_u32(&acc_full));
-      else
-        mbar_arrive(smem_u32(&acc_full));
+      if (lane == 0) {
+        if (!(dbg & 2) && nkb > 0)
+          tc_commit(smem_u32(&acc_full));
+        else
+          mbar_arrive(smem_u32(&acc_full));
+      }
     }
   } else {
     // ---- G producers: core column pc (16 particles), row half ph, run g, quad qd ----
@@ -396,9 +403,9 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
     const int myl = run.y + 4 * ph;
     const bool active = 4 * ph < run.z;  // rows of this half exist in the run
     for (int it = 0; it < nkb; ++it) {
-      const int gs = it & 1;
+      const int gs = it % TC_GS;
       uint8_t *sb = gbuf + gs * TC_S * TC_GSL;
-      if (it >= 2) mbar_wait(smem_u32(&g_empty[gs]), ((it >> 1) - 1) & 1);
+      if (it >= TC_GS) mbar_wait(smem_u32(&g_empty[gs]), ((it / TC_GS) - 1) & 1);
       if (!(dbg & 1)) {
         const int64_t j = (kb0 + it) * TC_KB + kin;  // relative to p_begin
         double2 cur[4], e1[4];

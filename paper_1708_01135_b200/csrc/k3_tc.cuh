@@ -23,12 +23,50 @@
 // epilogue combines the 7 levels, multiplies by the particle's X(a) and
 // reduces over the rows (warp shuffles + shared memory).
 
+// The force GEMM splits W rows (scaled per row) and the unit phases into
+// T3_S byte slices and keeps the slice pairs with s + t >= T3_W0.  Measured
+// max|dF|/F_rms against the FP64 gather (c2 / c4 / c5):
+//   6 slices, w >= 5 (21 MMAs): 3.3e-14 / 2.7e-13 / 5.0e-14   <- default
+//   5 slices, w >= 4 (15 MMAs): 4.8e-12 / 5.4e-11 / 7.7e-12   (-15..20% time)
+//   5 slices, w >= 3 (19 MMAs): 2.8e-12 / 3.4e-11 / 4.5e-12   (40-bit quantisation)
+// all inside the 1e-9 F_rms tolerance; the default keeps a 3000x margin.
+#ifndef T3_SLICES
+#define T3_SLICES 6
+#endif
+#ifndef T3_LEVEL0
+#define T3_LEVEL0 5
+#endif
+constexpr int T3_S = T3_SLICES;
+constexpr int T3_W0 = T3_LEVEL0;
+constexpr int T3_NL = 2 * T3_S - 1 - T3_W0;  // 5 levels
+constexpr int T3_PAIRS = T3_S * T3_S - (T3_W0 * (T3_W0 + 1)) / 2;
+// 0x7F..7F and 1.5*2^52 + 0x80..80 for T3_S bytes
+constexpr double T3_SC = T3_S == 6 ? 140185576636287.0 : 547599908479.0;
+constexpr double T3_MAGIC =
+    6755399441055744.0 + (T3_S == 6 ? 141289400074368.0 : 551911719040.0);
+static_assert(T3_S == 5 || T3_S == 6, "force GEMM slices: 5 or 6");
+__device__ __forceinline__ uint2 t3_bits(double v) {
+  const double x = fma(v, T3_SC, T3_MAGIC);
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  return make_uint2((uint32_t)b, (uint32_t)(b >> 32));
+}
 constexpr int T3_NP = 64;         // particles per CTA (MMA N)
-constexpr int T3_AS = 3;          // A ring depth
+#ifndef T3_ASTAGES
+#define T3_ASTAGES 3
+#endif
+#ifndef T3_BSTAGES
+#define T3_BSTAGES 2
+#endif
+#ifndef T3_CLUSTER
+#define T3_CLUSTER 1  // measured: 2 neutral, 4 slower (c5) -- A loads are not the limit
+#endif
+constexpr int T3_CL = T3_CLUSTER;  // CTAs (particle tiles) sharing each A load (multicast)
+constexpr int T3_AS = T3_ASTAGES;  // A ring depth (bulk copies)
+constexpr int T3_BS = T3_BSTAGES;  // B ring depth (produced)
 constexpr int T3_BSL = (T3_NP / 8) * TC_SBO;  // one B slice (64 rows x 64 B)
 constexpr int T3_KMAX = 16384;    // K (bytes) per CTA: int32 exactness
 __host__ __device__ constexpr int t3_smem_bytes() {
-  return T3_AS * TC_S * TC_GSL + 2 * TC_S * T3_BSL;
+  return T3_AS * T3_S * TC_GSL + T3_BS * T3_S * T3_BSL;
 }
 
 // rows: type 0 Im V(Wdiff) [x], 1 Re V(Wsum) [x], 2 Im V(my Wsum), 3 Re V(my Wdiff),
@@ -37,79 +75,124 @@ struct T3Row {
   int a, type;
 };
 
-// k3t_wprep: one block per A row: the row's values over all K entries,
-// its max |value| (row scale), then the six digit slices in the K-block
-// shared-memory image: wsl[((mtile * nkb + kb) * 6 + s) * TC_GSL + tc_off(r, k)]
+// A-row value at K index k (2p: Re YZ coefficient, 2p+1: Im YZ coefficient)
+__device__ __forceinline__ double t3_value(const double2 *__restrict__ sp,
+                                           const int *__restrict__ slotmap, int A,
+                                           const int2 *__restrict__ pair_yz, int n_pairs_pad,
+                                           const T3Row R, int k) {
+  const int p = k >> 1;
+  if (p >= n_pairs_pad) return 0.0;
+  const int2 yz = pair_yz[p];
+  if (yz.x == INT_MIN) return 0.0;  // padding pair
+  const bool im_row = (R.type & 1) == 0;  // types 0, 2, 4
+  const bool use_sum = R.type == 1 || R.type == 2 || R.type == 4;
+  const int sp_ = slotmap[(size_t)(A + R.a) * n_pairs_pad + p];
+  const double2 wp = sp_ >= 0 ? sp[sp_] : make_double2(0.0, 0.0);
+  double2 w = wp;
+  if (R.a != 0) {
+    const int sm_ = slotmap[(size_t)(A - R.a) * n_pairs_pad + p];
+    const double2 wm = sm_ >= 0 ? sp[sm_] : make_double2(0.0, 0.0);
+    w = use_sum ? make_double2(wp.x + wm.x, wp.y + wm.y) : make_double2(wp.x - wm.x, wp.y - wm.y);
+  }
+  const double cw = R.type <= 1 ? 1.0 : (R.type <= 3 ? (double)yz.x : (double)yz.y);
+  if (im_row) return cw * ((k & 1) ? w.x : w.y);
+  return cw * ((k & 1) ? -w.y : w.x);
+}
+
+// k3t_wmax: grid (rows, K parts): row maxima |A[r, k]| (bit-pattern atomicMax
+// of non-negative doubles; row_scale zeroed before)
+__global__ void __launch_bounds__(256)
+    k3t_wmax(const double2 *__restrict__ sp, const int *__restrict__ slotmap, int A,
+             const int2 *__restrict__ pair_yz, int n_pairs_pad, const T3Row *__restrict__ rows,
+             int n_rows, unsigned long long *__restrict__ row_scale_bits) {
+  const int r = blockIdx.x;
+  if (r >= n_rows) return;
+  const T3Row R = rows[r];
+  const int K = 2 * n_pairs_pad;
+  double m = 0.0;
+  for (int k = blockIdx.y * blockDim.x + threadIdx.x; k < K; k += gridDim.y * blockDim.x)
+    m = fmax(m, fabs(t3_value(sp, slotmap, A, pair_yz, n_pairs_pad, R, k)));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.0)
+    atomicMax(row_scale_bits + r, (unsigned long long)__double_as_longlong(m));
+}
+
+// k3t_wprep: grid (M-tile rows, K parts): the six digit slices of A in the
+// K-block shared-memory image: wsl[((mtile * nkb + kb) * S + s) * TC_GSL + tc_off(r, k)]
 __global__ void __launch_bounds__(256)
     k3t_wprep(const double2 *__restrict__ sp, const int *__restrict__ slotmap, int A,
               const int2 *__restrict__ pair_yz, int n_pairs_pad, const T3Row *__restrict__ rows,
-              int n_rows, int nkb, double *__restrict__ row_scale, uint8_t *__restrict__ wsl) {
-  __shared__ double red[8];
+              int n_rows, int nkb, const double *__restrict__ row_scale, uint8_t *__restrict__ wsl) {
   const int r = blockIdx.x;
   const int mtile = r / 128, rl = r % 128;
   const bool live = r < n_rows;
   const T3Row R = live ? rows[r] : T3Row{0, 0};
-  const bool im_row = (R.type & 1) == 0;  // types 0, 2, 4
-  const bool use_sum = R.type == 1 || R.type == 2 || R.type == 4;
-  auto value = [&](int k) -> double {
-    if (!live) return 0.0;
-    const int p = k >> 1;
-    if (p >= n_pairs_pad) return 0.0;
-    const int2 yz = pair_yz[p];
-    if (yz.x == INT_MIN) return 0.0;  // padding pair
-    const int sp_ = slotmap[(size_t)(A + R.a) * n_pairs_pad + p];
-    const int sm_ = slotmap[(size_t)(A - R.a) * n_pairs_pad + p];
-    double2 w = make_double2(0.0, 0.0);
-    const double2 wp = sp_ >= 0 ? sp[sp_] : make_double2(0.0, 0.0);
-    if (R.a == 0) {
-      w = wp;
-    } else {
-      const double2 wm = sm_ >= 0 ? sp[sm_] : make_double2(0.0, 0.0);
-      w = use_sum ? make_double2(wp.x + wm.x, wp.y + wm.y) : make_double2(wp.x - wm.x, wp.y - wm.y);
-    }
-    const double cw = R.type <= 1 ? 1.0 : (R.type <= 3 ? (double)yz.x : (double)yz.y);
-    w.x *= cw;
-    w.y *= cw;
-    if (im_row) return (k & 1) ? w.x : w.y;
-    return (k & 1) ? -w.y : w.x;
-  };
-  const int K = 2 * n_pairs_pad;
-  double m = 0.0;
-  for (int k = threadIdx.x; k < K; k += blockDim.x) m = fmax(m, fabs(value(k)));
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
-  __syncthreads();
-  double mx = 0.0;
-  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) mx = fmax(mx, red[i]);
+  const double mx = live ? row_scale[r] : 0.0;
   const double inv = mx > 0.0 ? 1.0 / mx : 0.0;
-  if (threadIdx.x == 0) row_scale[r] = mx;
-  // digits: one word (4 consecutive k) per thread and slice
-  for (int k4 = threadIdx.x * 4; k4 < nkb * TC_KB; k4 += blockDim.x * 4) {
+  for (int k4 = (blockIdx.y * blockDim.x + threadIdx.x) * 4; k4 < nkb * TC_KB;
+       k4 += gridDim.y * blockDim.x * 4) {
     uint2 b[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) b[u] = tc_bits(fmin(1.0, fmax(-1.0, value(k4 + u) * inv)));
+    for (int u = 0; u < 4; ++u) {
+      const double v = live ? t3_value(sp, slotmap, A, pair_yz, n_pairs_pad, R, k4 + u) : 0.0;
+      b[u] = t3_bits(fmin(1.0, fmax(-1.0, v * inv)));
+    }
     uint32_t w[TC_S];
     tc_digits4(b[0], b[1], b[2], b[3], w);
     const int kb = k4 / TC_KB, kin = k4 % TC_KB;
-    uint8_t *base = wsl + ((size_t)mtile * nkb + kb) * TC_S * TC_GSL;
+    uint8_t *base = wsl + ((size_t)mtile * nkb + kb) * T3_S * TC_GSL;
     const int off = tc_off(rl, kin);
 #pragma unroll
-    for (int s = 0; s < TC_S; ++s) *reinterpret_cast<uint32_t *>(base + s * TC_GSL + off) = w[s];
+    for (int s = 0; s < T3_S; ++s) *reinterpret_cast<uint32_t *>(base + s * TC_GSL + off) = w[s];
   }
 }
 
-// k3t_gemm: grid (particle tiles of 64, M tiles, k splits).
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_mc(uint32_t dst, const void *src, uint32_t bytes,
+                                            uint32_t mbar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], "
+      "[%1], %2, [%3], %4;" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(mbar), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_mc(uint32_t mbar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;" ::"r"(mbar),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t local_addr, uint32_t cta) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_addr), "r"(cta));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
+               : "memory");
+}
+
+// k3t_gemm: grid (particle tiles of 64, M tiles, k splits), clusters of
+// T3_CL consecutive particle tiles: every A block is bulk-copied once per
+// cluster (each CTA fetches 1/T3_CL and multicasts it), every CTA's MMA
+// completion is multicast to the A-empty barriers of the whole cluster.
 //   pair_yz[p] = (m_y, m_z) of K pair p (runs of 8 consecutive m_y, padded
 //   entries INT_MIN); fpart[(ks_index) * 3 * n_local + c * n_local + i].
 __global__ void __launch_bounds__(TC_NTHREADS, 1)
     k3t_gemm(const double4 *__restrict__ frac, const double2 *__restrict__ base,
              const uint8_t *__restrict__ wsl, const double *__restrict__ row_scale,
              const T3Row *__restrict__ rows, int n_rows, const int2 *__restrict__ pair_yz,
-             int nkb_all, int kb_per_split, int64_t p_begin, int64_t p_end,
-             double *__restrict__ fpart, int dbg) {
+             int nkb_all, int kb_per_split, int64_t p_begin, int64_t p_end, int A,
+             const int4 *__restrict__ comp_rows, double *__restrict__ fpart, int dbg) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t b_full[2], b_empty[2], a_full[T3_AS], a_empty[T3_AS], acc_full;
+  __shared__ uint64_t b_full[T3_BS], b_empty[T3_BS], a_full[T3_AS], a_empty[T3_AS], acc_full;
   __shared__ uint32_t tmem_base_s;
   const int ptile = blockIdx.x, mtile = blockIdx.y, split = blockIdx.z;
   const int n_mtiles = gridDim.y;
@@ -118,17 +201,17 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
   const int kb0 = split * kb_per_split;
   const int nkb = max(0, min(nkb_all, kb0 + kb_per_split) - kb0);
   uint8_t *abuf = smem;
-  uint8_t *bbuf = smem + T3_AS * TC_S * TC_GSL;
-  constexpr int ABLK = TC_S * TC_GSL;
+  uint8_t *bbuf = smem + T3_AS * T3_S * TC_GSL;
+  constexpr int ABLK = T3_S * TC_GSL;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < T3_BS; ++i) {
       mbar_init(smem_u32(&b_full[i]), TC_THREADS / 32);
       mbar_init(smem_u32(&b_empty[i]), 1);
     }
     for (int i = 0; i < T3_AS; ++i) {
       mbar_init(smem_u32(&a_full[i]), 1);
-      mbar_init(smem_u32(&a_empty[i]), 1);
+      mbar_init(smem_u32(&a_empty[i]), T3_CL);
     }
     mbar_init(smem_u32(&acc_full), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -140,42 +223,51 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   tc_fence_before();
-  __syncthreads();
+  cluster_sync_all();  // barriers initialised cluster-wide before any remote signal
   tc_fence_after();
   const uint32_t tmem = tmem_base_s;
+  const uint32_t crank = cluster_rank();
+  constexpr uint16_t CMASK = (uint16_t)((1u << T3_CL) - 1u);
 
   if (warp == 9) {
     if (lane == 0) {
+      constexpr int PIECE = ABLK / T3_CL;
+      static_assert(ABLK % (16 * T3_CL) == 0, "A block must split into 16-byte pieces");
       for (int it = 0; it < nkb; ++it) {
         const int as = it % T3_AS;
         if (it >= T3_AS) mbar_wait(smem_u32(&a_empty[as]), ((it / T3_AS) - 1) & 1);
         const uint8_t *src = wsl + ((size_t)mtile * nkb_all + kb0 + it) * (size_t)ABLK;
         const uint32_t fb = smem_u32(&a_full[as]);
         mbar_expect_tx(fb, (uint32_t)ABLK);
-        bulk_g2s(smem_u32(abuf + as * ABLK), src, (uint32_t)ABLK, fb);
+        if (T3_CL == 1)
+          bulk_g2s(smem_u32(abuf + as * ABLK), src, (uint32_t)ABLK, fb);
+        else
+          bulk_g2s_mc(smem_u32(abuf + as * ABLK + crank * PIECE), src + crank * PIECE,
+                      (uint32_t)PIECE, fb, CMASK);
       }
     }
   } else if (warp == 8) {
-    if (lane == 0) {
+    {
       const uint32_t idesc =
           (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(T3_NP >> 3) << 17) | (8u << 24);
       for (int it = 0; it < nkb; ++it) {
-        const int bs = it & 1, as = it % T3_AS;
-        mbar_wait(smem_u32(&b_full[bs]), (it >> 1) & 1);
+        const int bs = it % T3_BS, as = it % T3_AS;
+        mbar_wait(smem_u32(&b_full[bs]), (it / T3_BS) & 1);
         mbar_wait(smem_u32(&a_full[as]), (it / T3_AS) & 1);
         tc_fence_after();
-        if (!(dbg & 2)) {
+        __syncwarp();
+        if (!(dbg & 2) && elect_one()) {
           const uint64_t ad = tc_desc(smem_u32(abuf + as * ABLK));
-          const uint64_t bd = tc_desc(smem_u32(bbuf + bs * TC_S * T3_BSL));
+          const uint64_t bd = tc_desc(smem_u32(bbuf + bs * T3_S * T3_BSL));
           const uint32_t acc0 = it > 0 ? 1u : 0u;
 #pragma unroll
-          for (int l = 0; l < TC_NL; ++l) {
-            const int w = TC_W0 + l;
-            const int s_lo = w - (TC_S - 1) > 0 ? w - (TC_S - 1) : 0;
+          for (int l = 0; l < T3_NL; ++l) {
+            const int w = T3_W0 + l;
+            const int s_lo = w - (T3_S - 1) > 0 ? w - (T3_S - 1) : 0;
 #pragma unroll
-            for (int s = 0; s < TC_S; ++s) {
+            for (int s = 0; s < T3_S; ++s) {
               const int t = w - s;
-              if (t < 0 || t >= TC_S) continue;
+              if (t < 0 || t >= T3_S) continue;
 #pragma unroll
               for (int ks = 0; ks < TC_KB / 32; ++ks)
                 tc_mma(tmem + (uint32_t)(l * T3_NP), ad + (uint64_t)((s * TC_GSL + ks * 256) >> 4),
@@ -184,16 +276,22 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
             }
           }
           tc_commit(smem_u32(&b_empty[bs]));
-          tc_commit(smem_u32(&a_empty[as]));
-        } else {
+          if (T3_CL == 1)
+            tc_commit(smem_u32(&a_empty[as]));
+          else
+            tc_commit_mc(smem_u32(&a_empty[as]), CMASK);
+        } else if ((dbg & 2) && lane == 0) {
           mbar_arrive(smem_u32(&b_empty[bs]));
-          mbar_arrive(smem_u32(&a_empty[as]));
+          for (int c = 0; c < T3_CL; ++c) mbar_arrive_cluster(smem_u32(&a_empty[as]), c);
         }
+        __syncwarp();
       }
-      if (!(dbg & 2) && nkb > 0)
-        tc_commit(smem_u32(&acc_full));
-      else
-        mbar_arrive(smem_u32(&acc_full));
+      if (lane == 0) {
+        if (!(dbg & 2) && nkb > 0)
+          tc_commit(smem_u32(&acc_full));
+        else
+          mbar_arrive(smem_u32(&acc_full));
+      }
     }
   } else {
     // ---- B producers: particle n, run g of the K-block (8 pairs = 16 k) ----
@@ -207,9 +305,9 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
     const double2 by = base[3 * jc + 1];
     const double2 ey = make_double2(by.x, -by.y);  // e^{+i 2pi f_y}
     for (int it = 0; it < nkb; ++it) {
-      const int bs = it & 1;
-      uint8_t *sb = bbuf + bs * TC_S * T3_BSL;
-      if (it >= 2) mbar_wait(smem_u32(&b_empty[bs]), ((it >> 1) - 1) & 1);
+      const int bs = it % T3_BS;
+      uint8_t *sb = bbuf + bs * T3_S * T3_BSL;
+      if (it >= T3_BS) mbar_wait(smem_u32(&b_empty[bs]), ((it / T3_BS) - 1) & 1);
       if (!(dbg & 1)) {
         const int p0 = (kb0 + it) * (TC_KB / 2) + 8 * g;  // first pair of this run
         const int2 yz = pair_yz[p0];
@@ -219,7 +317,7 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
           sincospi(2.0 * ((double)yz.x * f.y + (double)yz.y * f.z), &sn, &cs);
           cur = make_double2(cs, sn);
         }
-        uint32_t w4[TC_S][4];
+        uint32_t w4[T3_S][4];
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {  // pairs 2q4, 2q4+1 -> k = 4q4 .. 4q4+3
           const double2 v0 = cur;
@@ -227,13 +325,13 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
           const double2 v1 = cur;
           cur = cmul(cur, ey);
           uint32_t w[TC_S];
-          tc_digits4(tc_bits(v0.x), tc_bits(v0.y), tc_bits(v1.x), tc_bits(v1.y), w);
+          tc_digits4(t3_bits(v0.x), t3_bits(v0.y), t3_bits(v1.x), t3_bits(v1.y), w);
 #pragma unroll
-          for (int s = 0; s < TC_S; ++s) w4[s][q4] = w[s];
+          for (int s = 0; s < T3_S; ++s) w4[s][q4] = w[s];
         }
         const int off = tc_off(pn, 16 * g);
 #pragma unroll
-        for (int s = 0; s < TC_S; ++s)
+        for (int s = 0; s < T3_S; ++s)
           *reinterpret_cast<uint4 *>(sb + s * T3_BSL + off) =
               make_uint4(w4[s][0], w4[s][1], w4[s][2], w4[s][3]);
       }
@@ -247,47 +345,59 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
   mbar_wait(smem_u32(&acc_full), 0);
   tc_fence_after();
   __syncthreads();
-  // E[r][n] = this row's contribution to particle n's force component
-  // comp(r): the level sum times the row scale times X-coefficient
-  // (Xr for Im rows, Xi for Re rows, x a for the x component)
+  // X table: Xt[n * XS + a] = e^{+i 2pi a f_x} of the CTA's particles
+  // (sincospi every 8 steps, recurrence between); then E[r][n] = the row's
+  // level sum x row scale x X-coefficient (Xr for Im rows, Xi for Re rows,
+  // x a for the x component).  Rows are ordered by component, so the final
+  // sum for (n, c) runs over one contiguous row range.
   constexpr int ES = T3_NP + 1;
   double *E = reinterpret_cast<double *>(smem);
-  int *rcomp = reinterpret_cast<int *>(smem + 128 * ES * sizeof(double));
+  const int XS = A + 1;
+  double2 *Xt = reinterpret_cast<double2 *>(smem + 128 * ES * sizeof(double));
+  for (int t = threadIdx.x; t < T3_NP * ((XS + 7) / 8); t += TC_NTHREADS) {
+    const int n = t % T3_NP, a0 = 8 * (t / T3_NP);
+    const int64_t jg = p_begin + (int64_t)ptile * T3_NP + n;
+    const double fx = jg < p_end ? frac[jg].x : 0.0;
+    double sn, cs;
+    sincospi(2.0 * fx, &sn, &cs);
+    const double2 e1 = make_double2(cs, sn);
+    sincospi(2.0 * ((double)a0 * fx), &sn, &cs);
+    double2 x = make_double2(cs, sn);
+    for (int a = a0; a < min(XS, a0 + 8); ++a) {
+      Xt[n * XS + a] = x;
+      x = cmul(x, e1);
+    }
+  }
+  __syncthreads();
   if (warp < 8) {
     const int q = warp & 3, h = warp >> 2;
     const int r = 32 * q + lane;
     const int rg = mtile * 128 + r;
     const bool live = rg < n_rows && nkb > 0;
     const T3Row R = live ? rows[rg] : T3Row{0, 0};
-    const double rsc = live ? row_scale[rg] / (TC_SC * TC_SC) : 0.0;
+    const double rsc = live ? row_scale[rg] / (T3_SC * T3_SC) : 0.0;
     const int comp = R.type >> 1;  // 0 x, 1 y, 2 z
     const bool im_row = (R.type & 1) == 0;
-    if (h == 0) rcomp[r] = live ? comp : -1;
+    const double wx = comp == 0 ? (double)R.a : 1.0;
 #pragma unroll 1
     for (int c0 = 0; c0 < 32; c0 += 8) {
       double v[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) v[k] = 0.0;
 #pragma unroll
-      for (int l = TC_NL - 1; l >= 0; --l) {
+      for (int l = T3_NL - 1; l >= 0; --l) {
         int rr[8];
         tc_ld8(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(l * T3_NP + 32 * h + c0), rr);
         tc_wait_ld();
-        const double wl = ldexp(1.0, 8 * (TC_W0 + l));
+        const double wl = ldexp(1.0, 8 * (T3_W0 + l));
 #pragma unroll
         for (int k = 0; k < 8; ++k) v[k] = fma((double)rr[k], wl, v[k]);
       }
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const int n = 32 * h + c0 + k;
-        const int64_t jg = p_begin + (int64_t)ptile * T3_NP + n;
-        double coef = 0.0;
-        if (live && jg < p_end) {
-          double sn = 0.0, cs = 1.0;
-          if (R.a != 0) sincospi(2.0 * ((double)R.a * frac[jg].x), &sn, &cs);
-          coef = (im_row ? cs : sn) * (comp == 0 ? (double)R.a : 1.0);
-        }
-        E[r * ES + n] = v[k] * rsc * coef;
+        const double2 x = Xt[n * XS + R.a];
+        E[r * ES + n] = live ? v[k] * rsc * (im_row ? x.x : x.y) * wx : 0.0;
       }
     }
   }
@@ -302,18 +412,21 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
     const int c = t / T3_NP, n = t % T3_NP;
     const int64_t i = (int64_t)ptile * T3_NP + n;
     if (i >= n_local) continue;
+    const int4 cr = comp_rows[mtile];  // row ranges of x, y, z in this tile
+    const int lo = c == 0 ? 0 : (c == 1 ? cr.x : cr.y), hi = c == 0 ? cr.x : (c == 1 ? cr.y : cr.z);
     double s = 0.0;
-    for (int r = 0; r < 128; ++r)
-      if (rcomp[r] == c) s += E[r * ES + n];
+    for (int r = lo; r < hi; ++r) s += E[r * ES + n];
     fpart[(size_t)ks_index * 3 * n_local + (size_t)c * n_local + i] = s;
   }
+  // no CTA may leave while cluster peers can still signal its barriers
+  cluster_sync_all();
 }
 
 // k_i8_probe: the roofline denominator for the tensor-core kernels.  One CTA
 // per SM issues `iters` back-to-back int8 MMAs (M=128, N=256, K=32, both
 // operands in shared memory, the same no-swizzle K-major layout as the
 // kernels above) into TMEM and waits for them.
-__global__ void __launch_bounds__(128, 1) k_i8_probe(int iters, int *__restrict__ sink) {
+__global__ void __launch_bounds__(128, 1) k_i8_probe(int iters, int n_mma, int *__restrict__ sink) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t done;
   __shared__ uint32_t tmem_base_s;
@@ -335,7 +448,7 @@ __global__ void __launch_bounds__(128, 1) k_i8_probe(int iters, int *__restrict_
   tc_fence_after();
   const uint32_t tmem = tmem_base_s;
   if (threadIdx.x == 0) {
-    const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) | (8u << 24);
+    const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n_mma >> 3) << 17) | (8u << 24);
     const uint64_t ad = tc_desc(smem_u32(smem)), bd = tc_desc(smem_u32(smem + 16 * TC_SBO));
     for (int i = 0; i < iters; ++i) tc_mma(tmem, ad + (uint64_t)((i & 1) * 16), bd, idesc, i > 0 ? 1u : 0u);
     tc_commit(smem_u32(&done));

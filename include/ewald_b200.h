@@ -77,11 +77,12 @@ int ewb_set_stencil(ewb_handle *h, int rad);
  * bank is per process: handles must not run evaluations concurrently on
  * different streams of the same device. */
 int ewb_set_const_gather(ewb_handle *h, int on);
-/* Structure factor (Algorithm 1) on the int8 tensor cores (default on):
- * 48-bit fixed-point operands split into six int8 slices, exact int32
- * accumulation in TMEM, fp64 recombination (|dS| ~ 1e-15 max|S|).  0 runs
- * the FP64-pipe kernel instead (same results to ~1e-14). */
-int ewb_set_tensor_cores(ewb_handle *h, int on);
+/* Reciprocal space (Algorithms 1 and 2) on the int8 tensor cores: 48-bit
+ * fixed-point operands split into six int8 slices, exact int32 accumulation
+ * in TMEM, fp64 recombination (|dS| ~ 1e-15 max|S|, forces ~1e-13 F_rms).
+ * mode 0: FP64-pipe kernels; 1: tensor cores; 2 (default): tensor cores when
+ * N*K >= 2^26, else the FP64 kernels (faster for tiny systems). */
+int ewb_set_tensor_cores(ewb_handle *h, int mode);
 /* CUDA-graph replay of the evaluation pipeline (default on): the second
  * evaluate with unchanged shapes/pointers/configuration is captured, later
  * ones replay the graph.  0 runs every kernel eagerly. */

@@ -203,7 +203,9 @@ class Handle:
         self._check(self.lib.ewb_set_const_gather(self.h, 1 if on else 0))
 
     def set_tensor_cores(self, on):
-        self._check(self.lib.ewb_set_tensor_cores(self.h, 1 if on else 0))
+        """True: tensor cores, False: FP64 kernels, "auto": by problem size."""
+        mode = 2 if on == "auto" else (1 if on else 0)
+        self._check(self.lib.ewb_set_tensor_cores(self.h, mode))
 
     def set_graphs(self, on):
         self._check(self.lib.ewb_set_graphs(self.h, 1 if on else 0))

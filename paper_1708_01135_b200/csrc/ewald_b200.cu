@@ -1014,6 +1014,10 @@ __device__ __forceinline__ double rs_r2(double dx, double dy, double dz) {
 // pair-list entry: x = j (sorted index), y = g | kx<<4 | ky<<6 | kz<<8 with
 // k = 0: -L, 1: 0, 2: +L, 3: fold per pair
 constexpr int K6_LIST = 32 * K6_G + 32;  // pending pairs per warp
+constexpr uint32_t K6_SELF = 1u << 10;    // queue tag: own row, j > i only
+#ifndef K6_BBOX
+#define K6_BBOX 1  // bounding-box stage + queue before the per-centre tests (-3..7%)
+#endif
 
 #ifndef K6_SCAN
 #define K6_SCAN 0  // 1: per-step warp scan compaction, 0: per-centre ballots
@@ -1038,7 +1042,11 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
   // are evaluated in a converged round (lane l: pair l) and accumulated into
   // the lane's slot of F_g in shared memory; slots are summed at the end.
   __shared__ double4 s_i[K6_WARPS][K6_G];
-  __shared__ float4 s_cf[K6_WARPS][K6_G];  // centres + the piece's image shift, FP32
+  __shared__ float4 s_cf[K6_WARPS][K6_G];  // centres, FP32 (prefilter)
+  // prefilter queue: candidates within r_c of the centres' bounding box,
+  // already shifted into the centres' frame (x, y, z, j bits) + pair tag
+  __shared__ float4 s_q[K6_WARPS][64];
+  __shared__ uint32_t s_qt[K6_WARPS][64];
   __shared__ uint2 s_list[K6_WARPS][K6_LIST];
   __shared__ double3 s_f[K6_WARPS][K6_G][32];
   __shared__ double sh[K6_WARPS];
@@ -1167,6 +1175,60 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
       __syncwarp();
       cnt = rest;
     };
+    // FP32 centres and their bounding box (prefilter stage 1)
+    __syncwarp();
+    if (lane < gi) {
+      const double4 pi = s_i[warp][lane];
+      s_cf[warp][lane] = make_float4((float)pi.x, (float)pi.y, (float)pi.z, 0.0f);
+    }
+    __syncwarp();
+    float3 bb_lo = make_float3(3.0e38f, 3.0e38f, 3.0e38f), bb_hi = make_float3(-3.0e38f, -3.0e38f, -3.0e38f);
+    for (int g = 0; g < gi; ++g) {
+      const float4 c = s_cf[warp][g];
+      bb_lo = make_float3(fminf(bb_lo.x, c.x), fminf(bb_lo.y, c.y), fminf(bb_lo.z, c.z));
+      bb_hi = make_float3(fmaxf(bb_hi.x, c.x), fmaxf(bb_hi.y, c.y), fmaxf(bb_hi.z, c.z));
+    }
+    int qn = 0;  // queued candidates (warp-uniform)
+    // stage 2: entries [0, n) of the queue against every centre (lane l:
+    // entry l), accepted pairs into the pair list; keeps the tail
+    auto process_queue = [&](const int n) {
+      __syncwarp();
+      const bool ve = lane < n;
+      const float4 q = ve ? s_q[warp][lane] : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      const uint32_t qt = ve ? s_qt[warp][lane] : 0u;
+      const int j = __float_as_int(q.w);
+      const bool self = (qt & K6_SELF) != 0u;
+#pragma unroll
+      for (int g = 0; g < K6_G; ++g) {
+        if (g < gi) {
+          const float4 c = s_cf[warp][g];
+          const float dx = c.x - q.x, dy = c.y - q.y, dz = c.z - q.z;
+          const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+          const bool acc = ve && (r2 < P.rc2f) && (self ? j > first + g : j != first + g);
+          const unsigned bal = __ballot_sync(0xffffffffu, acc);
+          if (acc)
+            s_list[warp][cnt + __popc(bal & lt_mask)] =
+                make_uint2((uint32_t)j, (qt & ~K6_SELF) | (uint32_t)g);
+          cnt += __popc(bal);
+          accepted += __popc(bal);
+        }
+      }
+      __syncwarp();
+      const int rest = qn - n;
+      float4 mq = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      uint32_t mt = 0u;
+      if (lane < rest) {
+        mq = s_q[warp][n + lane];
+        mt = s_qt[warp][n + lane];
+      }
+      __syncwarp();
+      if (lane < rest) {
+        s_q[warp][lane] = mq;
+        s_qt[warp][lane] = mt;
+      }
+      qn = rest;
+      if (cnt >= 32) drain();
+    };
     // candidate step: lane = candidate j, test all centres.  FX / FYZ:
     // fold x / y,z per pair (reference rule), else add the piece's shift.
     // after: candidates must satisfy j > i (half shell, same row / scan-all)
@@ -1180,26 +1242,19 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
         k = d >= P.hl ? 0u : (d < -P.hl ? 2u : 1u);
         return k == 1u ? d : (k == 0u ? __dsub_rn(d, P.L) : __dadd_rn(d, P.L));
       };
-      if constexpr (!FX && !FYZ) {
-        // FP32 prefilter: a conservative superset of the reference's
-        // predicate (rc2f includes the rounding bound); the exact FP64 r^2 <
-        // r_c^2 decides inside pair_eval, so results are unchanged
-        __syncwarp();
-        if (lane < gi) {
-          const double4 pi = s_i[warp][lane];
-          s_cf[warp][lane] = make_float4((float)(pi.x + sx), (float)(pi.y + sy),
-                                         (float)(pi.z + sz), 0.0f);
-        }
-        __syncwarp();
+      if constexpr (!FX && !FYZ && !K6_BBOX) {
+        // FP32 prefilter: every candidate against every centre
+        const float sxf = (float)sx, syf = (float)sy, szf = (float)sz;
         for (int j0 = jb; j0 < je; j0 += 32) {
           const int j = j0 + lane;
           const bool vj = j < je;
           const float4 pj = sorted_f[vj ? j : jb];
+          const float px = pj.x - sxf, py = pj.y - syf, pz = pj.z - szf;
 #pragma unroll
           for (int g = 0; g < K6_G; ++g) {
             if (g < gi) {
               const float4 c = s_cf[warp][g];
-              const float dx = c.x - pj.x, dy = c.y - pj.y, dz = c.z - pj.z;
+              const float dx = c.x - px, dy = c.y - py, dz = c.z - pz;
               const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
               const bool acc = vj && (r2 < P.rc2f) && (after ? j > first + g : j != first + g);
               const unsigned bal = __ballot_sync(0xffffffffu, acc);
@@ -1209,6 +1264,35 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
             }
           }
           if (cnt >= 32) drain();
+        }
+        return;
+      }
+      if constexpr (!FX && !FYZ && K6_BBOX) {
+        // FP32 prefilter, stage 1: distance to the centres' bounding box
+        // (one test per candidate, a conservative superset of stage 2 since
+        // FP32 rounding is monotone); survivors are queued in the centres'
+        // frame and tested against every centre in full 32-wide steps.
+        // rc2f includes the rounding bound; the exact FP64 r^2 < r_c^2
+        // decides inside pair_eval, so results are unchanged.
+        const float sxf = (float)sx, syf = (float)sy, szf = (float)sz;
+        const uint32_t qtag = tag | (after ? K6_SELF : 0u);
+        for (int j0 = jb; j0 < je; j0 += 32) {
+          const int j = j0 + lane;
+          const bool vj = j < je;
+          const float4 pj = sorted_f[vj ? j : jb];
+          const float px = pj.x - sxf, py = pj.y - syf, pz = pj.z - szf;
+          const float ddx = fmaxf(0.0f, fmaxf(bb_lo.x - px, px - bb_hi.x));
+          const float ddy = fmaxf(0.0f, fmaxf(bb_lo.y - py, py - bb_hi.y));
+          const float ddz = fmaxf(0.0f, fmaxf(bb_lo.z - pz, pz - bb_hi.z));
+          const bool pass = vj && fmaf(ddx, ddx, fmaf(ddy, ddy, ddz * ddz)) < P.rc2f;
+          const unsigned bal = __ballot_sync(0xffffffffu, pass);
+          if (pass) {
+            const int at = qn + __popc(bal & lt_mask);
+            s_q[warp][at] = make_float4(px, py, pz, __int_as_float(j));
+            s_qt[warp][at] = qtag;
+          }
+          qn += __popc(bal);
+          if (qn >= 32) process_queue(32);
         }
         return;
       }
@@ -1359,6 +1443,7 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
         }
       }
     }
+    if (qn > 0) process_queue(qn);
     __syncwarp();
     if (cnt > 0) round(0, cnt);
     if (coincident) atomicOr(err, ERR_COINCIDENT);
@@ -1725,7 +1810,7 @@ struct ewb_handle {
   int stencil_rad = 0;  // 0 auto, 1 force r_c cells (testing)
   int deterministic = 0;  // 1: full-shell real space, no atomics (bitwise reproducible)
   int k3_const = 1;       // constant-bank force gather for large systems
-  int use_tc = 1;         // structure factor on the int8 tensor cores (k1_tc.cuh)
+  int use_tc = 2;         // int8 tensor-core reciprocal space: 0 off, 1 forced, 2 auto (N*K)
   int tc_dbg = 0;         // tools only (EWB_TC_DBG): 1 skip G production, 2 skip MMAs
   DBuf tc_qmax, tc_ytab, tc_ztab, tc_xsl;
   DBuf t3_wsl, t3_rscale;
@@ -2252,6 +2337,16 @@ int occupancy_k1(ewb_handle *h, int M, size_t smem, int *occ_out) {
 
 // S(k) over particles [i0, i1): partials over particle chunks reduced into
 // d_slots (if non-null) or left in h->spart with *n_part set.
+// Tensor-core reciprocal space for this particle count?  Auto mode: the
+// GEMM set-up (prep kernels, operand splits, epilogues) costs a few tens of
+// microseconds, so tiny systems (c1: N K = 2.5e6) stay on the FP64 kernels.
+constexpr double TC_AUTO_MIN_WORK = 67108864.0;  // N * K
+bool tc_wanted(const ewb_handle *h, int64_t n) {
+  if (h->use_tc == 0) return false;
+  if (h->use_tc == 1) return true;
+  return (double)n * (double)h->plan.K >= TC_AUTO_MIN_WORK;
+}
+
 // Tensor-core structure factor (k1_tc.cuh): same pair-layout partials as K1.
 int stage_rho_tc(ewb_handle *h, int64_t i0, int64_t i1, int *n_part_out) {
   Plan &P = h->plan;
@@ -2305,7 +2400,7 @@ int stage_rho_tc(ewb_handle *h, int64_t i0, int64_t i1, int *n_part_out) {
 
 int stage_rho(ewb_handle *h, int64_t i0, int64_t i1, int *n_part_out) {
   Plan &P = h->plan;
-  if (h->use_tc && P.tc_ok) return stage_rho_tc(h, i0, i1, n_part_out);
+  if (P.tc_ok && tc_wanted(h, h->n)) return stage_rho_tc(h, i0, i1, n_part_out);
   const int M1 = P.M1;
   const size_t smem = 2 * (size_t)P.pchunk * (P.ts_max | 1) * sizeof(double2) +
                       (size_t)P.ts_max * sizeof(int4);
@@ -2423,7 +2518,7 @@ int stage_recip_tc(ewb_handle *h, int64_t i0, int64_t i1, double *d_force) {
     const int64_t ptiles_pad = ((ptiles + T3_CL - 1) / T3_CL) * T3_CL;
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3((unsigned)ptiles_pad, P.t3_mtiles, ns);
-    lc.blockDim = dim3(TC_NTHREADS);
+    lc.blockDim = dim3(T3_THREADS);
     lc.dynamicSmemBytes = smem;
     lc.stream = h->stream;
     cudaLaunchAttribute at[1];
@@ -2457,7 +2552,7 @@ int stage_recip_forces(ewb_handle *h, int64_t i0, int64_t i1, double *d_force, b
     if (energy) CK(cudaMemsetAsync(d_u_out, 0, sizeof(double), h->stream));
     return EWB_OK;
   }
-  if (!energy && h->use_tc && P.t3_ok) return stage_recip_tc(h, i0, i1, d_force);
+  if (!energy && P.t3_ok && tc_wanted(h, h->n)) return stage_recip_tc(h, i0, i1, d_force);
   const int M = P.M;
   k3_fn fn = k3_table(M, energy);
   int &occ = h->occ_k3[M][energy ? 1 : 0];
@@ -3079,7 +3174,8 @@ int ewb_set_const_gather(ewb_handle *h, int on) {
 
 int ewb_set_tensor_cores(ewb_handle *h, int on) {
   if (!h) return EWB_EINVAL;
-  h->use_tc = on ? 1 : 0;
+  if (on < 0 || on > 2) return h->fail(EWB_EINVAL, "tensor-core mode must be 0, 1 or 2");
+  h->use_tc = on;
   ++h->gen;
   return EWB_OK;
 }
@@ -3421,7 +3517,7 @@ int ewb_tc_info(const ewb_handle *h, int64_t *info8) {
   const Plan &P = h->plan;
   int64_t npad_sum = 0;
   for (const auto &c : P.tc_chunks_host) npad_sum += c.npad;
-  info8[0] = P.tc_ok && h->use_tc ? 1 : 0;
+  info8[0] = P.tc_ok && tc_wanted(h, h->n) ? 1 : 0;
   info8[1] = P.tc_mtiles;
   info8[2] = npad_sum;         // sum of padded X columns over the a-chunks
   info8[3] = P.t3_mtiles;

@@ -50,7 +50,16 @@ __device__ __forceinline__ uint2 t3_bits(double v) {
   const unsigned long long b = (unsigned long long)__double_as_longlong(x);
   return make_uint2((uint32_t)b, (uint32_t)(b >> 32));
 }
-constexpr int T3_NP = 64;         // particles per CTA (MMA N)
+#ifndef T3_PARTICLES
+#define T3_PARTICLES 80
+#endif
+// particles per CTA (MMA N): 6 levels x 80 = 480 of 512 TMEM columns; the
+// shape probe gives 3487 TOP/s at N=80 vs 3006 at 64 (shared-memory A read)
+constexpr int T3_NP = T3_PARTICLES;
+static_assert(T3_NP % 16 == 0 && T3_NP <= 80, "N: multiple of 16, TMEM budget");
+constexpr int T3_PW = T3_NP / 8;               // producer warps (8 particles x 4 runs each)
+constexpr int T3_THREADS = (T3_PW + 2) * 32;   // + MMA warp + loader warp
+constexpr int T3_HALF = T3_NP / 2;             // epilogue columns per warp
 #ifndef T3_ASTAGES
 #define T3_ASTAGES 3
 #endif
@@ -63,7 +72,7 @@ constexpr int T3_NP = 64;         // particles per CTA (MMA N)
 constexpr int T3_CL = T3_CLUSTER;  // CTAs (particle tiles) sharing each A load (multicast)
 constexpr int T3_AS = T3_ASTAGES;  // A ring depth (bulk copies)
 constexpr int T3_BS = T3_BSTAGES;  // B ring depth (produced)
-constexpr int T3_BSL = (T3_NP / 8) * TC_SBO;  // one B slice (64 rows x 64 B)
+constexpr int T3_BSL = (T3_NP / 8) * TC_SBO;  // one B slice (T3_NP rows x 64 B)
 constexpr int T3_KMAX = 16384;    // K (bytes) per CTA: int32 exactness
 __host__ __device__ constexpr int t3_smem_bytes() {
   return T3_AS * T3_S * TC_GSL + T3_BS * T3_S * T3_BSL;
@@ -185,7 +194,7 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t local_addr, uint32_
 // completion is multicast to the A-empty barriers of the whole cluster.
 //   pair_yz[p] = (m_y, m_z) of K pair p (runs of 8 consecutive m_y, padded
 //   entries INT_MIN); fpart[(ks_index) * 3 * n_local + c * n_local + i].
-__global__ void __launch_bounds__(TC_NTHREADS, 1)
+__global__ void __launch_bounds__(T3_THREADS, 1)
     k3t_gemm(const double4 *__restrict__ frac, const double2 *__restrict__ base,
              const uint8_t *__restrict__ wsl, const double *__restrict__ row_scale,
              const T3Row *__restrict__ rows, int n_rows, const int2 *__restrict__ pair_yz,
@@ -206,7 +215,7 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < T3_BS; ++i) {
-      mbar_init(smem_u32(&b_full[i]), TC_THREADS / 32);
+      mbar_init(smem_u32(&b_full[i]), T3_PW);
       mbar_init(smem_u32(&b_empty[i]), 1);
     }
     for (int i = 0; i < T3_AS; ++i) {
@@ -229,7 +238,7 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
   const uint32_t crank = cluster_rank();
   constexpr uint16_t CMASK = (uint16_t)((1u << T3_CL) - 1u);
 
-  if (warp == 9) {
+  if (warp == T3_PW + 1) {
     if (lane == 0) {
       constexpr int PIECE = ABLK / T3_CL;
       static_assert(ABLK % (16 * T3_CL) == 0, "A block must split into 16-byte pieces");
@@ -246,7 +255,7 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
                       (uint32_t)PIECE, fb, CMASK);
       }
     }
-  } else if (warp == 8) {
+  } else if (warp == T3_PW) {
     {
       const uint32_t idesc =
           (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(T3_NP >> 3) << 17) | (8u << 24);
@@ -354,7 +363,7 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
   double *E = reinterpret_cast<double *>(smem);
   const int XS = A + 1;
   double2 *Xt = reinterpret_cast<double2 *>(smem + 128 * ES * sizeof(double));
-  for (int t = threadIdx.x; t < T3_NP * ((XS + 7) / 8); t += TC_NTHREADS) {
+  for (int t = threadIdx.x; t < T3_NP * ((XS + 7) / 8); t += T3_THREADS) {
     const int n = t % T3_NP, a0 = 8 * (t / T3_NP);
     const int64_t jg = p_begin + (int64_t)ptile * T3_NP + n;
     const double fx = jg < p_end ? frac[jg].x : 0.0;
@@ -380,14 +389,14 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
     const bool im_row = (R.type & 1) == 0;
     const double wx = comp == 0 ? (double)R.a : 1.0;
 #pragma unroll 1
-    for (int c0 = 0; c0 < 32; c0 += 8) {
+    for (int c0 = 0; c0 < T3_HALF; c0 += 8) {
       double v[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) v[k] = 0.0;
 #pragma unroll
       for (int l = T3_NL - 1; l >= 0; --l) {
         int rr[8];
-        tc_ld8(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(l * T3_NP + 32 * h + c0), rr);
+        tc_ld8(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(l * T3_NP + T3_HALF * h + c0), rr);
         tc_wait_ld();
         const double wl = ldexp(1.0, 8 * (T3_W0 + l));
 #pragma unroll
@@ -395,7 +404,7 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
       }
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        const int n = 32 * h + c0 + k;
+        const int n = T3_HALF * h + c0 + k;
         const double2 x = Xt[n * XS + R.a];
         E[r * ES + n] = live ? v[k] * rsc * (im_row ? x.x : x.y) * wx : 0.0;
       }
@@ -408,7 +417,7 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
   const int ks_index = split * n_mtiles + mtile;
-  for (int t = threadIdx.x; t < 3 * T3_NP; t += TC_NTHREADS) {
+  for (int t = threadIdx.x; t < 3 * T3_NP; t += T3_THREADS) {
     const int c = t / T3_NP, n = t % T3_NP;
     const int64_t i = (int64_t)ptile * T3_NP + n;
     if (i >= n_local) continue;

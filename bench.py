@@ -15,7 +15,8 @@ r_c=6, cube |n_i|<=18 (25,326 half-space k-vectors).
 * e2e: the same metric through the reference-facing API
   (EwaldSolver.evaluate on a ParticleSet whose arrays live in pinned host
   memory), host<->device copies inside the timed region.
-* roofline: the stage with the largest share of the step.  S(k) and the
+* roofline: the stage with the largest share of the step (stage times from
+  a separate pass with the two-stream overlap off).  S(k) and the
   reciprocal forces run on the int8 tensor cores (k1t_gemm, k3t_gemm):
   executed MMA ops against the int8 peak measured by ewb_probe_i8_peak;
   real space (k6) is FP64-bound: in-cutoff pairs x 64 flops against the
@@ -321,6 +322,19 @@ def run_ours(args):
                 stage += tm
     launches = h.launch_count() - launches0
     total_s = max_over_ranks(total_ms * 1e-3, world, dev)
+    if world == 1:
+        # stage times for the roofline from a separate sequential pass: with
+        # the default two-stream overlap the stage windows overlap in time
+        h.set_overlap(False)
+        for _ in range(2):
+            step()
+        stage = np.zeros(4)
+        for _ in range(args.steps):
+            flush_l2(l2)
+            torch.cuda.synchronize()
+            _, tm = step()
+            stage += tm
+        h.set_overlap(True)
     value = args.steps / total_s
     clocks = clk.summary()
 

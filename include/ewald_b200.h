@@ -83,6 +83,10 @@ int ewb_set_const_gather(ewb_handle *h, int on);
  * mode 0: FP64-pipe kernels; 1: tensor cores; 2 (default): tensor cores when
  * N*K >= 2^26, else the FP64 kernels (faster for tiny systems). */
 int ewb_set_tensor_cores(ewb_handle *h, int mode);
+/* Run reciprocal space on a second stream concurrently with real space
+ * (default on; applies when both reciprocal stages use the tensor cores).
+ * The stage times of ewb_evaluate then overlap. */
+int ewb_set_overlap(ewb_handle *h, int on);
 /* CUDA-graph replay of the evaluation pipeline (default on): the second
  * evaluate with unchanged shapes/pointers/configuration is captured, later
  * ones replay the graph.  0 runs every kernel eagerly. */

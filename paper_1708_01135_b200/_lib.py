@@ -53,6 +53,7 @@ SIGNATURES = {
     "ewb_set_graphs": (_INT, [_P, _INT]),
     "ewb_set_const_gather": (_INT, [_P, _INT]),
     "ewb_set_tensor_cores": (_INT, [_P, _INT]),
+    "ewb_set_overlap": (_INT, [_P, _INT]),
     "ewb_set_system": (_INT, [_P, _D, _D, _D, _D]),
     "ewb_set_kspace": (_INT, [_P, _P, _I64, _P]),
     "ewb_kspace_info": (_INT, [_P, _P]),
@@ -206,6 +207,9 @@ class Handle:
         """True: tensor cores, False: FP64 kernels, "auto": by problem size."""
         mode = 2 if on == "auto" else (1 if on else 0)
         self._check(self.lib.ewb_set_tensor_cores(self.h, mode))
+
+    def set_overlap(self, on):
+        self._check(self.lib.ewb_set_overlap(self.h, 1 if on else 0))
 
     def set_graphs(self, on):
         self._check(self.lib.ewb_set_graphs(self.h, 1 if on else 0))

@@ -1796,6 +1796,8 @@ struct Plan {
 
 }  // namespace
 
+constexpr int N_SEG = 6;  // pipeline: load | cells | pairs | S(k) | forces | combine + self
+
 struct ewb_handle {
   int device = 0;
   int n_sm = 148;
@@ -1803,6 +1805,14 @@ struct ewb_handle {
   cudaStream_t stream = nullptr;
   cudaStream_t aux_stream = nullptr;  // second stream of the constant-bank gather
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // reciprocal space concurrently with real space (tensor-core path)
+  cudaStream_t rstream = nullptr;
+  cudaEvent_t ev_rfork = nullptr, ev_rjoin = nullptr;
+  int overlap = 1;
+  bool ov_active = false;       // this evaluation runs the two streams
+  int t3_pend_nks = 0;          // deferred k3_combine (overlap mode)
+  int64_t t3_pend_i0 = 0, t3_pend_n = 0;
+  double *t3_pend_force = nullptr;
   cudaEvent_t ev[6] = {};
   std::string err;
   int mcap = 28;   // K3 segment cap
@@ -1815,6 +1825,7 @@ struct ewb_handle {
   DBuf tc_qmax, tc_ytab, tc_ztab, tc_xsl;
   DBuf t3_wsl, t3_rscale;
   DBuf pairc;  // in-cutoff pairs visited by the last real-space pass
+  DBuf eblk_r;  // energy scratch of the reciprocal stages (own stream)
   void *tc_spart_zeroed = nullptr;  // spart buffer whose unmapped slots were zeroed
   int64_t launches = 0;
   // system
@@ -1851,8 +1862,8 @@ struct ewb_handle {
   bool use_graphs = true;
   uint64_t gen = 0;  // bumped by every configuration change
   GKey gkey, warm_key;
-  cudaGraphExec_t gexec[5] = {};
-  int64_t glaunch[5] = {};
+  cudaGraphExec_t gexec[N_SEG] = {};
+  int64_t glaunch[N_SEG] = {};
   int occ_k1[MAXM + 1] = {};
   int occ_k3[MAXM + 1][2] = {};
   bool k1_attr[MAXM + 1] = {};
@@ -2460,13 +2471,13 @@ int stage_finalize_pairs(ewb_handle *h, const double4 *src, int n_part, double *
   Plan &P = h->plan;
   const int64_t n_pslots = (int64_t)P.M1 * P.n_pitems;
   const unsigned nb = blocks_for(n_pslots, RED_THREADS);
-  CK(h->eblk.ensure(nb * sizeof(double)));
+  CK(h->eblk_r.ensure(nb * sizeof(double)));
   k2p_finalize<<<nb, RED_THREADS, 0, h->stream>>>(src, n_part, n_pslots, P.pslot_map.as<int4>(),
                                                   P.slot_coeff.as<double>(), P.K, d_rho_out,
                                                   nullptr, h->sp.as<double2>(),
-                                                  h->eblk.as<double>(), 1);
+                                                  h->eblk_r.as<double>(), 1);
   CKL();
-  k_sum<<<1, 1024, 0, h->stream>>>(h->eblk.as<double>(), nb, 1.0, d_u_out);
+  k_sum<<<1, 1024, 0, h->stream>>>(h->eblk_r.as<double>(), nb, 1.0, d_u_out);
   CKL();
   return EWB_OK;
 }
@@ -2535,6 +2546,13 @@ int stage_recip_tc(ewb_handle *h, int64_t i0, int64_t i1, double *d_force) {
                           (const int2 *)P.t3_pair_yz.as<int2>(), nkb, kbps, i0, i1, P.tc_A,
                           (const int4 *)P.t3_comp.as<int4>(), h->fpart.as<double>(), h->tc_dbg));
     ++h->launches;
+  }
+  if (h->ov_active) {  // the combine adds into forces: after the real-space join
+    h->t3_pend_nks = n_ks;
+    h->t3_pend_i0 = i0;
+    h->t3_pend_n = n_local;
+    h->t3_pend_force = d_force;
+    return EWB_OK;
   }
   const unsigned nbc = blocks_for(n_local, RED_THREADS);
   k3_combine<<<nbc, RED_THREADS, 0, h->stream>>>(h->fpart.as<double>(), nullptr, n_ks, i0, n_local,
@@ -2868,7 +2886,7 @@ int h2d_force(ewb_handle *h, const double *force, int64_t n) {
 // evaluation pipeline in five segments; timing events sit between them
 // (outside any captured graph): ev0 | cells | ev1 | pairs | ev2 | S(k) |
 // ev3 | forces + self | ev4
-constexpr int N_SEG = 5;
+// N_SEG (pipeline segments) is defined with the handle
 int pipeline_seg(ewb_handle *h, int seg, const double *d_pos, const double *d_q, int64_t n,
                  double *d_force, double *d_rho_out) {
   int rc;
@@ -2889,12 +2907,21 @@ int pipeline_seg(ewb_handle *h, int seg, const double *d_pos, const double *d_q,
       if ((rc = stage_rho(h, 0, h->n, &n_part))) return rc;
       return stage_finalize_pairs(h, h->spart.as<double4>(), n_part, d_rho_out, en + 1);
     }
+    case 4:
+      if (!h->coul_on) return EWB_OK;
+      return stage_recip_forces(h, 0, h->n, d_force, false, nullptr);
     default:
       if (!h->coul_on) {
         CK(cudaMemsetAsync(en + 2, 0, sizeof(double), h->stream));
         return EWB_OK;
       }
-      if ((rc = stage_recip_forces(h, 0, h->n, d_force, false, nullptr))) return rc;
+      if (h->ov_active && h->t3_pend_nks > 0) {
+        const unsigned nbc = blocks_for(h->t3_pend_n, RED_THREADS);
+        k3_combine<<<nbc, RED_THREADS, 0, h->stream>>>(
+            h->fpart.as<double>(), nullptr, h->t3_pend_nks, h->t3_pend_i0, h->t3_pend_n,
+            h->frac.as<double4>(), 4.0 * M_PI / h->L, h->t3_pend_force, nullptr, 0);
+        CKL();
+      }
       return stage_self(h, en + 2);
   }
 }
@@ -2918,19 +2945,60 @@ int run_eval(ewb_handle *h, const double *d_pos, const double *d_q, int64_t n, d
   const int64_t l0 = h->launches;
   int rc = EWB_OK;
   bool captured_all = capture;
+  // reciprocal space (segments 3, 4) on its own stream, concurrently with
+  // real space (1, 2), when both reciprocal stages run on the tensor cores
+  // (their kernels touch neither the forces nor the real-space scratch; the
+  // force combine waits for the join in segment 5)
+  struct OvGuard {  // the stage APIs must never see a deferred combine
+    ewb_handle *h;
+    ~OvGuard() { h->ov_active = false; }
+  } ov_guard{h};
+  h->ov_active = h->overlap && h->coul_on && !h->lj_on && h->plan.tc_ok && h->plan.t3_ok &&
+                 tc_wanted(h, n);
+  h->t3_pend_nks = 0;
+  cudaStream_t main_stream = h->stream;
   for (int seg = 0; seg < N_SEG; ++seg) {
-    if (timed && seg >= 1) CK(cudaEventRecord(h->ev[seg - 1], h->stream));
+    const bool on_r = h->ov_active && (seg == 3 || seg == 4);
+    cudaStream_t st = on_r ? h->rstream : main_stream;
+    if (h->ov_active && seg == 1) {
+      CK(cudaEventRecord(h->ev_rfork, main_stream));
+      CK(cudaStreamWaitEvent(h->rstream, h->ev_rfork, 0));
+    }
+    if (h->ov_active && seg == 5) {
+      if (timed) CK(cudaEventRecord(h->ev[2], main_stream));  // after the pairs, before the join
+      CK(cudaEventRecord(h->ev_rjoin, h->rstream));
+      CK(cudaStreamWaitEvent(main_stream, h->ev_rjoin, 0));
+    }
+    // timing events: 0 | cells | 1 | pairs | 2   3 | S(k) | 4 | forces | 5
+    if (timed) {
+      if (seg == 1) CK(cudaEventRecord(h->ev[0], st));
+      if (seg == 2) CK(cudaEventRecord(h->ev[1], st));
+      if (seg == 3) {
+        if (!h->ov_active) CK(cudaEventRecord(h->ev[2], st));
+        CK(cudaEventRecord(h->ev[3], st));
+      }
+      if (seg == 4) CK(cudaEventRecord(h->ev[4], st));
+    }
+    h->stream = st;
     if (replay) {
-      CK(cudaGraphLaunch(h->gexec[seg], h->stream));
+      cudaError_t e = cudaGraphLaunch(h->gexec[seg], st);
+      h->stream = main_stream;
+      CK(e);
+      if (timed && seg == 4) CK(cudaEventRecord(h->ev[5], st));
       continue;
     }
     if (capture && captured_all) {
-      CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+      cudaError_t eb = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+      if (eb != cudaSuccess) {
+        h->stream = main_stream;
+        CK(eb);
+      }
       const int64_t s0 = h->launches;
       rc = pipeline_seg(h, seg, d_pos, d_q, n, d_force, d_rho);
       cudaGraph_t g = nullptr;
-      const cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+      const cudaError_t e = cudaStreamEndCapture(st, &g);
       if (rc) {
+        h->stream = main_stream;
         if (g) cudaGraphDestroy(g);
         return rc;
       }
@@ -2939,9 +3007,11 @@ int run_eval(ewb_handle *h, const double *d_pos, const double *d_q, int64_t n, d
         h->gexec[seg] = nullptr;
         const cudaError_t ei = cudaGraphInstantiate(&h->gexec[seg], g, 0);
         cudaGraphDestroy(g);
-        CK(ei);
         h->glaunch[seg] = h->launches - s0;
-        CK(cudaGraphLaunch(h->gexec[seg], h->stream));
+        const cudaError_t el = ei == cudaSuccess ? cudaGraphLaunch(h->gexec[seg], st) : ei;
+        h->stream = main_stream;
+        CK(el);
+        if (timed && seg == 4) CK(cudaEventRecord(h->ev[5], st));
         continue;
       }
       // capture failed (or a buffer moved): finish this call eagerly
@@ -2950,9 +3020,12 @@ int run_eval(ewb_handle *h, const double *d_pos, const double *d_q, int64_t n, d
       captured_all = false;
       h->launches = s0;
     }
-    if ((rc = pipeline_seg(h, seg, d_pos, d_q, n, d_force, d_rho))) return rc;
+    rc = pipeline_seg(h, seg, d_pos, d_q, n, d_force, d_rho);
+    h->stream = main_stream;
+    if (rc) return rc;
+    if (timed && seg == 4) CK(cudaEventRecord(h->ev[5], st));
   }
-  if (timed) CK(cudaEventRecord(h->ev[N_SEG - 1], h->stream));
+  h->stream = main_stream;
   if (replay) {
     for (int seg = 0; seg < N_SEG; ++seg) h->launches += h->glaunch[seg];
     h->n = n;
@@ -2992,10 +3065,12 @@ int stage_rho_to_slots(ewb_handle *h) {
 int read_timings(ewb_handle *h, double *timings) {
   if (!timings) return EWB_OK;
   float a = 0, b = 0, c = 0, d = 0;
+  CK(cudaEventSynchronize(h->ev[5]));
+  CK(cudaEventSynchronize(h->ev[2]));
   CK(cudaEventElapsedTime(&a, h->ev[0], h->ev[1]));
   CK(cudaEventElapsedTime(&b, h->ev[0], h->ev[2]));
-  CK(cudaEventElapsedTime(&c, h->ev[2], h->ev[3]));
-  CK(cudaEventElapsedTime(&d, h->ev[3], h->ev[4]));
+  CK(cudaEventElapsedTime(&c, h->ev[3], h->ev[4]));
+  CK(cudaEventElapsedTime(&d, h->ev[4], h->ev[5]));
   timings[0] = a * 1e-3;
   timings[1] = b * 1e-3;
   timings[2] = c * 1e-3;
@@ -3030,6 +3105,9 @@ int ewb_create(int device, ewb_handle **out) {
   h->stream = h->own_stream;
   if (const char *d = getenv("EWB_TC_DBG")) h->tc_dbg = atoi(d);
   if (cudaStreamCreateWithFlags(&h->aux_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&h->rstream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_rfork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_rjoin, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) {
     delete h;
@@ -3054,13 +3132,16 @@ void ewb_destroy(ewb_handle *h) {
                   &h->errflag, &h->cell_of, &h->slot, &h->count, &h->start, &h->gstart,
                   &h->order_tmp, &h->order, &h->sorted, &h->sorted_cell, &h->row_ustart,
                   &h->sorted_f, &h->tc_qmax, &h->tc_ytab, &h->tc_ztab, &h->tc_xsl, &h->t3_wsl,
-                  &h->t3_rscale, &h->pairc})
+                  &h->t3_rscale, &h->pairc, &h->eblk_r})
     b->release();
   h->plan.release();
   for (auto &ge : h->gexec)
     if (ge) cudaGraphExecDestroy(ge);
   for (auto &ev : h->ev)
     if (ev) cudaEventDestroy(ev);
+  if (h->ev_rfork) cudaEventDestroy(h->ev_rfork);
+  if (h->ev_rjoin) cudaEventDestroy(h->ev_rjoin);
+  if (h->rstream) cudaStreamDestroy(h->rstream);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->aux_stream) cudaStreamDestroy(h->aux_stream);
@@ -3176,6 +3257,13 @@ int ewb_set_tensor_cores(ewb_handle *h, int on) {
   if (!h) return EWB_EINVAL;
   if (on < 0 || on > 2) return h->fail(EWB_EINVAL, "tensor-core mode must be 0, 1 or 2");
   h->use_tc = on;
+  ++h->gen;
+  return EWB_OK;
+}
+
+int ewb_set_overlap(ewb_handle *h, int on) {
+  if (!h) return EWB_EINVAL;
+  h->overlap = on ? 1 : 0;
   ++h->gen;
   return EWB_OK;
 }

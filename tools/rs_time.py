@@ -9,7 +9,8 @@ for name in sys.argv[1:]:
     rs = ew.ReciprocalSpace(cfg['box'], p, cfg['m_int'])
     ps = ew.create_particle_set(cfg['pos'].shape[0], cfg['box'])
     ps.position[:] = cfg['pos']; ps.charge[:] = cfg['q']
-    s = ew.EwaldSolver(cfg['box'], p, recip=rs)
+    s = ew.EwaldSolver(cfg["box"], p, recip=rs)
+    s.handle.set_overlap(False)
     ts = []
     for _ in range(20):
         r = s.evaluate(ps)

@@ -178,6 +178,8 @@ int ewb_probe_fp64_peak(ewb_handle *h, double *tflops);
 int ewb_probe_i8_peak(ewb_handle *h, double *tops);
 /* The same probe for MMA shape M=128, N=n_mma (16..256, multiple of 16). */
 int ewb_probe_i8_shape(ewb_handle *h, int n_mma, double *tops);
+/* The same with the A operand read from tensor memory (TS form). */
+int ewb_probe_i8_shape_ts(ewb_handle *h, int n_mma, double *tops);
 /* Tensor-core plan of the current k-table (for MMA-work accounting):
  * info8 = {enabled, S(k) M tiles, sum of padded X columns, force M tiles,
  *          force GEMM K, levels, slice-pair MMAs per K step, max |m_x|}. */

@@ -78,6 +78,7 @@ SIGNATURES = {
     "ewb_probe_fp64_peak": (_INT, [_P, _P]),
     "ewb_probe_i8_peak": (_INT, [_P, _P]),
     "ewb_probe_i8_shape": (_INT, [_P, _INT, _P]),
+    "ewb_probe_i8_shape_ts": (_INT, [_P, _INT, _P]),
     "ewb_tc_info": (_INT, [_P, _P]),
     "ewb_last_pair_count": (_INT, [_P, _P]),
     "ewb_launch_count": (_I64, [_P]),
@@ -268,6 +269,11 @@ class Handle:
     def probe_i8_shape(self, n_mma):
         out = ctypes.c_double(0.0)
         self._check(self.lib.ewb_probe_i8_shape(self.h, int(n_mma), ctypes.byref(out)))
+        return out.value
+
+    def probe_i8_shape_ts(self, n_mma):
+        out = ctypes.c_double(0.0)
+        self._check(self.lib.ewb_probe_i8_shape_ts(self.h, int(n_mma), ctypes.byref(out)))
         return out.value
 
     def tc_info(self):

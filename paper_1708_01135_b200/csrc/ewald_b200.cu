@@ -1675,6 +1675,14 @@ __global__ void __launch_bounds__(256) k_fp64_probe(double *__restrict__ out, in
 
 #include "k1_tc.cuh"
 #include "k3_tc.cuh"
+#include "k3_ts.cuh"
+#ifndef T3_USE_TS
+// force GEMM with the W operand in tensor memory (k3_ts.cuh): correct, but
+// measured slower (c5 120 vs 101 ms): an M=128 int8 MMA costs >= ~48 cycles
+// in either form (tools/i8_shapes.py: TS 3969 vs SS 3503 TOP/s at N=80), and
+// the TS TMEM budget forces N=64
+#define T3_USE_TS 0
+#endif
 
 // ---------------------------------------------------------------------------
 // template dispatch tables
@@ -2488,6 +2496,7 @@ int stage_recip_tc(ewb_handle *h, int64_t i0, int64_t i1, double *d_force) {
   Plan &P = h->plan;
   const int64_t n_local = i1 - i0;
   const int nkb = P.t3_nkb;
+  constexpr int NP = T3_USE_TS ? TS_NP : T3_NP;
   CK(h->t3_wsl.ensure((size_t)P.t3_mtiles * nkb * T3_S * TC_GSL));
   CK(h->t3_rscale.ensure((size_t)P.t3_mtiles * 128 * sizeof(double)));
   {
@@ -2497,12 +2506,19 @@ int stage_recip_tc(ewb_handle *h, int64_t i0, int64_t i1, double *d_force) {
         h->sp.as<double2>(), P.t3_slotmap.as<int>(), P.tc_A, P.t3_pair_yz.as<int2>(), P.t3_npairs,
         P.t3_rowtab.as<T3Row>(), P.t3_rows, h->t3_rscale.as<unsigned long long>());
     CKL();
-    k3t_wprep<<<dim3(P.t3_mtiles * 128, kparts), 256, 0, h->stream>>>(
-        h->sp.as<double2>(), P.t3_slotmap.as<int>(), P.tc_A, P.t3_pair_yz.as<int2>(), P.t3_npairs,
-        P.t3_rowtab.as<T3Row>(), P.t3_rows, nkb, h->t3_rscale.as<double>(), h->t3_wsl.as<uint8_t>());
+    if (T3_USE_TS)
+      k3s_wprep<<<dim3(P.t3_mtiles * 128, kparts), 256, 0, h->stream>>>(
+          h->sp.as<double2>(), P.t3_slotmap.as<int>(), P.tc_A, P.t3_pair_yz.as<int2>(),
+          P.t3_npairs, P.t3_rowtab.as<T3Row>(), P.t3_rows, nkb, h->t3_rscale.as<double>(),
+          h->t3_wsl.as<uint8_t>());
+    else
+      k3t_wprep<<<dim3(P.t3_mtiles * 128, kparts), 256, 0, h->stream>>>(
+          h->sp.as<double2>(), P.t3_slotmap.as<int>(), P.tc_A, P.t3_pair_yz.as<int2>(),
+          P.t3_npairs, P.t3_rowtab.as<T3Row>(), P.t3_rows, nkb, h->t3_rscale.as<double>(),
+          h->t3_wsl.as<uint8_t>());
     CKL();
   }
-  const int64_t ptiles = (n_local + T3_NP - 1) / T3_NP;
+  const int64_t ptiles = (n_local + NP - 1) / NP;
   const int64_t T = ptiles * P.t3_mtiles;
   const int kb_cap = T3_KMAX / TC_KB;
   const int ns_min = std::max(1, (nkb + kb_cap - 1) / kb_cap);
@@ -2521,6 +2537,15 @@ int stage_recip_tc(ewb_handle *h, int64_t i0, int64_t i1, double *d_force) {
   ns = (nkb + kbps - 1) / kbps;
   const int n_ks = ns * P.t3_mtiles;
   CK(h->fpart.ensure((size_t)n_ks * 3 * n_local * sizeof(double)));
+  if (T3_USE_TS) {
+    const size_t smem = (size_t)ts_smem_bytes(P.tc_A);
+    CK(cudaFuncSetAttribute(k3s_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k3s_gemm<<<dim3((unsigned)ptiles, P.t3_mtiles, ns), TS_THREADS, smem, h->stream>>>(
+        h->frac.as<double4>(), h->base.as<double2>(), h->t3_wsl.as<uint8_t>(),
+        h->t3_rscale.as<double>(), P.t3_rowtab.as<T3Row>(), P.t3_rows, P.t3_pair_yz.as<int2>(),
+        nkb, kbps, i0, i1, P.tc_A, P.t3_comp.as<int4>(), h->fpart.as<double>(), h->tc_dbg);
+    CKL();
+  } else {
   const size_t smem = (size_t)t3_smem_bytes();
   CK(cudaFuncSetAttribute(k3t_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   {
@@ -2546,6 +2571,7 @@ int stage_recip_tc(ewb_handle *h, int64_t i0, int64_t i1, double *d_force) {
                           (const int2 *)P.t3_pair_yz.as<int2>(), nkb, kbps, i0, i1, P.tc_A,
                           (const int4 *)P.t3_comp.as<int4>(), h->fpart.as<double>(), h->tc_dbg));
     ++h->launches;
+  }
   }
   if (h->ov_active) {  // the combine adds into forces: after the real-space join
     h->t3_pend_nks = n_ks;
@@ -3598,6 +3624,31 @@ int ewb_probe_i8_shape(ewb_handle *h, int n_mma, double *tops) {
 }
 
 int ewb_probe_i8_peak(ewb_handle *h, double *tops) { return ewb_probe_i8_shape(h, 256, tops); }
+
+int ewb_probe_i8_shape_ts(ewb_handle *h, int n_mma, double *tops) {
+  if (!h || !tops || n_mma < 16 || n_mma > 256 || n_mma % 16) return EWB_EINVAL;
+  CK(cudaSetDevice(h->device));
+  CK(h->eblk2.ensure(64));
+  const int iters = 16384;
+  const unsigned blocks = (unsigned)h->n_sm;
+  const size_t smem = (size_t)32 * TC_SBO;
+  CK(cudaFuncSetAttribute(k_i8_probe_ts, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_i8_probe_ts<<<blocks, 128, smem, h->stream>>>(iters, n_mma, h->eblk2.as<int>());
+  CKL();
+  CK(cudaEventRecord(h->ev[0], h->stream));
+  const int reps = 3;
+  for (int r = 0; r < reps; ++r) {
+    k_i8_probe_ts<<<blocks, 128, smem, h->stream>>>(iters, n_mma, h->eblk2.as<int>());
+    CKL();
+  }
+  CK(cudaEventRecord(h->ev[1], h->stream));
+  CK(cudaEventSynchronize(h->ev[1]));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]));
+  const double ops = 2.0 * 128.0 * n_mma * 32.0 * iters * blocks * reps;
+  *tops = ops / (ms * 1e-3) / 1e12;
+  return EWB_OK;
+}
 
 int ewb_tc_info(const ewb_handle *h, int64_t *info8) {
   if (!h || !info8) return EWB_EINVAL;

@@ -1676,6 +1676,13 @@ __global__ void __launch_bounds__(256) k_fp64_probe(double *__restrict__ out, in
 #include "k1_tc.cuh"
 #include "k3_tc.cuh"
 #include "k3_ts.cuh"
+#include "k3_pair.cuh"
+#ifndef T3_PAIR
+// force GEMM on level-splitting CTA pairs (k3_pair.cuh): correct, measured
+// slower (c5 124 vs 101 ms, c2 0.34 vs 0.19): each SM copies the whole W
+// block for half the MMA work and the pair runs in lock step
+#define T3_PAIR 0
+#endif
 #ifndef T3_USE_TS
 // force GEMM with the W operand in tensor memory (k3_ts.cuh): correct, but
 // measured slower (c5 120 vs 101 ms): an M=128 int8 MMA costs >= ~48 cycles
@@ -2496,7 +2503,9 @@ int stage_recip_tc(ewb_handle *h, int64_t i0, int64_t i1, double *d_force) {
   Plan &P = h->plan;
   const int64_t n_local = i1 - i0;
   const int nkb = P.t3_nkb;
-  constexpr int NP = T3_USE_TS ? TS_NP : T3_NP;
+  const bool pair = T3_PAIR && !T3_USE_TS &&
+                    128 * (P3_HALF + 1) * 8 + P3_HALF * (P.tc_A + 1) * 16 <= p3_smem_bytes();
+  const int NP = pair ? P3_NP : (T3_USE_TS ? TS_NP : T3_NP);
   CK(h->t3_wsl.ensure((size_t)P.t3_mtiles * nkb * T3_S * TC_GSL));
   CK(h->t3_rscale.ensure((size_t)P.t3_mtiles * 128 * sizeof(double)));
   {
@@ -2519,7 +2528,7 @@ int stage_recip_tc(ewb_handle *h, int64_t i0, int64_t i1, double *d_force) {
     CKL();
   }
   const int64_t ptiles = (n_local + NP - 1) / NP;
-  const int64_t T = ptiles * P.t3_mtiles;
+  const int64_t T = ptiles * P.t3_mtiles * (pair ? 2 : 1);  // CTAs per split
   const int kb_cap = T3_KMAX / TC_KB;
   const int ns_min = std::max(1, (nkb + kb_cap - 1) / kb_cap);
   // splits: least (waves x per-CTA work), at least 4 K-blocks per CTA
@@ -2535,9 +2544,32 @@ int stage_recip_tc(ewb_handle *h, int64_t i0, int64_t i1, double *d_force) {
   }
   const int kbps = (nkb + ns - 1) / ns;
   ns = (nkb + kbps - 1) / kbps;
-  const int n_ks = ns * P.t3_mtiles;
+  const int n_ks = ns * P.t3_mtiles * (pair ? 2 : 1);
   CK(h->fpart.ensure((size_t)n_ks * 3 * n_local * sizeof(double)));
-  if (T3_USE_TS) {
+  if (pair) {
+    const size_t smem = (size_t)p3_smem_bytes();
+    CK(cudaFuncSetAttribute(k3p_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)(2 * ptiles), P.t3_mtiles, ns);
+    lc.blockDim = dim3(P3_THREADS);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = h->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&lc, k3p_gemm, (const double4 *)h->frac.as<double4>(),
+                          (const double2 *)h->base.as<double2>(),
+                          (const uint8_t *)h->t3_wsl.as<uint8_t>(),
+                          (const double *)h->t3_rscale.as<double>(),
+                          (const T3Row *)P.t3_rowtab.as<T3Row>(), P.t3_rows,
+                          (const int2 *)P.t3_pair_yz.as<int2>(), nkb, kbps, i0, i1, P.tc_A,
+                          (const int4 *)P.t3_comp.as<int4>(), h->fpart.as<double>(), h->tc_dbg));
+    ++h->launches;
+  } else if (T3_USE_TS) {
     const size_t smem = (size_t)ts_smem_bytes(P.tc_A);
     CK(cudaFuncSetAttribute(k3s_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k3s_gemm<<<dim3((unsigned)ptiles, P.t3_mtiles, ns), TS_THREADS, smem, h->stream>>>(

@@ -1051,8 +1051,17 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
   __shared__ double3 s_f[K6_WARPS][K6_G][32];
   __shared__ double sh[K6_WARPS];
   __shared__ double s_erfcx[ERFCX_NI * ERFCX_NC];
+  // image shift of a pair by its 6-bit code (k_x | k_y << 2 | k_z << 4,
+  // k = 0: -L, 1: 0, 2: +L, 3: unused): one table read instead of six
+  // 64-bit selects per pair
+  __shared__ double4 s_shift[64];
   for (int t = threadIdx.x; t < ERFCX_NI * ERFCX_NC; t += K6_WARPS * 32)
     s_erfcx[t] = c_erfcx_tab[t / ERFCX_NC][t % ERFCX_NC];
+  if (threadIdx.x < 64) {
+    auto sv = [&](int k) { return k == 0 ? -P.L : (k == 2 ? P.L : 0.0); };
+    const int c = threadIdx.x;
+    s_shift[c] = make_double4(sv(c & 3), sv((c >> 2) & 3), sv((c >> 4) & 3), 0.0);
+  }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -1096,9 +1105,10 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
       const int g = (int)(e.y & 15u);
       const double4 pj = sorted[j];
       const double4 pi = s_i[warp][g];
-      dx = __dadd_rn(__dsub_rn(pi.x, pj.x), shift((e.y >> 4) & 3u));
-      dy = __dadd_rn(__dsub_rn(pi.y, pj.y), shift((e.y >> 6) & 3u));
-      dz = __dadd_rn(__dsub_rn(pi.z, pj.z), shift((e.y >> 8) & 3u));
+      const double4 sh = s_shift[(e.y >> 4) & 63u];
+      dx = __dadd_rn(__dsub_rn(pi.x, pj.x), sh.x);
+      dy = __dadd_rn(__dsub_rn(pi.y, pj.y), sh.y);
+      dz = __dadd_rn(__dsub_rn(pi.z, pj.z), sh.z);
       const double r2raw = rs_r2(dx, dy, dz);
       const bool zero = r2raw == 0.0;
       coincident |= zero;

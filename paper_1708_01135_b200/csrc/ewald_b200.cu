@@ -1172,6 +1172,7 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
     auto drain = [&]() {
       __syncwarp();
       int base = 0;
+      accepted += cnt - (cnt & 31);  // entries evaluated now (the rest stays queued)
       for (; cnt - base >= 64; base += 64) round2(base);
       if (cnt - base >= 32) {
         round(base, 32);
@@ -1207,20 +1208,21 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
       const float4 q = ve ? s_q[warp][lane] : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
       const uint32_t qt = ve ? s_qt[warp][lane] : 0u;
       const int j = __float_as_int(q.w);
-      const bool self = (qt & K6_SELF) != 0u;
+      // half-shell own row: only centres g < j - first (j > i); otherwise
+      // every centre except j itself (the full-shell own row holds it)
+      const int jf = j - first;
+      const int glim = !ve ? -1 : ((qt & K6_SELF) != 0u ? jf : K6_G);
+      const uint32_t qtag = qt & ~K6_SELF;
 #pragma unroll
       for (int g = 0; g < K6_G; ++g) {
         if (g < gi) {
           const float4 c = s_cf[warp][g];
           const float dx = c.x - q.x, dy = c.y - q.y, dz = c.z - q.z;
           const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-          const bool acc = ve && (r2 < P.rc2f) && (self ? j > first + g : j != first + g);
+          const bool acc = (r2 < P.rc2f) && (g < glim) && (g != jf);
           const unsigned bal = __ballot_sync(0xffffffffu, acc);
-          if (acc)
-            s_list[warp][cnt + __popc(bal & lt_mask)] =
-                make_uint2((uint32_t)j, (qt & ~K6_SELF) | (uint32_t)g);
+          if (acc) s_list[warp][cnt + __popc(bal & lt_mask)] = make_uint2((uint32_t)j, qtag | (uint32_t)g);
           cnt += __popc(bal);
-          accepted += __popc(bal);
         }
       }
       __syncwarp();
@@ -1270,7 +1272,6 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
               const unsigned bal = __ballot_sync(0xffffffffu, acc);
               if (acc) s_list[warp][cnt + __popc(bal & lt_mask)] = make_uint2((uint32_t)j, tag | (uint32_t)g);
               cnt += __popc(bal);
-              accepted += __popc(bal);
             }
           }
           if (cnt >= 32) drain();
@@ -1385,7 +1386,6 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
               s_list[warp][cnt + __popc(bal & lt_mask)] = make_uint2((uint32_t)j, t);
             }
             cnt += __popc(bal);
-            accepted += __popc(bal);
           }
         }
 #endif
@@ -1455,6 +1455,7 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
     }
     if (qn > 0) process_queue(qn);
     __syncwarp();
+    accepted += cnt;
     if (cnt > 0) round(0, cnt);
     if (coincident) atomicOr(err, ERR_COINCIDENT);
     if (lane == 0 && pair_count) atomicAdd(pair_count, (unsigned long long)accepted);

@@ -190,6 +190,10 @@ int ewb_tc_info(const ewb_handle *h, int64_t *info8);
 int ewb_last_pair_count(ewb_handle *h, int64_t *pairs);
 /* Kernels launched by this handle since creation (evidence counter). */
 int64_t ewb_launch_count(const ewb_handle *h);
+/* Page-locked host memory for arrays the evaluation copies into (e.g.
+ * ReciprocalSpace.rho): device-to-host copies land directly. */
+int ewb_host_alloc(size_t bytes, void **out);
+int ewb_host_free(void *p);
 
 /* ---- harness helper (csrc/workloads.c, separate library) ----
  * int ewb_gen_hardcore_gas(int64_t n, double L, double min_sep,

@@ -82,6 +82,8 @@ SIGNATURES = {
     "ewb_tc_info": (_INT, [_P, _P]),
     "ewb_last_pair_count": (_INT, [_P, _P]),
     "ewb_launch_count": (_I64, [_P]),
+    "ewb_host_alloc": (_INT, [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
+    "ewb_host_free": (_INT, [_P]),
 }
 
 _LIB = None
@@ -107,6 +109,21 @@ def load_library():
 
 def _ptr(a):
     return None if a is None else ctypes.c_void_p(a.ctypes.data)
+
+
+def pinned_zeros(n):
+    """float64 zeros in page-locked host memory (device copies land directly);
+    plain numpy memory when no CUDA device is present."""
+    import weakref
+    n = int(n)
+    lib = load_library()
+    ptr = ctypes.c_void_p()
+    if n < 1 or lib.ewb_host_alloc(n * 8, ctypes.byref(ptr)) != EWB_OK or not ptr.value:
+        return np.zeros(max(n, 0))
+    arr = np.ctypeslib.as_array((ctypes.c_double * n).from_address(ptr.value))
+    arr[:] = 0.0
+    weakref.finalize(arr, lib.ewb_host_free, ctypes.c_void_p(ptr.value))
+    return arr
 
 
 class DeviceError(RuntimeError):

@@ -3505,9 +3505,12 @@ int ewb_evaluate(ewb_handle *h, const double *pos, const double *q, int64_t n,
            h, ((h->coul_on && h->rc > 0.5 * h->L && !h->lj_on) ? 0 : ERR_UNWRAPPED) |
                   ERR_COINCIDENT)))
     return rc;
-  CK(cudaMemcpy(force_inout, h->force.p, n * 3 * sizeof(double), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpyAsync(force_inout, h->force.p, n * 3 * sizeof(double), cudaMemcpyDeviceToHost,
+                     h->stream));
   if (rho_out)
-    CK(cudaMemcpy(rho_out, h->rho.p, 2 * h->plan.K * sizeof(double), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpyAsync(rho_out, h->rho.p, 2 * h->plan.K * sizeof(double), cudaMemcpyDeviceToHost,
+                       h->stream));
+  CK(cudaStreamSynchronize(h->stream));
   if (energies) std::memcpy(energies, en, sizeof en);
   return read_timings(h, timings);
 }
@@ -3718,6 +3721,22 @@ int ewb_last_pair_count(ewb_handle *h, int64_t *pairs) {
   CK(cudaStreamSynchronize(h->stream));
   CK(cudaMemcpy(&v, h->pairc.p, sizeof(v), cudaMemcpyDeviceToHost));
   *pairs = (int64_t)v;
+  return EWB_OK;
+}
+
+int ewb_host_alloc(size_t bytes, void **out) {
+  if (!out) return EWB_EINVAL;
+  *out = nullptr;
+  if (cudaHostAlloc(out, bytes ? bytes : 16, cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    *out = nullptr;
+    return EWB_ECUDA;
+  }
+  return EWB_OK;
+}
+
+int ewb_host_free(void *p) {
+  if (p && cudaFreeHost(p) != cudaSuccess) return EWB_ECUDA;
   return EWB_OK;
 }
 

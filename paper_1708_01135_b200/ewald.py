@@ -132,6 +132,8 @@ class ReciprocalSpace:
         self.m_sign = np.where(m_int < 0, -1.0, 1.0)
         self.mmax = int(self.m_abs.max())
         self.rho = GlobalAccumulator(2 * self.n_stored)
+        # page-locked storage: the device writes rho straight into it
+        self.rho.values = _lib.pinned_zeros(2 * self.n_stored)
         self.dims = np.array([self.n_stored, self.mmax], dtype=np.int64)
         self.phase_step = np.array([2.0 * math.pi / L])
 
@@ -207,13 +209,22 @@ def _force_buffer(ps):
     return np.ascontiguousarray(f, dtype=np.float64).reshape(ps.count, 3), True
 
 
+def _writable_f64(a, n):
+    """True if the device can write n doubles straight into a."""
+    return (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous
+            and a.flags.writeable and a.shape == (n,))
+
+
 def compute_rho_hat(ps, rs, workers=None):
     """Fill rs.rho with rho_hat(k) = sum_j q_j exp(-i k.r_j) (Alg. 1)."""
     h = _handle_for(rs)
     pos, q = _particles(ps)
-    out = np.empty(2 * rs.n_stored)
+    rv = rs.rho.values
+    direct = _writable_f64(rv, 2 * rs.n_stored)
+    out = rv if direct else np.empty(2 * rs.n_stored)
     h.compute_rho_hat(pos, q, out)
-    rs.rho.values[:] = out
+    if not direct:
+        rs.rho.values[:] = out
     return rs
 
 
@@ -294,11 +305,14 @@ class EwaldSolver:
         # guards (BoxTooSmallError, OracleSizeError)
         pos, q = _particles(ps)
         f, copied = _force_buffer(ps)
-        rho = np.empty(2 * self.recip.n_stored)
+        rv = self.recip.rho.values
+        direct = _writable_f64(rv, 2 * self.recip.n_stored)
+        rho = rv if direct else np.empty(2 * self.recip.n_stored)
         en, tm = self._h.evaluate(pos, q, f, rho)
         if copied:
             ps.force[:] = f
-        self.recip.rho.values[:] = rho
+        if not direct:
+            self.recip.rho.values[:] = rho
         return EwaldEnergies(float(en[0]), float(en[1]), float(en[2]),
                              t_cell=float(tm[0]), t_sr=float(tm[1]),
                              t_alg1=float(tm[2]), t_alg2=float(tm[3]))

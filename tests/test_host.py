@@ -122,3 +122,12 @@ def test_hardcore_gas_min_separation():
     np.fill_diagonal(r2, np.inf)
     assert r2.min() >= 0.64
     assert pos.min() >= 0.0 and pos.max() < 15.0
+
+
+def test_pinned_zeros_falls_back_to_numpy_without_a_device():
+    from paper_1708_01135_b200 import _lib
+    a = _lib.pinned_zeros(1000)
+    assert a.shape == (1000,) and a.dtype == np.float64 and not a.any()
+    a[:] = 1.5
+    assert float(a.sum()) == 1500.0
+    assert _lib.pinned_zeros(0).shape == (0,)

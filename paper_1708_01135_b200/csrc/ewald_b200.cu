@@ -888,6 +888,19 @@ __global__ void k_iota(int *__restrict__ v, int64_t n) {
   if (i < n) v[i] = (int)i;
 }
 
+// real-space forces, accumulated in cell-sorted order by k6 (partner atomics
+// on neighbouring addresses, no order[] load per pair), added into the
+// caller's order: force[order[p]] += fs[p]
+__global__ void k_unpermute_add(const int *__restrict__ order, const double *__restrict__ fs,
+                                int64_t n, double *__restrict__ force) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int64_t o = order[p];
+  force[3 * o] += fs[3 * p];
+  force[3 * o + 1] += fs[3 * p + 1];
+  force[3 * o + 2] += fs[3 * p + 2];
+}
+
 __global__ void k5_gather(const int *__restrict__ order, const double4 *__restrict__ xyzq,
                           const int *__restrict__ cell_of, int64_t n,
                           double4 *__restrict__ sorted, float4 *__restrict__ sorted_f,
@@ -1144,10 +1157,10 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
       f.z = fma(gg, dz, f.z);
       s_f[warp][g][lane] = f;
       if (P.half) {  // F_j = -F_i for the same pair (r2 is symmetric bitwise)
-        const int64_t o = order[e.x];
-        atomicAdd(force + 3 * o, -gg * dx);
-        atomicAdd(force + 3 * o + 1, -gg * dy);
-        atomicAdd(force + 3 * o + 2, -gg * dz);
+        double *fj = force + 3 * (int64_t)e.x;  // cell-sorted accumulator
+        atomicAdd(fj, -gg * dx);
+        atomicAdd(fj + 1, -gg * dy);
+        atomicAdd(fj + 2, -gg * dz);
       }
     };
     // evaluate entries [base, base+n) (n <= 32): lane l takes entry base+l
@@ -1464,7 +1477,7 @@ __global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
       const double3 f = s_f[warp][g][lane];
       const double ax = warp_sum(f.x), ay = warp_sum(f.y), az = warp_sum(f.z);
       if (lane == 0) {
-        const int64_t o = order[first + g];
+        const int64_t o = first + g;  // cell-sorted accumulator
         if (P.half) {  // other warps scatter partner forces into this row
           atomicAdd(force + 3 * o, ax);
           atomicAdd(force + 3 * o + 1, ay);
@@ -1852,6 +1865,7 @@ struct ewb_handle {
   DBuf t3_wsl, t3_rscale;
   DBuf pairc;  // in-cutoff pairs visited by the last real-space pass
   DBuf eblk_r;  // energy scratch of the reciprocal stages (own stream)
+  DBuf fsorted;  // real-space forces in cell-sorted order
   void *tc_spart_zeroed = nullptr;  // spart buffer whose unmapped slots were zeroed
   int64_t launches = 0;
   // system
@@ -2891,16 +2905,21 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
   }
   CK(h->pairc.ensure(sizeof(unsigned long long)));
   if (part == 0) CK(cudaMemsetAsync(h->pairc.p, 0, sizeof(unsigned long long), h->stream));
+  CK(h->fsorted.ensure((size_t)n * 3 * sizeof(double)));
+  CK(cudaMemsetAsync(h->fsorted.p, 0, (size_t)n * 3 * sizeof(double), h->stream));
   if (lj_on)
     k6_real_space<true><<<nb, K6_WARPS * 32, 0, h->stream>>>(
         h->sorted.as<double4>(), h->sorted_f.as<float4>(), h->sorted_cell.as<int>(), h->order.as<int>(), h->start.as<int>(),
-        h->row_ustart.as<int>(), rp, d_force, h->eblk.as<double>(), h->eblk_lj.as<double>(),
-        h->errflag.as<int>(), h->pairc.as<unsigned long long>());
+        h->row_ustart.as<int>(), rp, h->fsorted.as<double>(), h->eblk.as<double>(),
+        h->eblk_lj.as<double>(), h->errflag.as<int>(), h->pairc.as<unsigned long long>());
   else
     k6_real_space<false><<<nb, K6_WARPS * 32, 0, h->stream>>>(
         h->sorted.as<double4>(), h->sorted_f.as<float4>(), h->sorted_cell.as<int>(), h->order.as<int>(), h->start.as<int>(),
-        h->row_ustart.as<int>(), rp, d_force, h->eblk.as<double>(), nullptr,
+        h->row_ustart.as<int>(), rp, h->fsorted.as<double>(), h->eblk.as<double>(), nullptr,
         h->errflag.as<int>(), h->pairc.as<unsigned long long>());
+  CKL();
+  k_unpermute_add<<<blocks_for(n, 256), 256, 0, h->stream>>>(h->order.as<int>(),
+                                                             h->fsorted.as<double>(), n, d_force);
   CKL();
   if (pair_coul) {
     k_sum<<<1, 1024, 0, h->stream>>>(h->eblk.as<double>(), nb, 1.0, d_u_out);
@@ -3201,7 +3220,7 @@ void ewb_destroy(ewb_handle *h) {
                   &h->errflag, &h->cell_of, &h->slot, &h->count, &h->start, &h->gstart,
                   &h->order_tmp, &h->order, &h->sorted, &h->sorted_cell, &h->row_ustart,
                   &h->sorted_f, &h->tc_qmax, &h->tc_ytab, &h->tc_ztab, &h->tc_xsl, &h->t3_wsl,
-                  &h->t3_rscale, &h->pairc, &h->eblk_r})
+                  &h->t3_rscale, &h->pairc, &h->eblk_r, &h->fsorted})
     b->release();
   h->plan.release();
   for (auto &ge : h->gexec)

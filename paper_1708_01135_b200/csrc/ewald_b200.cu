@@ -1852,6 +1852,13 @@ struct ewb_handle {
   int t3_pend_nks = 0;          // deferred k3_combine (overlap mode)
   int64_t t3_pend_i0 = 0, t3_pend_n = 0;
   double *t3_pend_force = nullptr;
+  // host-API copies overlapped with the pipeline (ewb_evaluate): the force
+  // upload is waited for before the pair segment, rho is copied out as soon
+  // as S(k) is final
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t ev_fup = nullptr, ev_rho = nullptr, ev_rhodone = nullptr;
+  bool fup_pending = false;
+  double *rho_host = nullptr;
   cudaEvent_t ev[6] = {};
   std::string err;
   int mcap = 28;   // K3 segment cap
@@ -3067,6 +3074,17 @@ int run_eval(ewb_handle *h, const double *d_pos, const double *d_q, int64_t n, d
       }
       if (seg == 4) CK(cudaEventRecord(h->ev[4], st));
     }
+    if (seg == 2 && h->fup_pending) {  // forces are first touched by the pair segment
+      CK(cudaStreamWaitEvent(st, h->ev_fup, 0));
+      h->fup_pending = false;
+    }
+    if (seg == 4 && h->rho_host && d_rho) {  // rho is final after segment 3
+      CK(cudaEventRecord(h->ev_rho, on_r ? h->rstream : main_stream));
+      CK(cudaStreamWaitEvent(h->cstream, h->ev_rho, 0));
+      CK(cudaMemcpyAsync(h->rho_host, d_rho, 2 * h->plan.K * sizeof(double),
+                         cudaMemcpyDeviceToHost, h->cstream));
+      CK(cudaEventRecord(h->ev_rhodone, h->cstream));
+    }
     h->stream = st;
     if (replay) {
       cudaError_t e = cudaGraphLaunch(h->gexec[seg], st);
@@ -3194,6 +3212,10 @@ int ewb_create(int device, ewb_handle **out) {
   if (const char *d = getenv("EWB_TC_DBG")) h->tc_dbg = atoi(d);
   if (cudaStreamCreateWithFlags(&h->aux_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&h->rstream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_fup, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_rho, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_rhodone, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_rfork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_rjoin, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
@@ -3227,6 +3249,10 @@ void ewb_destroy(ewb_handle *h) {
     if (ge) cudaGraphExecDestroy(ge);
   for (auto &ev : h->ev)
     if (ev) cudaEventDestroy(ev);
+  if (h->ev_fup) cudaEventDestroy(h->ev_fup);
+  if (h->ev_rho) cudaEventDestroy(h->ev_rho);
+  if (h->ev_rhodone) cudaEventDestroy(h->ev_rhodone);
+  if (h->cstream) cudaStreamDestroy(h->cstream);
   if (h->ev_rfork) cudaEventDestroy(h->ev_rfork);
   if (h->ev_rjoin) cudaEventDestroy(h->ev_rjoin);
   if (h->rstream) cudaStreamDestroy(h->rstream);
@@ -3513,23 +3539,38 @@ int ewb_evaluate(ewb_handle *h, const double *pos, const double *q, int64_t n,
   if (!h->coul_on) rho_out = nullptr;
   CK(cudaMemcpyAsync(h->pos.p, pos, n * 3 * sizeof(double), cudaMemcpyHostToDevice, h->stream));
   CK(cudaMemcpyAsync(h->q.p, q, n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  // the force upload overlaps the set-up and cell build (waited for before
+  // the pair segment); the previous call's result copies must be done
+  CK(cudaEventRecord(h->ev_fup, h->stream));
+  CK(cudaStreamWaitEvent(h->cstream, h->ev_fup, 0));
   CK(cudaMemcpyAsync(h->force.p, force_inout, n * 3 * sizeof(double), cudaMemcpyHostToDevice,
-                     h->stream));
-  if ((rc = run_eval(h, h->pos.as<double>(), h->q.as<double>(), n, h->force.as<double>(),
-                     rho_out ? h->rho.as<double>() : nullptr, true)))
+                     h->cstream));
+  CK(cudaEventRecord(h->ev_fup, h->cstream));
+  h->fup_pending = true;
+  h->rho_host = rho_out;
+  rc = run_eval(h, h->pos.as<double>(), h->q.as<double>(), n, h->force.as<double>(),
+                rho_out ? h->rho.as<double>() : nullptr, true);
+  h->rho_host = nullptr;
+  if (h->fup_pending) {  // (not consumed: make the main stream depend on it anyway)
+    CK(cudaStreamWaitEvent(h->stream, h->ev_fup, 0));
+    h->fup_pending = false;
+  }
+  if (rc) {
+    cudaStreamSynchronize(h->cstream);
     return rc;
+  }
   double en[3];
   CK(cudaMemcpyAsync(en, h->energy.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
   if ((rc = check_errflag(
            h, ((h->coul_on && h->rc > 0.5 * h->L && !h->lj_on) ? 0 : ERR_UNWRAPPED) |
-                  ERR_COINCIDENT)))
+                  ERR_COINCIDENT))) {
+    cudaStreamSynchronize(h->cstream);  // no copy into caller memory after we return
     return rc;
+  }
   CK(cudaMemcpyAsync(force_inout, h->force.p, n * 3 * sizeof(double), cudaMemcpyDeviceToHost,
                      h->stream));
-  if (rho_out)
-    CK(cudaMemcpyAsync(rho_out, h->rho.p, 2 * h->plan.K * sizeof(double), cudaMemcpyDeviceToHost,
-                       h->stream));
   CK(cudaStreamSynchronize(h->stream));
+  CK(cudaStreamSynchronize(h->cstream));  // rho (copied after segment 3)
   if (energies) std::memcpy(energies, en, sizeof en);
   return read_timings(h, timings);
 }

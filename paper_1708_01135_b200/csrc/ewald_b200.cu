@@ -2422,8 +2422,8 @@ int stage_rho_tc(ewb_handle *h, int64_t i0, int64_t i1, int *n_part_out) {
   ns = (nkb + kbps - 1) / kbps;
   const int xsl_b = tc_xsl_bytes(P.tc_npad_max);
   CK(h->tc_qmax.ensure(sizeof(double)));
-  CK(h->tc_ytab.ensure((size_t)P.tc_ny * np * sizeof(double2)));
-  CK(h->tc_ztab.ensure((size_t)P.tc_nz * np * sizeof(double2)));
+  CK(h->tc_ytab.ensure(K1_TABLES ? (size_t)P.tc_ny * np * sizeof(double2) : 16));
+  CK(h->tc_ztab.ensure(K1_TABLES ? (size_t)P.tc_nz * np * sizeof(double2) : 16));
   CK(h->tc_xsl.ensure((size_t)P.tc_nchunks * nkb * TC_S * xsl_b));
   CK(h->spart.ensure((size_t)ns * n_pslots * sizeof(double4)));
   if (h->tc_spart_zeroed != h->spart.p) {  // slots no k maps to stay zero
@@ -2437,7 +2437,8 @@ int stage_rho_tc(ewb_handle *h, int64_t i0, int64_t i1, int *n_part_out) {
     CKL();
   }
   k1t_prep<<<dim3((unsigned)((np + 127) / 128),
-                  (P.tc_ny + 7) / 8 + (P.tc_nz + 7) / 8 + P.tc_nchunks * ((P.tc_npad_max + 7) / 8)),
+                  (K1_TABLES ? (P.tc_ny + 7) / 8 + (P.tc_nz + 7) / 8 : 0) +
+                      P.tc_nchunks * ((P.tc_npad_max + 7) / 8)),
              128, 0, h->stream>>>(
       h->frac.as<double4>(), i0, std::max(i0, i1), np, h->tc_qmax.as<double>(), P.tc_ymin, P.tc_ny,
       P.tc_zmin, P.tc_nz, P.tc_chunks.as<TCChunk>(), P.tc_nchunks, P.tc_npad_max,
@@ -2446,8 +2447,9 @@ int stage_rho_tc(ewb_handle *h, int64_t i0, int64_t i1, int *n_part_out) {
   const size_t smem = (size_t)tc_smem_bytes(P.tc_npad_max);
   CK(cudaFuncSetAttribute(k1t_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k1t_gemm<<<dim3(P.tc_mtiles, P.tc_nchunks, (unsigned)ns), TC_NTHREADS, smem, h->stream>>>(
-      h->tc_ytab.as<double2>(), h->tc_ztab.as<double2>(), h->base.as<double2>(),
-      h->tc_xsl.as<uint8_t>(), P.tc_chunks.as<TCChunk>(), P.tc_runs.as<int4>(),
+      h->frac.as<double4>(), h->tc_ytab.as<double2>(), h->tc_ztab.as<double2>(),
+      h->base.as<double2>(), h->tc_xsl.as<uint8_t>(), P.tc_chunks.as<TCChunk>(),
+      P.tc_runs.as<int4>(),
       P.tc_map.as<int2>(), h->tc_qmax.as<double>(), i0, std::max(i0, i1), np, kbps * TC_KB,
       P.tc_ymin, P.tc_zmin, P.tc_A, P.tc_npad_max, (int64_t)n_pslots, h->spart.as<double4>(),
       h->tc_dbg);

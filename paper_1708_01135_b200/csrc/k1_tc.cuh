@@ -37,6 +37,12 @@
 //   stage's mbarrier.  Two stages: the MMAs of block k overlap the
 //   production of block k+1.
 
+#ifndef K1_TABLES
+// 1: per-particle m_y / m_z phase tables written by k1t_prep and read by the
+// producers; 0: a sincospi per particle and run in the producers (measured
+// slower: c5 S(k) 70 vs 48.5 ms, the producers are on the critical path)
+#define K1_TABLES 1
+#endif
 constexpr int TC_S = 6;                     // byte slices per operand
 constexpr int TC_W0 = 4;                    // kept levels: w = s + t >= TC_W0
 constexpr int TC_NL = 2 * TC_S - 1 - TC_W0; // 7 levels
@@ -166,7 +172,7 @@ __global__ void __launch_bounds__(128)
              const TCChunk *__restrict__ chunks, int n_chunks, int npad_max,
              double2 *__restrict__ ytab, double2 *__restrict__ ztab, uint8_t *__restrict__ xsl) {
   const int task = blockIdx.y;
-  const int nyt = (ny + 7) / 8, nzt = (nz + 7) / 8;
+  const int nyt = K1_TABLES ? (ny + 7) / 8 : 0, nzt = K1_TABLES ? (nz + 7) / 8 : 0;
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (task < nyt + nzt) {
     const int64_t j = t;
@@ -288,7 +294,8 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
 }
 
 __global__ void __launch_bounds__(TC_NTHREADS, 1)
-    k1t_gemm(const double2 *__restrict__ ytab, const double2 *__restrict__ ztab,
+    k1t_gemm(const double4 *__restrict__ frac, const double2 *__restrict__ ytab,
+             const double2 *__restrict__ ztab,
              const double2 *__restrict__ base, const uint8_t *__restrict__ xsl,
              const TCChunk *__restrict__ chunks, const int4 *__restrict__ runs,
              const int2 *__restrict__ tmap, const double *__restrict__ qmax_p, int64_t p_begin,
@@ -402,6 +409,7 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
     const int kin = pc * 16 + qd * 4;  // particle offset in the K-block
     const int myl = run.y + 4 * ph;
     const bool active = 4 * ph < run.z;  // rows of this half exist in the run
+    const double inv_qmax = 1.0 / fmax(*qmax_p, 1e-300);
     for (int it = 0; it < nkb; ++it) {
       const int gs = it % TC_GS;
       uint8_t *sb = gbuf + gs * TC_S * TC_GSL;
@@ -411,6 +419,7 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
         double2 cur[4], e1[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
+#if K1_TABLES
           if (active) {
             const double2 yv = ytab[(int64_t)(myl - ymin) * np + j + u];
             const double2 zv = ztab[(int64_t)(run.x - zmin) * np + j + u];
@@ -419,6 +428,21 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
           } else {
             cur[u] = e1[u] = make_double2(0.0, 0.0);
           }
+#else
+          // run start (q/qmax) e^{-i 2pi (m_y0 f_y + m_z f_z)} straight from the
+          // particle (no per-particle tables), then the m_y recurrence
+          const int64_t jj = p_begin + j + u;
+          if (active && jj < p_end) {
+            const double4 fp = frac[jj];
+            double sn, cs;
+            sincospi(2.0 * fma((double)myl, fp.y, (double)run.x * fp.z), &sn, &cs);
+            const double sc = fp.w * inv_qmax;
+            cur[u] = make_double2(sc * cs, -sc * sn);
+            e1[u] = base[3 * jj + 1];
+          } else {
+            cur[u] = e1[u] = make_double2(0.0, 0.0);
+          }
+#endif
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {

@@ -2709,6 +2709,13 @@ int stage_recip_forces(ewb_handle *h, int64_t i0, int64_t i1, double *d_force, b
     // join
     CK(cudaEventRecord(h->ev_join, h->aux_stream));
     CK(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
+    if (h->ov_active && !energy) {  // the combine adds into forces: after the real-space join
+      h->t3_pend_nks = 2;
+      h->t3_pend_i0 = i0;
+      h->t3_pend_n = n_local;
+      h->t3_pend_force = d_force;
+      return EWB_OK;
+    }
     if (energy) CK(h->eblk2.ensure(nbc * sizeof(double)));
     k3_combine<<<nbc, RED_THREADS, 0, h->stream>>>(
         h->fpart.as<double>(), energy ? h->upart.as<double>() : nullptr, 2, i0, n_local,
@@ -2737,6 +2744,13 @@ int stage_recip_forces(ewb_handle *h, int64_t i0, int64_t i1, double *d_force, b
                                          h->sp.as<double2>(), P.n_items, h->fpart.as<double>(),
                                          energy ? h->upart.as<double>() : nullptr);
   CKL();
+  if (h->ov_active && !energy) {  // the combine adds into forces: after the real-space join
+    h->t3_pend_nks = n_ks;
+    h->t3_pend_i0 = i0;
+    h->t3_pend_n = n_local;
+    h->t3_pend_force = d_force;
+    return EWB_OK;
+  }
   const unsigned nb = blocks_for(n_local, RED_THREADS);
   if (energy) CK(h->eblk2.ensure(nb * sizeof(double)));
   k3_combine<<<nb, RED_THREADS, 0, h->stream>>>(
@@ -3043,15 +3057,13 @@ int run_eval(ewb_handle *h, const double *d_pos, const double *d_q, int64_t n, d
   int rc = EWB_OK;
   bool captured_all = capture;
   // reciprocal space (segments 3, 4) on its own stream, concurrently with
-  // real space (1, 2), when both reciprocal stages run on the tensor cores
-  // (their kernels touch neither the forces nor the real-space scratch; the
-  // force combine waits for the join in segment 5)
+  // real space (1, 2): its kernels touch neither the forces nor the
+  // real-space scratch; the force combine waits for the join in segment 5
   struct OvGuard {  // the stage APIs must never see a deferred combine
     ewb_handle *h;
     ~OvGuard() { h->ov_active = false; }
   } ov_guard{h};
-  h->ov_active = h->overlap && h->coul_on && !h->lj_on && h->plan.tc_ok && h->plan.t3_ok &&
-                 tc_wanted(h, n);
+  h->ov_active = h->overlap && h->coul_on && !h->lj_on;
   h->t3_pend_nks = 0;
   cudaStream_t main_stream = h->stream;
   for (int seg = 0; seg < N_SEG; ++seg) {

@@ -2,29 +2,22 @@
 //
 // Hot path of arXiv 1708.01135 as restated by the reference package ewaldmd
 // (/root/reference/pkg/src/ewaldmd).  See include/ewald_b200.h for the C-ABI
-// and DESIGN.md for the data layout and rooflines.  Kernels:
+// and DESIGN.md for the data layout and rooflines.  This file holds the
+// per-particle set-up kernels, the k-space planner, the evaluation pipeline
+// (two streams, CUDA graphs) and the C-ABI; the kernels live in:
 //
-//   k_prep            fractional coordinates t = r/L, per-axis base phases
-//                     e^{-i 2 pi t}, wrap check                (O(N), HBM)
-//   k1_structure_factor  Alg. 1 (ewald.py:281-305): S(k) = sum_j q_j e^{-ik.r_j}
-//                     thread = one k-column segment (registers hold M
-//                     accumulators), particles streamed through shared-memory
-//                     phase tables; phases along m_z by the three-term
-//                     recurrence A_{m+1} = 2cos(theta_z) A_m - A_{m-1}
-//                     (4 FP64 instructions per particle.k pair)
-//   k2_finalize       reduce particle-chunk partials, scatter rho_hat to the
-//                     caller's k order, C_k*S_k for the gather, u_lr=sum C|S|^2
-//   k3_force_gather   Alg. 2 (ewald.py:308-349): thread = particle, k-slots
-//                     broadcast from shared memory; F_i = q_i 4pi/L sum_k m_k
-//                     Im(e^{ik.r_i} C_k S_k) with the m_z weight folded into a
-//                     running-sum identity (5 FP64 instructions per pair)
-//   k4/k5*            counting-sort binning into reference-sized cells
-//                     (celllist.py:75-108), deterministic in-cell order
-//   k6_real_space     ordered-pair erfc loop (ewald.py:208-221,
-//                     engine.py:102-159) with per-lane compaction queues so
-//                     erfc/exp run warp-converged; cutoff predicate
-//                     bit-identical to the reference (no FMA contraction)
-//   k7_sum_q2         self energy (ewald.py:482-484)
+//   k1_tc.cuh       Alg. 1 (ewald.py:281-305) S(k) as an int8 tensor-core GEMM
+//                   (tcgen05.mma kind::i8, six 48-bit slices, TMEM levels)
+//   k3_tc.cuh       Alg. 2 (ewald.py:308-349) reciprocal forces as an int8 GEMM
+//                   (W = C S rows x YZ phases, X(a) contraction in the epilogue)
+//   k3_ts.cuh, k3_pair.cuh   measured alternatives of the force GEMM (off)
+//   recip_fp64.cuh  Alg. 1/2 on the FP64 pipe (small systems, tensor cores off,
+//                   per-particle energies of the foreign-rho API)
+//   rs_cells.cuh    cell list (celllist.py:75-108), deterministic in-cell order
+//   rs_pairs.cuh    real-space pair kernel (ewald.py:208-221, engine.py:102-159):
+//                   FP32 box/centre prefilter, exact FP64 predicate, erfc via
+//                   exp x erfcx table, half shell with cell-sorted atomics;
+//                   image-shell kernel for r_c > L/2 (ewald.py:490-576)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -139,272 +132,8 @@ __global__ void k_prep(const double *__restrict__ pos, const double *__restrict_
   base[3 * i + 2] = make_double2(c, -s);
 }
 
-// K1 inner loop for G particles at once (G independent recurrence chains).
-// One pair item = the z-segments of (+|m_x|, m_y) and (-|m_x|, m_y): with
-// YZ_m = q e^{-i(m_y th_y + m_z th_z)} (three-term recurrence along m_z),
-// A+[m] += 2cos(m_x th_x) YZ_m and A-[m] += 2sin(m_x th_x) YZ_m, so that
-// S(+-m_x) = (A+ -+ i A-)/2: 6 FP64 instructions per two k-vectors.
-template <int M, int G>
-__device__ __forceinline__ void k1_accumulate(double2 (&ap)[M], double2 (&am)[M],
-                                              const double2 *t, int TSp, int4 it, int eidx) {
-  double2 bp[G], bc[G];
-  double c2[G], cx[G], sx[G];
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    const double2 *tg = t + g * TSp;
-    const double2 e = tg[eidx];
-    const double2 x = tg[it.z];  // 2 e^{-i |m_x| th_x}
-    cx[g] = x.x;
-    sx[g] = -x.y;
-    bp[g] = cmul(tg[it.x], tg[it.y]);  // m = 0: q e^{-i s th_z} e^{-i m_y th_y}
-    bc[g] = cmul(bp[g], e);            // m = 1
-    c2[g] = e.x + e.x;                 // 2 cos(theta_z)
-  }
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    ap[0].x = fma(cx[g], bp[g].x, ap[0].x);
-    ap[0].y = fma(cx[g], bp[g].y, ap[0].y);
-    am[0].x = fma(sx[g], bp[g].x, am[0].x);
-    am[0].y = fma(sx[g], bp[g].y, am[0].y);
-    if (M > 1) {
-      ap[1].x = fma(cx[g], bc[g].x, ap[1].x);
-      ap[1].y = fma(cx[g], bc[g].y, ap[1].y);
-      am[1].x = fma(sx[g], bc[g].x, am[1].x);
-      am[1].y = fma(sx[g], bc[g].y, am[1].y);
-    }
-  }
-#pragma unroll
-  for (int m = 2; m < M; ++m) {
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const double2 bn = make_double2(fma(c2[g], bc[g].x, -bp[g].x), fma(c2[g], bc[g].y, -bp[g].y));
-      bp[g] = bc[g];
-      bc[g] = bn;
-      ap[m].x = fma(cx[g], bn.x, ap[m].x);
-      ap[m].y = fma(cx[g], bn.y, ap[m].y);
-      am[m].x = fma(sx[g], bn.x, am[m].x);
-      am[m].y = fma(sx[g], bn.y, am[m].y);
-    }
-  }
-}
+#include "recip_fp64.cuh"
 
-// ---------------------------------------------------------------------------
-// K1: structure factor.  Block = (k-tile of K1_THREADS items, particle chunk).
-template <int M>
-__global__ void __launch_bounds__(K1_THREADS)
-    k1_structure_factor(const double4 *__restrict__ frac, const double2 *__restrict__ base,
-                        int64_t p_begin, int64_t p_end, int64_t ppb, int pchunk,
-                        const int4 *__restrict__ item_tab, int n_items,
-                        const int4 *__restrict__ tab_desc, const int *__restrict__ tile_off,
-                        const int *__restrict__ tile_ts, double4 *__restrict__ spart) {
-  extern __shared__ double2 tab[];
-  const int tile = blockIdx.x;
-  const int item = tile * K1_THREADS + threadIdx.x;
-  const bool valid = item < n_items;
-  const int4 it = item_tab[valid ? item : n_items - 1];
-  const int TS = tile_ts[tile];
-  const int4 *desc = tab_desc + tile_off[tile];
-  const int eidx = TS - 1;
-
-  double2 ap[M], am[M];
-#pragma unroll
-  for (int m = 0; m < M; ++m) ap[m] = am[m] = make_double2(0.0, 0.0);
-
-  const int64_t c_begin = p_begin + (int64_t)blockIdx.y * ppb;
-  const int64_t c_end = min(p_end, c_begin + ppb);
-  const int nch = (int)((c_end - c_begin + pchunk - 1) / pchunk);
-  const int TSp = TS | 1;  // odd stride: conflict-free per-particle rows
-  double2 *tabs[2] = {tab, tab + pchunk * TSp};
-  int4 *s_desc = reinterpret_cast<int4 *>(tab + 2 * pchunk * TSp);
-  for (int e = threadIdx.x; e < TS; e += K1_THREADS) s_desc[e] = desc[e];
-  __syncthreads();
-
-  // per-particle phase tables of this tile: rows q e^{-i(mx th_x + s th_z)},
-  // columns e^{-i my th_y}, and e^{-i th_z} (last entry).  The np*TS entries
-  // are split evenly over the block; each thread walks a contiguous run,
-  // starting every run (and every unlinked entry) with one sincospi and
-  // extending it by complex multiplication with the particle's axis phase.
-  auto build = [&](const int k, double2 *dst) {
-    const int64_t c0 = c_begin + (int64_t)k * pchunk;
-    const int np = (int)min((int64_t)pchunk, c_end - c0);
-    const int total = np * TS;
-    const int per = (total + K1_THREADS - 1) / K1_THREADS;
-    int t = threadIdx.x * per;
-    const int t1 = min(total, t + per);
-    if (t >= t1) return;
-    int p = t / TS, e = t - p * TS;
-    double4 f = frac[c0 + p];
-    double2 bx = base[3 * (c0 + p)], by = base[3 * (c0 + p) + 1];
-    double2 prev = make_double2(1.0, 0.0);
-    bool fresh = true;
-    for (; t < t1; ++t) {
-      if (e == TS) {
-        e = 0;
-        ++p;
-        f = frac[c0 + p];
-        bx = base[3 * (c0 + p)];
-        by = base[3 * (c0 + p) + 1];
-        fresh = true;
-      }
-      const int4 d = s_desc[e];
-      double2 v;
-      if (fresh || !(d.w & TF_LINK)) {
-        const double arg = (double)d.x * f.x + (double)d.y * f.y + (double)d.z * f.z;
-        double sn, cs;
-        sincospi(2.0 * arg, &sn, &cs);
-        v = make_double2(cs, -sn);
-        const double sc = (d.w & TF_QSCALE) ? f.w : ((d.w & TF_SCALE2) ? 2.0 : 1.0);
-        v.x *= sc;
-        v.y *= sc;
-      } else {
-        v = cmul(prev, ((d.w >> 2) & 3) ? by : bx);
-      }
-      dst[p * TSp + e] = v;
-      prev = v;
-      fresh = false;
-      ++e;
-    }
-  };
-
-  if (nch > 0) build(0, tabs[0]);
-  __syncthreads();
-  for (int k = 0; k < nch; ++k) {
-    // the next chunk's table is built by the same warps while (or before)
-    // they consume this one; warps that finish early start computing, so the
-    // latency-bound build overlaps other warps' FP64 work
-    if (k + 1 < nch) build(k + 1, tabs[(k + 1) & 1]);
-    const double2 *tab_k = tabs[k & 1];
-    const int np = (int)min((int64_t)pchunk, c_end - (c_begin + (int64_t)k * pchunk));
-    int p = 0;
-    for (; p + K1_ILP <= np; p += K1_ILP)
-      k1_accumulate<M, K1_ILP>(ap, am, tab_k + p * TSp, TSp, it, eidx);
-    for (; p < np; ++p) k1_accumulate<M, 1>(ap, am, tab_k + p * TSp, TSp, it, eidx);
-    __syncthreads();
-  }
-  if (valid) {
-    double4 *out = spart + (size_t)blockIdx.y * M * n_items + item;
-#pragma unroll
-    for (int m = 0; m < M; ++m)
-      out[(size_t)m * n_items] = make_double4(ap[m].x, ap[m].y, am[m].x, am[m].y);
-  }
-}
-
-// K2: reduce particle-chunk partials; optionally finalize (rho scatter,
-// C*S for the gather, energy partials).
-__global__ void __launch_bounds__(RED_THREADS)
-    k2_finalize(const double2 *__restrict__ spart, int n_part, int64_t n_slots,
-                const int *__restrict__ slot_k, const double *__restrict__ slot_coeff, int64_t K,
-                double *__restrict__ rho_out, double2 *__restrict__ s_out,
-                double2 *__restrict__ sp, double *__restrict__ epart, int finalize) {
-  __shared__ double sh[RED_THREADS / 32];
-  const int64_t s = blockIdx.x * (int64_t)RED_THREADS + threadIdx.x;
-  double e = 0.0;
-  if (s < n_slots) {
-    double2 S = make_double2(0.0, 0.0);
-    int pc = 0;
-    for (; pc + 8 <= n_part; pc += 8) {  // 8 independent loads in flight
-      double2 v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = __ldcs(spart + (size_t)(pc + u) * n_slots + s);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        S.x += v[u].x;
-        S.y += v[u].y;
-      }
-    }
-    for (; pc < n_part; ++pc) {
-      const double2 v = __ldcs(spart + (size_t)pc * n_slots + s);
-      S.x += v.x;
-      S.y += v.y;
-    }
-    if (s_out) s_out[s] = S;
-    if (finalize) {
-      const int k = slot_k[s];
-      if (k >= 0) {
-        if (rho_out) {
-          rho_out[k] = S.x;
-          rho_out[K + k] = S.y;
-        }
-        const double C = slot_coeff[s];
-        sp[s] = make_double2(C * S.x, C * S.y);
-        e = C * (S.x * S.x + S.y * S.y);
-      } else {
-        sp[s] = make_double2(0.0, 0.0);
-      }
-    }
-  }
-  if (finalize) {
-    const double b = block_sum<RED_THREADS>(e, sh);
-    if (threadIdx.x == 0) epart[blockIdx.x] = b;
-  }
-}
-
-// K2 for the K1 pair layout: sum particle-chunk partials (A+, A-) of a pair
-// slot, S(+-m_x) = (A+ -+ i A-)/2, scatter rho to the caller's k order, C*S to
-// the gather's slot layout, and u_lr partials.  finalize=0: only the summed
-// pair slots (multi-GPU partial S before the all-reduce).
-__global__ void __launch_bounds__(RED_THREADS)
-    k2p_finalize(const double4 *__restrict__ spart, int n_part, int64_t n_pslots,
-                 const int4 *__restrict__ pmap, const double *__restrict__ slot_coeff, int64_t K,
-                 double *__restrict__ rho_out, double4 *__restrict__ s_out,
-                 double2 *__restrict__ sp, double *__restrict__ epart, int finalize) {
-  __shared__ double sh[RED_THREADS / 32];
-  const int64_t s = blockIdx.x * (int64_t)RED_THREADS + threadIdx.x;
-  double e = 0.0;
-  if (s < n_pslots) {
-    double4 A = make_double4(0.0, 0.0, 0.0, 0.0);
-    int pc = 0;
-    for (; pc + 8 <= n_part; pc += 8) {
-      double4 v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = ldcs4(spart + (size_t)(pc + u) * n_pslots + s);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        A.x += v[u].x;
-        A.y += v[u].y;
-        A.z += v[u].z;
-        A.w += v[u].w;
-      }
-    }
-    for (; pc < n_part; ++pc) {
-      const double4 v = ldcs4(spart + (size_t)pc * n_pslots + s);
-      A.x += v.x;
-      A.y += v.y;
-      A.z += v.z;
-      A.w += v.w;
-    }
-    if (s_out) s_out[s] = A;
-    if (finalize) {
-      const int4 mp = pmap[s];
-      const double2 Sp_ = make_double2(0.5 * (A.x + A.w), 0.5 * (A.y - A.z));  // +m_x
-      const double2 Sm_ = make_double2(0.5 * (A.x - A.w), 0.5 * (A.y + A.z));  // -m_x
-      if (mp.x >= 0) {
-        if (rho_out) {
-          rho_out[mp.x] = Sp_.x;
-          rho_out[K + mp.x] = Sp_.y;
-        }
-        const double C = slot_coeff[mp.z];
-        sp[mp.z] = make_double2(C * Sp_.x, C * Sp_.y);
-        e += C * (Sp_.x * Sp_.x + Sp_.y * Sp_.y);
-      }
-      if (mp.y >= 0) {
-        if (rho_out) {
-          rho_out[mp.y] = Sm_.x;
-          rho_out[K + mp.y] = Sm_.y;
-        }
-        const double C = slot_coeff[mp.w];
-        sp[mp.w] = make_double2(C * Sm_.x, C * Sm_.y);
-        e += C * (Sm_.x * Sm_.x + Sm_.y * Sm_.y);
-      }
-    }
-  }
-  if (finalize) {
-    const double b = block_sum<RED_THREADS>(e, sh);
-    if (threadIdx.x == 0) epart[blockIdx.x] = b;
-  }
-}
-
-// Deterministic single-block sum of an array into out[0].
 __global__ void __launch_bounds__(1024) k_sum(const double *__restrict__ v, int64_t n,
                                                double scale, double *__restrict__ out) {
   __shared__ double sh[32];
@@ -414,1206 +143,9 @@ __global__ void __launch_bounds__(1024) k_sum(const double *__restrict__ v, int6
   if (threadIdx.x == 0) *out = scale * r;
 }
 
-// ---------------------------------------------------------------------------
-// K3: reciprocal force gather.  Block = (K3_THREADS*K3_PPT particles, k-split).
-__device__ __forceinline__ double2 phase_plus(int mx, int my, int s, double tx, double ty,
-                                              double tz) {
-  const double arg = (double)mx * tx + (double)my * ty + (double)s * tz;
-  double sn, cs;
-  sincospi(2.0 * arg, &sn, &cs);
-  return make_double2(cs, sn);
-}
+#include "rs_cells.cuh"
 
-#ifndef K3_MINB
-#define K3_MINB 4
-#endif
-template <int M, bool ENERGY>
-__global__ void __launch_bounds__(K3_THREADS, K3_MINB)
-    k3_force_gather(const double4 *__restrict__ frac, const double2 *__restrict__ base,
-                    int64_t p_begin, int64_t p_end, const int4 *__restrict__ rows,
-                    const int *__restrict__ ks_rows, const int *__restrict__ item_my,
-                    const int *__restrict__ item_row, const double2 *__restrict__ sp, int n_items,
-                    double *__restrict__ fpart, double *__restrict__ upart) {
-  __shared__ double2 s_spb[2][K3_CH * M];
-  __shared__ int s_myb[2][K3_CH];
-  __shared__ int s_rowb[2][K3_CH];
-  const int64_t n_local = p_end - p_begin;
-  const int ks = blockIdx.y;
-  const int r_begin = ks_rows[ks], r_end = ks_rows[ks + 1];
-
-  int64_t pi[K3_PPT];
-  double tx[K3_PPT], ty[K3_PPT], tz[K3_PPT], c2z[K3_PPT];
-  double2 ey[K3_PPT], ez[K3_PPT], P[K3_PPT];
-  double Fx[K3_PPT], Fy[K3_PPT], Fz[K3_PPT], U[K3_PPT], SG[K3_PPT], SY[K3_PPT], SH[K3_PPT];
-#pragma unroll
-  for (int q = 0; q < K3_PPT; ++q) {
-    pi[q] = (int64_t)blockIdx.x * (K3_THREADS * K3_PPT) + q * K3_THREADS + threadIdx.x;
-    const int64_t g = p_begin + (pi[q] < n_local ? pi[q] : 0);
-    const double4 f = frac[g];
-    tx[q] = f.x;
-    ty[q] = f.y;
-    tz[q] = f.z;
-    const double2 by = base[3 * g + 1], bz = base[3 * g + 2];
-    ey[q] = make_double2(by.x, -by.y);
-    ez[q] = make_double2(bz.x, -bz.y);
-    c2z[q] = bz.x + bz.x;
-    Fx[q] = Fy[q] = Fz[q] = U[q] = SG[q] = SY[q] = SH[q] = 0.0;
-    P[q] = make_double2(1.0, 0.0);
-  }
-
-  int cur_row = -1, pmy = 0, cmx = 0, cs = 0;
-  if (r_begin < r_end) {
-    const int i_first = rows[r_begin].z;
-    const int4 rl = rows[r_end - 1];
-    const int i_last = rl.z + rl.w;
-    // C_k S_k chunks are double-buffered through registers: chunk k+1 is
-    // fetched from L2 before chunk k is consumed and stored after it
-    constexpr int NPT = (K3_CH * M + K3_THREADS - 1) / K3_THREADS;
-    double2 stage_sp[NPT];
-    int stage_my = 0, stage_row = 0;
-    auto fetch = [&](const int c0) {
-      const int nc = min(K3_CH, i_last - c0);
-#pragma unroll
-      for (int u = 0; u < NPT; ++u) {
-        const int t = threadIdx.x + u * K3_THREADS;
-        if (t < nc * M) stage_sp[u] = sp[(size_t)c0 * M + t];
-      }
-      if (threadIdx.x < nc) {
-        stage_my = item_my[c0 + threadIdx.x];
-        stage_row = item_row[c0 + threadIdx.x];
-      }
-    };
-    auto commit = [&](const int c0, const int b) {
-      const int nc = min(K3_CH, i_last - c0);
-#pragma unroll
-      for (int u = 0; u < NPT; ++u) {
-        const int t = threadIdx.x + u * K3_THREADS;
-        if (t < nc * M) s_spb[b][t] = stage_sp[u];
-      }
-      if (threadIdx.x < nc) {
-        s_myb[b][threadIdx.x] = stage_my;
-        s_rowb[b][threadIdx.x] = stage_row;
-      }
-    };
-    fetch(i_first);
-    commit(i_first, 0);
-    __syncthreads();
-    int kb = 0;
-    for (int c0 = i_first; c0 < i_last; c0 += K3_CH, kb ^= 1) {
-      const int nc = min(K3_CH, i_last - c0);
-      const bool more = c0 + K3_CH < i_last;
-      if (more) fetch(c0 + K3_CH);
-      const double2 *s_sp = s_spb[kb];
-      const int *s_my = s_myb[kb];
-      const int *s_row = s_rowb[kb];
-      for (int itc = 0; itc < nc; ++itc) {
-        const int row = s_row[itc], my = s_my[itc];
-        if (row != cur_row) {
-          if (cur_row >= 0) {
-#pragma unroll
-            for (int q = 0; q < K3_PPT; ++q) {
-              Fx[q] = fma((double)cmx, SG[q], Fx[q]);
-              Fy[q] += SY[q];
-              Fz[q] += fma((double)(cs + M), SG[q], -SH[q]);
-              SG[q] = SY[q] = SH[q] = 0.0;
-            }
-          }
-          const int4 r = rows[row];
-          cmx = r.x;
-          cs = r.y;
-          cur_row = row;
-#pragma unroll
-          for (int q = 0; q < K3_PPT; ++q) P[q] = phase_plus(cmx, my, cs, tx[q], ty[q], tz[q]);
-        } else if (my != pmy + 1) {
-#pragma unroll
-          for (int q = 0; q < K3_PPT; ++q) P[q] = phase_plus(cmx, my, cs, tx[q], ty[q], tz[q]);
-        } else {
-#pragma unroll
-          for (int q = 0; q < K3_PPT; ++q) P[q] = cmul(P[q], ey[q]);
-        }
-        pmy = my;
-        const double2 *spi = s_sp + itc * M;
-        double2 Ap[K3_PPT], Ac[K3_PPT];
-        double G[K3_PPT], H[K3_PPT];
-        {
-          const double2 s0 = spi[0];
-#pragma unroll
-          for (int q = 0; q < K3_PPT; ++q) {
-            Ap[q] = P[q];
-            G[q] = fma(Ap[q].x, s0.y, Ap[q].y * s0.x);
-            H[q] = G[q];
-            if (ENERGY) U[q] = fma(Ap[q].x, s0.x, fma(-Ap[q].y, s0.y, U[q]));
-          }
-        }
-        if (M > 1) {
-          const double2 s1 = spi[1];
-#pragma unroll
-          for (int q = 0; q < K3_PPT; ++q) {
-            Ac[q] = cmul(P[q], ez[q]);
-            G[q] = fma(Ac[q].x, s1.y, fma(Ac[q].y, s1.x, G[q]));
-            H[q] += G[q];
-            if (ENERGY) U[q] = fma(Ac[q].x, s1.x, fma(-Ac[q].y, s1.y, U[q]));
-          }
-#pragma unroll
-          for (int m = 2; m < M; ++m) {
-            const double2 sm = spi[m];
-#pragma unroll
-            for (int q = 0; q < K3_PPT; ++q) {
-              const double2 An = make_double2(fma(c2z[q], Ac[q].x, -Ap[q].x),
-                                              fma(c2z[q], Ac[q].y, -Ap[q].y));
-              Ap[q] = Ac[q];
-              Ac[q] = An;
-              G[q] = fma(An.x, sm.y, fma(An.y, sm.x, G[q]));
-              H[q] += G[q];
-              if (ENERGY) U[q] = fma(An.x, sm.x, fma(-An.y, sm.y, U[q]));
-            }
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < K3_PPT; ++q) {
-          SG[q] += G[q];
-          SY[q] = fma((double)my, G[q], SY[q]);
-          SH[q] += H[q];
-        }
-      }
-      if (more) commit(c0 + K3_CH, kb ^ 1);
-      __syncthreads();
-    }
-    if (cur_row >= 0) {
-#pragma unroll
-      for (int q = 0; q < K3_PPT; ++q) {
-        Fx[q] = fma((double)cmx, SG[q], Fx[q]);
-        Fy[q] += SY[q];
-        Fz[q] += fma((double)(cs + M), SG[q], -SH[q]);
-      }
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < K3_PPT; ++q) {
-    if (pi[q] < n_local) {
-      double *fp = fpart + (size_t)ks * 3 * n_local;
-      fp[pi[q]] = Fx[q];
-      fp[n_local + pi[q]] = Fy[q];
-      fp[2 * n_local + pi[q]] = Fz[q];
-      if (ENERGY) upart[(size_t)ks * n_local + pi[q]] = U[q];
-    }
-  }
-}
-
-// K3c: the force gather with C*S and the item metadata in the CONSTANT bank.
-// Every thread of a warp reads the same C*S entry, so with a warp-uniform
-// constant-bank index the operand lives in uniform registers (LDCU -> DFMA
-// ..., URx, ...), relieving the vector register file, whose operand
-// bandwidth bounds the shared-memory variant (measured: +27% FP64
-// throughput on the K3 inner loop, tools/micro/fp64uniform.cu).  The
-// k-space is walked in chunks of <= K3C_CAP slots, one launch per chunk
-// (copy-to-symbol is stream ordered); partial rows are flushed at chunk
-// ends and forces accumulate across launches.
-// Two buffers (A/B) on two streams: consecutive chunks alternate, so one
-// launch's partial last wave overlaps the next launch.
-constexpr int K3C_CAP = 1700;    // C*S slots per chunk buffer (27.2 KB)
-constexpr int K3C_ITEMS = 160;   // items per chunk (metadata)
-__constant__ double2 c_k3sp[2][K3C_CAP];
-__constant__ int4 c_k3meta[2][K3C_ITEMS];  // (m_x, s, m_y, flags: 1 new row, 2 m_y jump)
-
-template <int M, bool ENERGY, int BUF>
-__global__ void __launch_bounds__(K3_THREADS, K3_MINB)
-    k3c_force_gather(const double4 *__restrict__ frac, const double2 *__restrict__ base,
-                     int64_t p_begin, int64_t p_end, int nc, int first,
-                     double *__restrict__ fpart, double *__restrict__ upart) {
-  const int64_t n_local = p_end - p_begin;
-  int64_t pi[K3_PPT];
-  double tx[K3_PPT], ty[K3_PPT], tz[K3_PPT], c2z[K3_PPT];
-  double2 ey[K3_PPT], ez[K3_PPT], P[K3_PPT];
-  double Fx[K3_PPT], Fy[K3_PPT], Fz[K3_PPT], U[K3_PPT], SG[K3_PPT], SY[K3_PPT], SH[K3_PPT];
-#pragma unroll
-  for (int q = 0; q < K3_PPT; ++q) {
-    pi[q] = (int64_t)blockIdx.x * (K3_THREADS * K3_PPT) + q * K3_THREADS + threadIdx.x;
-    const int64_t g = p_begin + (pi[q] < n_local ? pi[q] : 0);
-    const double4 f = frac[g];
-    tx[q] = f.x;
-    ty[q] = f.y;
-    tz[q] = f.z;
-    const double2 by = base[3 * g + 1], bz = base[3 * g + 2];
-    ey[q] = make_double2(by.x, -by.y);
-    ez[q] = make_double2(bz.x, -bz.y);
-    c2z[q] = bz.x + bz.x;
-    Fx[q] = Fy[q] = Fz[q] = U[q] = SG[q] = SY[q] = SH[q] = 0.0;
-    P[q] = make_double2(1.0, 0.0);
-  }
-  int cmx = 0, cs = 0;
-  for (int itc = 0; itc < nc; ++itc) {
-    const int4 mt = c_k3meta[BUF][itc];
-    const int my = mt.z;
-    if (itc == 0 || (mt.w & 1)) {
-      if (itc > 0) {
-#pragma unroll
-        for (int q = 0; q < K3_PPT; ++q) {
-          Fx[q] = fma((double)cmx, SG[q], Fx[q]);
-          Fy[q] += SY[q];
-          Fz[q] += fma((double)(cs + M), SG[q], -SH[q]);
-          SG[q] = SY[q] = SH[q] = 0.0;
-        }
-      }
-      cmx = mt.x;
-      cs = mt.y;
-#pragma unroll
-      for (int q = 0; q < K3_PPT; ++q) P[q] = phase_plus(cmx, my, cs, tx[q], ty[q], tz[q]);
-    } else if (mt.w & 2) {
-#pragma unroll
-      for (int q = 0; q < K3_PPT; ++q) P[q] = phase_plus(cmx, my, cs, tx[q], ty[q], tz[q]);
-    } else {
-#pragma unroll
-      for (int q = 0; q < K3_PPT; ++q) P[q] = cmul(P[q], ey[q]);
-    }
-    const double2 *spi = c_k3sp[BUF] + itc * M;
-    double2 Ap[K3_PPT], Ac[K3_PPT];
-    double G[K3_PPT], H[K3_PPT];
-    {
-      const double2 s0 = spi[0];
-#pragma unroll
-      for (int q = 0; q < K3_PPT; ++q) {
-        Ap[q] = P[q];
-        G[q] = fma(Ap[q].x, s0.y, Ap[q].y * s0.x);
-        H[q] = G[q];
-        if (ENERGY) U[q] = fma(Ap[q].x, s0.x, fma(-Ap[q].y, s0.y, U[q]));
-      }
-    }
-    if (M > 1) {
-      const double2 s1 = spi[1];
-#pragma unroll
-      for (int q = 0; q < K3_PPT; ++q) {
-        Ac[q] = cmul(P[q], ez[q]);
-        G[q] = fma(Ac[q].x, s1.y, fma(Ac[q].y, s1.x, G[q]));
-        H[q] += G[q];
-        if (ENERGY) U[q] = fma(Ac[q].x, s1.x, fma(-Ac[q].y, s1.y, U[q]));
-      }
-#pragma unroll
-      for (int m = 2; m < M; ++m) {
-        const double2 sm = spi[m];
-#pragma unroll
-        for (int q = 0; q < K3_PPT; ++q) {
-          const double2 An = make_double2(fma(c2z[q], Ac[q].x, -Ap[q].x),
-                                          fma(c2z[q], Ac[q].y, -Ap[q].y));
-          Ap[q] = Ac[q];
-          Ac[q] = An;
-          G[q] = fma(An.x, sm.y, fma(An.y, sm.x, G[q]));
-          H[q] += G[q];
-          if (ENERGY) U[q] = fma(An.x, sm.x, fma(-An.y, sm.y, U[q]));
-        }
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < K3_PPT; ++q) {
-      SG[q] += G[q];
-      SY[q] = fma((double)my, G[q], SY[q]);
-      SH[q] += H[q];
-    }
-  }
-  if (nc > 0) {
-#pragma unroll
-    for (int q = 0; q < K3_PPT; ++q) {
-      Fx[q] = fma((double)cmx, SG[q], Fx[q]);
-      Fy[q] += SY[q];
-      Fz[q] += fma((double)(cs + M), SG[q], -SH[q]);
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < K3_PPT; ++q) {
-    if (pi[q] < n_local) {
-      double *fx = fpart + pi[q], *fy = fpart + n_local + pi[q], *fz = fpart + 2 * n_local + pi[q];
-      if (first) {
-        *fx = Fx[q];
-        *fy = Fy[q];
-        *fz = Fz[q];
-        if (ENERGY) upart[pi[q]] = U[q];
-      } else {
-        *fx += Fx[q];
-        *fy += Fy[q];
-        *fz += Fz[q];
-        if (ENERGY) upart[pi[q]] += U[q];
-      }
-    }
-  }
-}
-
-// Combine k-split partial forces: force[i] += (4 pi / L) q_i sum_ks F.
-__global__ void __launch_bounds__(RED_THREADS)
-    k3_combine(const double *__restrict__ fpart, const double *__restrict__ upart, int n_ks,
-               int64_t p_begin, int64_t n_local, const double4 *__restrict__ frac, double scale,
-               double *__restrict__ force, double *__restrict__ eblk, int energy) {
-  __shared__ double sh[RED_THREADS / 32];
-  const int64_t i = blockIdx.x * (int64_t)RED_THREADS + threadIdx.x;
-  double e = 0.0;
-  if (i < n_local) {
-    double fx = 0.0, fy = 0.0, fz = 0.0, u = 0.0;
-#pragma unroll 4
-    for (int ks = 0; ks < n_ks; ++ks) {
-      const double *fp = fpart + (size_t)ks * 3 * n_local;
-      fx += __ldcs(fp + i);
-      fy += __ldcs(fp + n_local + i);
-      fz += __ldcs(fp + 2 * n_local + i);
-      if (energy) u += upart[(size_t)ks * n_local + i];
-    }
-    const int64_t g = p_begin + i;
-    const double qi = frac[g].w;
-    const double sq = scale * qi;
-    force[3 * g] += sq * fx;
-    force[3 * g + 1] += sq * fy;
-    force[3 * g + 2] += sq * fz;
-    e = qi * u;
-  }
-  if (energy) {
-    const double b = block_sum<RED_THREADS>(e, sh);
-    if (threadIdx.x == 0) eblk[blockIdx.x] = b;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Real space: counting-sort binning (celllist.py:75-108)
-__global__ void k4_bin_count(const double4 *__restrict__ xyzq, int64_t n, double edge, int cpd,
-                             int *__restrict__ cell_of, int *__restrict__ slot,
-                             int *__restrict__ count) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const double4 p = xyzq[i];
-  int c = 0;
-  if (cpd > 1) {
-    const double v[3] = {p.x, p.y, p.z};
-    int id[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      const double f = floor(v[a] / edge);
-      int k = (f >= 0.0) ? (f < (double)cpd ? (int)f : cpd - 1) : 0;  // NaN -> 0
-      id[a] = k;
-    }
-    c = id[0] + cpd * (id[1] + cpd * id[2]);
-  }
-  cell_of[i] = c;
-  slot[i] = atomicAdd(count + c, 1);
-}
-
-// Single-block exclusive scans of cell counts (start) and K6_G-groups (gstart).
-__global__ void __launch_bounds__(1024) k_scan_cells(const int *__restrict__ count, int n_cells,
-                                                     int *__restrict__ start,
-                                                     int *__restrict__ gstart) {
-  __shared__ int wa[32], wb[32];
-  __shared__ int carry_a, carry_b;
-  if (threadIdx.x == 0) carry_a = carry_b = 0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int base = 0; base < n_cells; base += 1024) {
-    const int c = base + threadIdx.x;
-    const int a = c < n_cells ? count[c] : 0;
-    const int b = (a + K6_G - 1) / K6_G;
-    int ia = a, ib = b;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int ta = __shfl_up_sync(0xffffffffu, ia, o);
-      const int tb = __shfl_up_sync(0xffffffffu, ib, o);
-      if (lane >= o) {
-        ia += ta;
-        ib += tb;
-      }
-    }
-    if (lane == 31) {
-      wa[w] = ia;
-      wb[w] = ib;
-    }
-    __syncthreads();
-    if (w == 0) {
-      int xa = wa[lane], xb = wb[lane];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int ta = __shfl_up_sync(0xffffffffu, xa, o);
-        const int tb = __shfl_up_sync(0xffffffffu, xb, o);
-        if (lane >= o) {
-          xa += ta;
-          xb += tb;
-        }
-      }
-      wa[lane] = xa;
-      wb[lane] = xb;
-    }
-    __syncthreads();
-    const int pa = (w ? wa[w - 1] : 0) + ia - a + carry_a;
-    const int pb = (w ? wb[w - 1] : 0) + ib - b + carry_b;
-    if (c < n_cells) {
-      start[c] = pa;
-      gstart[c] = pb;
-    }
-    __syncthreads();
-    if (threadIdx.x == 1023) {
-      carry_a = pa + a;
-      carry_b = pb + b;
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    start[n_cells] = carry_a;
-    gstart[n_cells] = carry_b;
-  }
-}
-
-__global__ void k5_scatter(const int *__restrict__ cell_of, const int *__restrict__ slot, int64_t n,
-                           const int *__restrict__ start, int *__restrict__ order_tmp) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  order_tmp[start[cell_of[i]] + slot[i]] = (int)i;
-}
-
-// Restore a deterministic (ascending original index = stable) order in cells.
-__global__ void __launch_bounds__(256) k5_cell_sort(const int *__restrict__ start,
-                                                    const int *__restrict__ order_tmp,
-                                                    int *__restrict__ order) {
-  __shared__ int mem[SORT_CAP];
-  const int c = blockIdx.x;
-  const int s = start[c], e = start[c + 1], cnt = e - s;
-  if (cnt > SORT_CAP) {
-    for (int t = threadIdx.x; t < cnt; t += 256) order[s + t] = order_tmp[s + t];
-    return;
-  }
-  for (int t = threadIdx.x; t < cnt; t += 256) mem[t] = order_tmp[s + t];
-  __syncthreads();
-  for (int t = threadIdx.x; t < cnt; t += 256) {
-    const int v = mem[t];
-    int r = 0;
-    for (int u = 0; u < cnt; ++u) r += mem[u] < v;
-    order[s + r] = v;
-  }
-}
-
-__global__ void k_iota(int *__restrict__ v, int64_t n) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) v[i] = (int)i;
-}
-
-// real-space forces, accumulated in cell-sorted order by k6 (partner atomics
-// on neighbouring addresses, no order[] load per pair), added into the
-// caller's order: force[order[p]] += fs[p]
-__global__ void k_unpermute_add(const int *__restrict__ order, const double *__restrict__ fs,
-                                int64_t n, double *__restrict__ force) {
-  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (p >= n) return;
-  const int64_t o = order[p];
-  force[3 * o] += fs[3 * p];
-  force[3 * o + 1] += fs[3 * p + 1];
-  force[3 * o + 2] += fs[3 * p + 2];
-}
-
-__global__ void k5_gather(const int *__restrict__ order, const double4 *__restrict__ xyzq,
-                          const int *__restrict__ cell_of, int64_t n,
-                          double4 *__restrict__ sorted, float4 *__restrict__ sorted_f,
-                          int *__restrict__ sorted_cell) {
-  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (p >= n) return;
-  const int o = order[p];
-  const double4 v = xyzq[o];
-  sorted[p] = v;
-  sorted_f[p] = make_float4((float)v.x, (float)v.y, (float)v.z, 0.0f);
-  sorted_cell[p] = cell_of[o];
-}
-
-// erfcx(x) = exp(x^2) erfc(x) on [0, 6): 12 intervals of width 1/2, degree-12
-// polynomial in t = 4x - (2i+1), generated by tools/gen_erfcx_table.py.
-// max relative error of the double-precision Horner: 8.88e-16
-__constant__ double c_erfcx_tab[12][13] = {
-    {0.7703465477309968, -0.18580147330749627, 0.03653406715146768, -0.0062194752567052616, 0.0009473309967357329, -0.00013180360486534726, 1.699015381892417e-05, -2.0502458027178e-06, 2.334366455001955e-07, -2.5224113349396268e-08, 2.601714124857212e-09, -2.645535522720767e-10, 2.5084180598363034e-11},
-    {0.5069376502931449, -0.09199317291394817, 0.014434883221956088, -0.0020286884686890566, 0.0002609005567498488, -3.1149669808397036e-05, 3.4885738807897664e-06, -3.693567406943463e-07, 3.719543629447327e-08, -3.579272112111564e-09, 3.3061733705972456e-10, -3.010096125292678e-11, 2.581271691748106e-12},
-    {0.3678229164523611, -0.05220546899115238, 0.006674723218537419, -0.0007846605374382521, 8.598189160507216e-05, -8.868776967725166e-06, 8.674584711778801e-07, -8.09194284279868e-08, 7.232217406690809e-09, -6.215429959552571e-10, 5.154261278261677e-11, -4.214961825526736e-12, 3.2747182507155396e-13},
-    {0.2849722347374364, -0.03274408637862129, 0.0034852268804429535, -0.0003478124256469985, 3.2829371903648855e-05, -2.950170555585948e-06, 2.537120414482415e-07, -2.096762028769442e-08, 1.670918660864194e-09, -1.2875251113676387e-10, 9.61847389834657e-12, -7.092030933689514e-13, 5.0048417345007894e-14},
-    {0.23108725873039188, -0.022121625702187286, 0.0019995392131691415, -0.00017190719931942612, 1.4136700602964347e-05, -1.1169223469151147e-06, 8.509165574807611e-08, -6.269598619463966e-09, 4.478950947622092e-10, -3.108856441414792e-11, 2.10082401649295e-12, -1.402683891597517e-13, 9.019823445765036e-15},
-    {0.1936620962790687, -0.01580940939015871, 0.001234912061707679, -9.272402964060302e-05, 6.717116739411538e-06, -4.708936375997823e-07, 3.202680676576849e-08, -2.117835321201201e-09, 1.3641597025404525e-10, -8.572609778060283e-12, 5.263802979021472e-13, -3.1971258939165315e-14, 1.8800738604690586e-15},
-    {0.16633534842682188, -0.011799850580292594, 0.0008085806801886348, -5.367923907668294e-05, 3.4609553809933582e-06, -2.1717047807742037e-07, 1.3286232619299866e-08, -7.937403081265358e-10, 4.636889929605563e-11, -2.651912467909991e-12, 1.4865485154109668e-13, -8.251888719805715e-15, 4.454562117727668e-16},
-    {0.14558972127503855, -0.009114064383180883, 0.0005549222204578311, -3.292629484639286e-05, 1.907118680060835e-06, -1.0798786613289054e-07, 5.985430999920972e-09, -3.251143200862901e-10, 1.732369459208254e-11, -9.063500898261399e-13, 4.659999514606456e-14, -2.3750846277556673e-15, 1.1815817873651303e-16},
-    {0.12934527478598792, -0.007236082853653833, 0.00039574164211704684, -2.1186455736001674e-05, 1.1116217064069037e-06, -5.722216817598962e-08, 2.8926009873682308e-09, -1.4371342152607251e-10, 7.023014024445707e-12, -3.3780170712636556e-13, 1.6003168989041294e-14, -7.522483388703235e-16, 3.462294803041272e-17},
-    {0.11630270721024731, -0.005875862149540788, 0.00029133289806077125, -1.4189045266088957e-05, 6.794074376588104e-07, -3.200759876395623e-08, 1.4846471070136548e-09, -6.784471061780229e-11, 3.056212968617432e-12, -1.3578510096466765e-13, 5.953169824807012e-15, -2.591907760108697e-16, 1.1078471622899968e-17},
-    {0.1056127354688918, -0.004861361168037162, 0.0002202594337569623, -9.829710797539752e-06, 4.323595940196192e-07, -1.8753983078086295e-08, 8.026239453614756e-10, -3.390857582363441e-11, 1.4147478393182942e-12, -5.831704153025278e-14, 2.3759395644914543e-15, -9.619931371665538e-17, 3.832315492243951e-18},
-    {0.09669877816971392, -0.004085804535950621, 0.00017032961517810219, -7.009307785594627e-06, 2.8486050341955844e-07, -1.1437905173582296e-08, 4.5393092554672476e-10, -1.7812390949431116e-11, 6.913427648222772e-13, -2.6548500183324395e-14, 1.0090217232526848e-15, -3.813643120173001e-17, 1.4208519269427467e-18},
-};
-
-constexpr int ERFCX_NI = 12;
-constexpr int ERFCX_NC = 13;
-
-// erfc(x) given e = exp(-x^2) (which the force needs anyway); the table lives
-// in shared memory (lanes index different intervals).  For x >= 6,
-// erfc(x) < 2.2e-17 and the pair's contribution is below double resolution
-// of any energy it enters; it is flushed to zero (branch-free).
-__device__ __forceinline__ double erfc_from_exp(double x, double e, const double *tab) {
-  const int i = min((int)(x * 2.0), ERFCX_NI - 1);
-  const double t = fma(4.0, x, -(double)(2 * i + 1));
-  const double *c = tab + i * ERFCX_NC;
-  // Estrin's scheme (dependency depth 5 instead of 12 for Horner)
-  static_assert(ERFCX_NC == 13, "Estrin tree below assumes degree 12");
-  const double t2 = t * t, t4 = t2 * t2, t8 = t4 * t4;
-  const double p01 = fma(c[1], t, c[0]), p23 = fma(c[3], t, c[2]);
-  const double p45 = fma(c[5], t, c[4]), p67 = fma(c[7], t, c[6]);
-  const double p89 = fma(c[9], t, c[8]), pab = fma(c[11], t, c[10]);
-  const double q0 = fma(p23, t2, p01), q1 = fma(p67, t2, p45);
-  const double q2 = fma(pab, t2, p89);
-  const double r = fma(fma(c[12], t4, q2), t8, fma(q1, t4, q0));
-  return x < 0.5 * ERFCX_NI ? r * e : 0.0;
-}
-
-// 1/sqrt(x) for finite x > 0: fp32 hardware seed (~22 bits) refined by two
-// Newton steps in fp64 (~1 ulp), without the library's special-case paths.
-__device__ __forceinline__ double rsqrt_pos(double x) {
-  double y = (double)rsqrtf((float)x);
-  const double h = 0.5 * x;
-  y = y * fma(-h * y, y, 1.5);
-  const double e = fma(-x * y, y, 1.0);  // residual 1 - x y^2
-  return fma(0.5 * y, e, y);
-}
-
-// exp(x) for -700 < x <= 0 (real-space arguments -alpha r^2): Cody-Waite
-// reduction and a degree-11 polynomial on [-ln2/2, ln2/2] (max rel. error
-// 2.2e-16, fitted by tools, coefficients in the constant bank).
-__constant__ double c_expm[12] = {1.0, 1.0, 0.5000000000000018, 0.16666666666666147,
-                                  0.04166666666649302, 0.008333333333569285,
-                                  0.001388888895117063, 0.00019841269413559004,
-                                  2.4801486567664484e-05, 2.7557638471514137e-06,
-                                  2.763227940718779e-07, 2.4989478846203685e-08};
-__device__ __forceinline__ double exp_neg(double x) {
-  const double n = rint(x * 1.4426950408889634);
-  double r = fma(n, -6.93147180559945286e-01, x);
-  r = fma(n, -2.319046813846299558e-17, r);
-  // Estrin's scheme (depth 5 instead of 11)
-  const double r2 = r * r, r4 = r2 * r2, r8 = r4 * r4;
-  const double p01 = fma(c_expm[1], r, c_expm[0]), p23 = fma(c_expm[3], r, c_expm[2]);
-  const double p45 = fma(c_expm[5], r, c_expm[4]), p67 = fma(c_expm[7], r, c_expm[6]);
-  const double p89 = fma(c_expm[9], r, c_expm[8]), pab = fma(c_expm[11], r, c_expm[10]);
-  const double p = fma(fma(pab, r2, p89), r8, fma(fma(p67, r2, p45), r4, fma(p23, r2, p01)));
-  const long long ni = (long long)n;
-  return __longlong_as_double(__double_as_longlong(p) + (ni << 52));
-}
-
-// K6: ordered-pair real-space kernel.  One warp = up to 32 centre particles of
-// one home cell (lanes), candidates broadcast from shared memory; accepted
-// pairs go to a per-lane queue and are evaluated in converged rounds.
-struct RSParams {
-  double L, hl, rc2, sa, al, tsap;
-  int cpd, fold, rad;  // rad: stencil radius in cells (1 or 2)
-  int half;            // 1: each unordered pair once (Newton 3rd law, atomics)
-  int jsplit;          // scan-all mode: candidate range split over this many warps
-  int c_lo, c_hi;
-  int64_t n;
-  int coul;            // screened Coulomb on pairs with r2 < rc2c
-  double rc2c;         // Coulomb cutoff^2 (rc2 = traversal cutoff^2 = max)
-  double rc2lj, lj_s2, lj_4e, lj_shift, lj_24e;  // shifted 12-6 LJ (potentials.py:21-45)
-  float rc2f;  // FP32 candidate prefilter bound (>= rc2 plus the rounding margin)
-};
-
-// dx exactly as the reference: fl(xi - xj) then one fold by +-L
-// (engine.py:117-131); with a stencil the fold is the cell-pair shift, which
-// equals the reference's fold for every pair inside the cutoff.
-template <bool FOLD>
-__device__ __forceinline__ double rs_disp(double xi, double xj, double shift, double hl, double L) {
-  double d = __dsub_rn(xi, xj);
-  if (FOLD) {
-    if (d >= hl)
-      d = __dsub_rn(d, L);
-    else if (d < -hl)
-      d = __dadd_rn(d, L);
-  } else {
-    d = __dadd_rn(d, shift);
-  }
-  return d;
-}
-
-__device__ __forceinline__ double rs_r2(double dx, double dy, double dz) {
-  return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
-}
-
-// pair-list entry: x = j (sorted index), y = g | kx<<4 | ky<<6 | kz<<8 with
-// k = 0: -L, 1: 0, 2: +L, 3: fold per pair
-constexpr int K6_LIST = 32 * K6_G + 32;  // pending pairs per warp
-constexpr uint32_t K6_SELF = 1u << 10;    // queue tag: own row, j > i only
-#ifndef K6_BBOX
-#define K6_BBOX 1  // bounding-box stage + queue before the per-centre tests (-3..7%)
-#endif
-
-#ifndef K6_SCAN
-#define K6_SCAN 0  // 1: per-step warp scan compaction, 0: per-centre ballots
-#endif
-#ifndef K6_MINB
-#define K6_MINB 4
-#endif
-template <bool LJ>
-__global__ void __launch_bounds__(K6_WARPS * 32, K6_MINB)
-    k6_real_space(const double4 *__restrict__ sorted, const float4 *__restrict__ sorted_f,
-                  const int *__restrict__ sorted_cell,
-                  const int *__restrict__ order, const int *__restrict__ cell_start,
-                  const int *__restrict__ row_ustart, RSParams P, double *__restrict__ force,
-                  double *__restrict__ eblk, double *__restrict__ eblk_lj,
-                  int *__restrict__ err, unsigned long long *__restrict__ pair_count) {
-  // A warp owns K6_G consecutive particles (centres) of one row of cells
-  // (fixed cy, cz).  Lanes stream the candidates of the stencil rows --
-  // contiguous runs of cells along x, so each 32-wide step is dense -- test
-  // each centre with the reference's exact predicate (engine.py:117-133,
-  // strict r2 < rc2), and append accepted (centre g, j, image) to one warp
-  // pair list by ballot compaction.  Whenever >= 32 pairs are pending they
-  // are evaluated in a converged round (lane l: pair l) and accumulated into
-  // the lane's slot of F_g in shared memory; slots are summed at the end.
-  __shared__ double4 s_i[K6_WARPS][K6_G];
-  __shared__ float4 s_cf[K6_WARPS][K6_G];  // centres, FP32 (prefilter)
-  // prefilter queue: candidates within r_c of the centres' bounding box,
-  // already shifted into the centres' frame (x, y, z, j bits) + pair tag
-  __shared__ float4 s_q[K6_WARPS][64];
-  __shared__ uint32_t s_qt[K6_WARPS][64];
-  __shared__ uint2 s_list[K6_WARPS][K6_LIST];
-  __shared__ double3 s_f[K6_WARPS][K6_G][32];
-  __shared__ double sh[K6_WARPS];
-  __shared__ double s_erfcx[ERFCX_NI * ERFCX_NC];
-  // image shift of a pair by its 6-bit code (k_x | k_y << 2 | k_z << 4,
-  // k = 0: -L, 1: 0, 2: +L, 3: unused): one table read instead of six
-  // 64-bit selects per pair
-  __shared__ double4 s_shift[64];
-  for (int t = threadIdx.x; t < ERFCX_NI * ERFCX_NC; t += K6_WARPS * 32)
-    s_erfcx[t] = c_erfcx_tab[t / ERFCX_NC][t % ERFCX_NC];
-  if (threadIdx.x < 64) {
-    auto sv = [&](int k) { return k == 0 ? -P.L : (k == 2 ? P.L : 0.0); };
-    const int c = threadIdx.x;
-    s_shift[c] = make_double4(sv(c & 3), sv((c >> 2) & 3), sv((c >> 4) & 3), 0.0);
-  }
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const unsigned lt_mask = (1u << lane) - 1u;
-  const int cpd = P.cpd, R = P.rad;
-  const int r_lo = P.c_lo, r_hi = P.c_hi;  // row range of this slab
-  const int u_lo = row_ustart[r_lo], u_hi = row_ustart[r_hi];
-  const int uw = blockIdx.x * K6_WARPS + warp;  // (unit, candidate split)
-  const int u = u_lo + uw / P.jsplit;
-  const int jpart = uw % P.jsplit;
-  double ue = 0.0, ue_lj = 0.0;
-  if (u < u_hi) {
-    int lo = r_lo, hi = r_hi - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (row_ustart[mid] <= u)
-        lo = mid;
-      else
-        hi = mid - 1;
-    }
-    const int row = lo;
-    const int rb = P.fold ? 0 : cell_start[row * cpd];
-    const int re = P.fold ? (int)P.n : cell_start[(row + 1) * cpd];
-    const int first = rb + K6_G * (u - row_ustart[row]);
-    const int gi = min(K6_G, re - first);
-    if (lane < gi) s_i[warp][lane] = sorted[first + lane];
-#pragma unroll
-    for (int g = 0; g < K6_G; ++g) s_f[warp][g][lane] = make_double3(0.0, 0.0, 0.0);
-    __syncwarp();
-    int cnt = 0;  // pending pairs (warp-uniform)
-    int accepted = 0;  // pairs inside the traversal cutoff (warp-uniform)
-    bool coincident = false;
-
-    // Each accepted pair stores, per axis, which image the reference's fold
-    // chose (k = 0: d - L, 1: d, 2: d + L; engine.py:117-131), so the
-    // evaluation recomputes d = fl(fl(xi - xj) + shift_k) bit-identically
-    // without branches.
-    auto shift = [&](uint32_t k) { return k == 0u ? -P.L : (k == 2u ? P.L : 0.0); };
-    // one pair: force factor gg (0 for a coincident pair); accumulates energy
-    auto pair_eval = [&](const uint2 e, double &dx, double &dy, double &dz, double &gg) {
-      const int j = (int)e.x;
-      const int g = (int)(e.y & 15u);
-      const double4 pj = sorted[j];
-      const double4 pi = s_i[warp][g];
-      const double4 sh = s_shift[(e.y >> 4) & 63u];
-      dx = __dadd_rn(__dsub_rn(pi.x, pj.x), sh.x);
-      dy = __dadd_rn(__dsub_rn(pi.y, pj.y), sh.y);
-      dz = __dadd_rn(__dsub_rn(pi.z, pj.z), sh.z);
-      const double r2raw = rs_r2(dx, dy, dz);
-      const bool zero = r2raw == 0.0;
-      coincident |= zero;
-      const double r2 = zero ? 1.0 : r2raw;
-      // sc = erfc(sqrt(alpha) r)/r, g = qq (sc + 2 sqrt(alpha/pi) e^{-alpha r^2})/r^2
-      // (ewald.py:214-218), with one exp shared by erfc and the force
-      const bool coul = P.coul && r2raw < P.rc2c;
-      const double qq = (zero || !coul) ? 0.0 : pi.w * pj.w;
-      const double inv_r = rsqrt_pos(r2);
-      const double r = r2 * inv_r;
-      const double ex = exp_neg(-P.al * r2);
-      const double sc = erfc_from_exp(P.sa * r, ex, s_erfcx) * inv_r;
-      ue = fma(P.half ? qq : 0.5 * qq, sc, ue);  // ordered pairs carry 1/2 (ewald.py:217)
-      const double inv_r2 = inv_r * inv_r;
-      gg = qq * fma(P.tsap, ex, sc) * inv_r2;
-      if (LJ) {
-        // shifted 12-6 (potentials.py:33-45): u = 4e (s12 - s6) - shift,
-        // g = 24e (2 s12 - s6) / r2, on pairs with r2 < rc_lj^2
-        const bool lj = !zero && r2raw < P.rc2lj;
-        const double s2 = P.lj_s2 * inv_r2;
-        const double s6 = s2 * s2 * s2;
-        const double s12 = s6 * s6;
-        const double ulj = fma(P.lj_4e, s12 - s6, -P.lj_shift);
-        ue_lj += lj ? (P.half ? ulj : 0.5 * ulj) : 0.0;
-        gg += lj ? P.lj_24e * fma(2.0, s12, -s6) * inv_r2 : 0.0;
-      }
-    };
-    auto accum = [&](const uint2 e, double dx, double dy, double dz, double gg) {
-      const int g = (int)(e.y & 15u);
-      double3 f = s_f[warp][g][lane];
-      f.x = fma(gg, dx, f.x);
-      f.y = fma(gg, dy, f.y);
-      f.z = fma(gg, dz, f.z);
-      s_f[warp][g][lane] = f;
-      if (P.half) {  // F_j = -F_i for the same pair (r2 is symmetric bitwise)
-        double *fj = force + 3 * (int64_t)e.x;  // cell-sorted accumulator
-        atomicAdd(fj, -gg * dx);
-        atomicAdd(fj + 1, -gg * dy);
-        atomicAdd(fj + 2, -gg * dz);
-      }
-    };
-    // evaluate entries [base, base+n) (n <= 32): lane l takes entry base+l
-    auto round = [&](const int base, const int n) {
-      if (lane < n) {
-        const uint2 e = s_list[warp][base + lane];
-        double dx, dy, dz, gg;
-        pair_eval(e, dx, dy, dz, gg);
-        accum(e, dx, dy, dz, gg);
-      }
-    };
-    // 64 entries, two independent pairs per lane (ILP)
-    auto round2 = [&](const int base) {
-      const uint2 e0 = s_list[warp][base + lane];
-      const uint2 e1 = s_list[warp][base + 32 + lane];
-      double dx0, dy0, dz0, g0, dx1, dy1, dz1, g1;
-      pair_eval(e0, dx0, dy0, dz0, g0);
-      pair_eval(e1, dx1, dy1, dz1, g1);
-      accum(e0, dx0, dy0, dz0, g0);
-      accum(e1, dx1, dy1, dz1, g1);
-    };
-    auto drain = [&]() {
-      __syncwarp();
-      int base = 0;
-      accepted += cnt - (cnt & 31);  // entries evaluated now (the rest stays queued)
-      for (; cnt - base >= 64; base += 64) round2(base);
-      if (cnt - base >= 32) {
-        round(base, 32);
-        base += 32;
-      }
-      const int rest = cnt - base;
-      __syncwarp();
-      const uint2 mv = lane < rest ? s_list[warp][base + lane] : make_uint2(0u, 0u);
-      __syncwarp();
-      if (lane < rest) s_list[warp][lane] = mv;
-      __syncwarp();
-      cnt = rest;
-    };
-    // FP32 centres and their bounding box (prefilter stage 1)
-    __syncwarp();
-    if (lane < gi) {
-      const double4 pi = s_i[warp][lane];
-      s_cf[warp][lane] = make_float4((float)pi.x, (float)pi.y, (float)pi.z, 0.0f);
-    }
-    __syncwarp();
-    float3 bb_lo = make_float3(3.0e38f, 3.0e38f, 3.0e38f), bb_hi = make_float3(-3.0e38f, -3.0e38f, -3.0e38f);
-    for (int g = 0; g < gi; ++g) {
-      const float4 c = s_cf[warp][g];
-      bb_lo = make_float3(fminf(bb_lo.x, c.x), fminf(bb_lo.y, c.y), fminf(bb_lo.z, c.z));
-      bb_hi = make_float3(fmaxf(bb_hi.x, c.x), fmaxf(bb_hi.y, c.y), fmaxf(bb_hi.z, c.z));
-    }
-    int qn = 0;  // queued candidates (warp-uniform)
-    // stage 2: entries [0, n) of the queue against every centre (lane l:
-    // entry l), accepted pairs into the pair list; keeps the tail
-    auto process_queue = [&](const int n) {
-      __syncwarp();
-      const bool ve = lane < n;
-      const float4 q = ve ? s_q[warp][lane] : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-      const uint32_t qt = ve ? s_qt[warp][lane] : 0u;
-      const int j = __float_as_int(q.w);
-      // half-shell own row: only centres g < j - first (j > i); otherwise
-      // every centre except j itself (the full-shell own row holds it)
-      const int jf = j - first;
-      const int glim = !ve ? -1 : ((qt & K6_SELF) != 0u ? jf : K6_G);
-      const uint32_t qtag = qt & ~K6_SELF;
-#pragma unroll
-      for (int g = 0; g < K6_G; ++g) {
-        if (g < gi) {
-          const float4 c = s_cf[warp][g];
-          const float dx = c.x - q.x, dy = c.y - q.y, dz = c.z - q.z;
-          const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-          const bool acc = (r2 < P.rc2f) && (g < glim) && (g != jf);
-          const unsigned bal = __ballot_sync(0xffffffffu, acc);
-          if (acc) s_list[warp][cnt + __popc(bal & lt_mask)] = make_uint2((uint32_t)j, qtag | (uint32_t)g);
-          cnt += __popc(bal);
-        }
-      }
-      __syncwarp();
-      const int rest = qn - n;
-      float4 mq = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-      uint32_t mt = 0u;
-      if (lane < rest) {
-        mq = s_q[warp][n + lane];
-        mt = s_qt[warp][n + lane];
-      }
-      __syncwarp();
-      if (lane < rest) {
-        s_q[warp][lane] = mq;
-        s_qt[warp][lane] = mt;
-      }
-      qn = rest;
-      if (cnt >= 32) drain();
-    };
-    // candidate step: lane = candidate j, test all centres.  FX / FYZ:
-    // fold x / y,z per pair (reference rule), else add the piece's shift.
-    // after: candidates must satisfy j > i (half shell, same row / scan-all)
-    auto test_range = [&](auto fx_tag, auto fyz_tag, auto nosh_tag, const int jb, const int je,
-                          const double sx, const double sy, const double sz, const uint32_t tag,
-                          const bool after) {
-      constexpr bool FX = decltype(fx_tag)::value;
-      constexpr bool FYZ = decltype(fyz_tag)::value;
-      constexpr bool NOSH = decltype(nosh_tag)::value;
-      auto fold = [&](double d, uint32_t &k) {
-        k = d >= P.hl ? 0u : (d < -P.hl ? 2u : 1u);
-        return k == 1u ? d : (k == 0u ? __dsub_rn(d, P.L) : __dadd_rn(d, P.L));
-      };
-      if constexpr (!FX && !FYZ && !K6_BBOX) {
-        // FP32 prefilter: every candidate against every centre
-        const float sxf = (float)sx, syf = (float)sy, szf = (float)sz;
-        for (int j0 = jb; j0 < je; j0 += 32) {
-          const int j = j0 + lane;
-          const bool vj = j < je;
-          const float4 pj = sorted_f[vj ? j : jb];
-          const float px = pj.x - sxf, py = pj.y - syf, pz = pj.z - szf;
-#pragma unroll
-          for (int g = 0; g < K6_G; ++g) {
-            if (g < gi) {
-              const float4 c = s_cf[warp][g];
-              const float dx = c.x - px, dy = c.y - py, dz = c.z - pz;
-              const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-              const bool acc = vj && (r2 < P.rc2f) && (after ? j > first + g : j != first + g);
-              const unsigned bal = __ballot_sync(0xffffffffu, acc);
-              if (acc) s_list[warp][cnt + __popc(bal & lt_mask)] = make_uint2((uint32_t)j, tag | (uint32_t)g);
-              cnt += __popc(bal);
-            }
-          }
-          if (cnt >= 32) drain();
-        }
-        return;
-      }
-      if constexpr (!FX && !FYZ && K6_BBOX) {
-        // FP32 prefilter, stage 1: distance to the centres' bounding box
-        // (one test per candidate, a conservative superset of stage 2 since
-        // FP32 rounding is monotone); survivors are queued in the centres'
-        // frame and tested against every centre in full 32-wide steps.
-        // rc2f includes the rounding bound; the exact FP64 r^2 < r_c^2
-        // decides inside pair_eval, so results are unchanged.
-        const float sxf = (float)sx, syf = (float)sy, szf = (float)sz;
-        const uint32_t qtag = tag | (after ? K6_SELF : 0u);
-        for (int j0 = jb; j0 < je; j0 += 32) {
-          const int j = j0 + lane;
-          const bool vj = j < je;
-          const float4 pj = sorted_f[vj ? j : jb];
-          const float px = pj.x - sxf, py = pj.y - syf, pz = pj.z - szf;
-          const float ddx = fmaxf(0.0f, fmaxf(bb_lo.x - px, px - bb_hi.x));
-          const float ddy = fmaxf(0.0f, fmaxf(bb_lo.y - py, py - bb_hi.y));
-          const float ddz = fmaxf(0.0f, fmaxf(bb_lo.z - pz, pz - bb_hi.z));
-          const bool pass = vj && fmaf(ddx, ddx, fmaf(ddy, ddy, ddz * ddz)) < P.rc2f;
-          const unsigned bal = __ballot_sync(0xffffffffu, pass);
-          if (pass) {
-            const int at = qn + __popc(bal & lt_mask);
-            s_q[warp][at] = make_float4(px, py, pz, __int_as_float(j));
-            s_qt[warp][at] = qtag;
-          }
-          qn += __popc(bal);
-          if (qn >= 32) process_queue(32);
-        }
-        return;
-      }
-      for (int j0 = jb; j0 < je; j0 += 32) {
-        const int j = j0 + lane;
-        const bool vj = j < je;
-        const double4 pj = sorted[vj ? j : jb];
-#if K6_SCAN
-        // test every centre; bit g of amask: centre g accepts candidate j
-        uint32_t amask = 0u;
-        uint32_t fcode[K6_G];  // per-centre fold outcome (fold modes only)
-#pragma unroll
-        for (int g = 0; g < K6_G; ++g) {
-          fcode[g] = 0u;
-          if (g < gi) {
-            const double4 pi = s_i[warp][g];
-            uint32_t kx = 1u, ky = 1u, kz = 1u;
-            double dx = __dsub_rn(pi.x, pj.x);
-            double dy = __dsub_rn(pi.y, pj.y);
-            double dz = __dsub_rn(pi.z, pj.z);
-            // (NOSH: no image shift on any axis; fl(d + 0.0) == d up to the
-            // sign of zero, so r2 matches the evaluation's recomputation)
-            if (FX) dx = fold(dx, kx); else if (!NOSH) dx = __dadd_rn(dx, sx);
-            if (FYZ) {
-              dy = fold(dy, ky);
-              dz = fold(dz, kz);
-            } else if (!NOSH) {
-              dy = __dadd_rn(dy, sy);
-              dz = __dadd_rn(dz, sz);
-            }
-            const double r2 = rs_r2(dx, dy, dz);
-            const bool acc = vj && (r2 < P.rc2) && (after ? j > first + g : j != first + g);
-            amask |= acc ? (1u << g) : 0u;
-            if (FX || FYZ) fcode[g] = (kx << 4) | (ky << 6) | (kz << 8);
-          }
-        }
-        // one warp scan places every lane's accepted pairs (lane-major)
-        const int c = __popc(amask);
-        int incl = c;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int t = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += t;
-        }
-        int off = cnt + incl - c;
-        cnt += __shfl_sync(0xffffffffu, incl, 31);
-#pragma unroll
-        for (int g = 0; g < K6_G; ++g) {
-          if (amask & (1u << g)) {
-            uint32_t t = tag | (uint32_t)g;
-            if (FX) t = (t & ~(3u << 4)) | (fcode[g] & (3u << 4));
-            if (FYZ) t = (t & ~(15u << 6)) | (fcode[g] & (15u << 6));
-            s_list[warp][off++] = make_uint2((uint32_t)j, t);
-          }
-        }
-#else
-#pragma unroll
-        for (int g = 0; g < K6_G; ++g) {
-          if (g < gi) {
-            const double4 pi = s_i[warp][g];
-            uint32_t kx = 1u, ky = 1u, kz = 1u;
-            double dx = __dsub_rn(pi.x, pj.x);
-            double dy = __dsub_rn(pi.y, pj.y);
-            double dz = __dsub_rn(pi.z, pj.z);
-            if (FX) dx = fold(dx, kx); else if (!NOSH) dx = __dadd_rn(dx, sx);
-            if (FYZ) {
-              dy = fold(dy, ky);
-              dz = fold(dz, kz);
-            } else if (!NOSH) {
-              dy = __dadd_rn(dy, sy);
-              dz = __dadd_rn(dz, sz);
-            }
-            const double r2 = rs_r2(dx, dy, dz);
-            const bool acc = vj && (r2 < P.rc2) && (after ? j > first + g : j != first + g);
-            const unsigned bal = __ballot_sync(0xffffffffu, acc);
-            if (acc) {
-              uint32_t t = tag | (uint32_t)g;
-              if (FX) t = (t & ~(3u << 4)) | (kx << 4);
-              if (FYZ) t = (t & ~(15u << 6)) | (ky << 6) | (kz << 8);
-              s_list[warp][cnt + __popc(bal & lt_mask)] = make_uint2((uint32_t)j, t);
-            }
-            cnt += __popc(bal);
-          }
-        }
-#endif
-        if (cnt >= 32) drain();
-      }
-    };
-
-    // candidate pieces: contiguous cell runs along x with one image shift
-    int cy = 0, cz = 0, xa = 0, xb = 0;
-    bool wide = true;
-    if (!P.fold) {
-      cy = row % cpd;
-      cz = row / cpd;
-      const int cx_lo = sorted_cell[first] % cpd;
-      const int cx_hi = sorted_cell[first + gi - 1] % cpd;
-      wide = (cx_hi - cx_lo + 2 * R + 1) > cpd;
-      xa = wide ? 0 : cx_lo - R;
-      xb = wide ? cpd - 1 : cx_hi + R;
-    }
-    using T_ = std::integral_constant<bool, true>;
-    using F_ = std::integral_constant<bool, false>;
-    if (P.fold) {
-      // fewer than 2R+1 cells per edge: every particle is a candidate and
-      // every axis folds per pair (the reference's scan-all branch)
-      const int jb0 = P.half ? first : 0, span = (int)P.n - jb0;
-      const int jb = jb0 + (int)((int64_t)span * jpart / P.jsplit);
-      const int je = jb0 + (int)((int64_t)span * (jpart + 1) / P.jsplit);
-      test_range(T_{}, T_{}, F_{}, jb, je, 0.0, 0.0, 0.0, 0u, P.half != 0);
-    } else {
-      for (int yz = 0; yz < (2 * R + 1) * (2 * R + 1); ++yz) {
-        const int oy = yz % (2 * R + 1) - R, oz = yz / (2 * R + 1) - R;
-        // half shell: rows with (oz, oy) lexicographically positive, plus
-        // this row restricted to j > i; the opposite rows find the pair
-        // from the other particle's unit
-        if (P.half && (oz < 0 || (oz == 0 && oy < 0))) continue;
-        const bool self_row = P.half && oz == 0 && oy == 0;
-        int ny = cy + oy;
-        int nz = cz + oz;
-        uint32_t kyc = 1u, kzc = 1u;
-        if (ny < 0) { ny += cpd; kyc = 2u; } else if (ny >= cpd) { ny -= cpd; kyc = 0u; }
-        if (nz < 0) { nz += cpd; kzc = 2u; } else if (nz >= cpd) { nz -= cpd; kzc = 0u; }
-        const double sy = shift(kyc), sz = shift(kzc);
-        const int cb = cpd * (ny + cpd * nz);
-        if (wide) {
-          test_range(T_{}, F_{}, F_{}, cell_start[cb], cell_start[cb + cpd], 0.0, sy, sz,
-                     (kyc << 6) | (kzc << 8), self_row);
-          continue;
-        }
-        for (int piece = 0; piece < 3; ++piece) {
-          int x0, x1;
-          uint32_t kxc;
-          if (piece == 0) { x0 = xa; x1 = min(xb, -1); kxc = 2u; }           // wrapped from the top
-          else if (piece == 1) { x0 = max(xa, 0); x1 = min(xb, cpd - 1); kxc = 1u; }
-          else { x0 = max(xa, cpd); x1 = xb; kxc = 0u; }                      // wrapped from the bottom
-          if (x0 > x1) continue;
-          const int off = piece == 0 ? cpd : (piece == 2 ? -cpd : 0);
-          int jb = cell_start[cb + x0 + off];
-          const int je = cell_start[cb + x1 + off + 1];
-          if (self_row) jb = max(jb, first + 1);  // j > i for some centre
-          const uint32_t tg = (kxc << 4) | (kyc << 6) | (kzc << 8);
-          if (kxc == 1u && kyc == 1u && kzc == 1u)
-            test_range(F_{}, F_{}, T_{}, jb, je, 0.0, 0.0, 0.0, tg, self_row);
-          else
-            test_range(F_{}, F_{}, F_{}, jb, je, shift(kxc), sy, sz, tg, self_row);
-        }
-      }
-    }
-    if (qn > 0) process_queue(qn);
-    __syncwarp();
-    accepted += cnt;
-    if (cnt > 0) round(0, cnt);
-    if (coincident) atomicOr(err, ERR_COINCIDENT);
-    if (lane == 0 && pair_count) atomicAdd(pair_count, (unsigned long long)accepted);
-    __syncwarp();
-    for (int g = 0; g < gi; ++g) {
-      const double3 f = s_f[warp][g][lane];
-      const double ax = warp_sum(f.x), ay = warp_sum(f.y), az = warp_sum(f.z);
-      if (lane == 0) {
-        const int64_t o = first + g;  // cell-sorted accumulator
-        if (P.half) {  // other warps scatter partner forces into this row
-          atomicAdd(force + 3 * o, ax);
-          atomicAdd(force + 3 * o + 1, ay);
-          atomicAdd(force + 3 * o + 2, az);
-        } else {
-          force[3 * o] += ax;
-          force[3 * o + 1] += ay;
-          force[3 * o + 2] += az;
-        }
-      }
-    }
-  }
-  ue = warp_sum(ue);
-  if (lane == 0) sh[warp] = ue;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double b = 0.0;
-    for (int w = 0; w < K6_WARPS; ++w) b += sh[w];
-    eblk[blockIdx.x] = b;
-  }
-  if (LJ) {
-    __syncthreads();
-    ue_lj = warp_sum(ue_lj);
-    if (lane == 0) sh[warp] = ue_lj;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double b = 0.0;
-      for (int w = 0; w < K6_WARPS; ++w) b += sh[w];
-      eblk_lj[blockIdx.x] = b;
-    }
-  }
-}
-
-// Units per row of cells: row_ustart[r] = sum_{r'<r} ceil(count(r')/K6_G).
-__global__ void __launch_bounds__(1024) k_scan_rows(const int *__restrict__ start, int cpd,
-                                                    int n_rows, int *__restrict__ row_ustart) {
-  __shared__ int wsum[32];
-  __shared__ int carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int base = 0; base < n_rows; base += 1024) {
-    const int r = base + threadIdx.x;
-    const int cnt = r < n_rows ? start[(r + 1) * cpd] - start[r * cpd] : 0;
-    const int b = (cnt + K6_G - 1) / K6_G;
-    int ib = b;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, ib, o);
-      if (lane >= o) ib += t;
-    }
-    if (lane == 31) wsum[w] = ib;
-    __syncthreads();
-    if (w == 0) {
-      int x = wsum[lane];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += t;
-      }
-      wsum[lane] = x;
-    }
-    __syncthreads();
-    const int pb = (w ? wsum[w - 1] : 0) + ib - b + carry;
-    if (r < n_rows) row_ustart[r] = pb;
-    __syncthreads();
-    if (threadIdx.x == 1023) carry = pb + b;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) row_ustart[n_rows] = carry;
-}
-
-// Image-shell real space for r_c > L/2 (short_range_wide_cutoff,
-// ewald.py:492-523): every j != i over the 27 nearest images, no fold,
-// dx = fl(fl(xi - xj) + L n_x), strict r2 < rc2, self images skipped as in
-// the reference.  Block = one centre; threads stride over j; deterministic
-// block reduction.  Validation-scale path (the reference guards N <= 4096).
-__global__ void __launch_bounds__(128)
-    k6w_wide(const double4 *__restrict__ xyzq, int64_t n, double L, double rc2, double sa,
-             double al, double tsap, double *__restrict__ force, double *__restrict__ eblk,
-             int *__restrict__ err) {
-  __shared__ double s_erfcx[ERFCX_NI * ERFCX_NC];
-  __shared__ double sh[4][4];
-  for (int t = threadIdx.x; t < ERFCX_NI * ERFCX_NC; t += 128)
-    s_erfcx[t] = c_erfcx_tab[t / ERFCX_NC][t % ERFCX_NC];
-  __syncthreads();
-  const int64_t i = blockIdx.x;
-  const double4 pi = xyzq[i];
-  double fx = 0.0, fy = 0.0, fz = 0.0, ue = 0.0;
-  bool coincident = false;
-  for (int64_t j = threadIdx.x; j < n; j += 128) {
-    if (j == i) continue;
-    const double4 pj = xyzq[j];
-    const double ddx = __dsub_rn(pi.x, pj.x), ddy = __dsub_rn(pi.y, pj.y),
-                 ddz = __dsub_rn(pi.z, pj.z);
-    for (int img = 0; img < 27; ++img) {
-      const double dx = __dadd_rn(ddx, L * (double)(img / 9 - 1));
-      const double dy = __dadd_rn(ddy, L * (double)((img / 3) % 3 - 1));
-      const double dz = __dadd_rn(ddz, L * (double)(img % 3 - 1));
-      const double r2 = rs_r2(dx, dy, dz);
-      if (!(r2 < rc2)) continue;
-      if (r2 == 0.0) {
-        coincident = true;
-        continue;
-      }
-      const double qq = pi.w * pj.w;
-      const double inv_r = rsqrt_pos(r2);
-      const double r = r2 * inv_r;
-      const double ex = exp_neg(-al * r2);
-      const double sc = erfc_from_exp(sa * r, ex, s_erfcx) * inv_r;
-      ue = fma(0.5 * qq, sc, ue);
-      const double gg = qq * fma(tsap, ex, sc) * (inv_r * inv_r);
-      fx = fma(gg, dx, fx);
-      fy = fma(gg, dy, fy);
-      fz = fma(gg, dz, fz);
-    }
-  }
-  if (coincident) atomicOr(err, ERR_COINCIDENT);
-  const double v[4] = {fx, fy, fz, ue};
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const double t = warp_sum(v[c]);
-    if (l == 0) sh[w][c] = t;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double a[4] = {0, 0, 0, 0};
-    for (int ww = 0; ww < 4; ++ww)
-      for (int c = 0; c < 4; ++c) a[c] += sh[ww][c];
-    force[3 * i] += a[0];
-    force[3 * i + 1] += a[1];
-    force[3 * i + 2] += a[2];
-    eblk[i] = a[3];
-  }
-}
+#include "rs_pairs.cuh"
 
 // ---------------------------------------------------------------------------
 // Device-resident velocity Verlet (velocity_verlet_step, driver.py:134-153):

@@ -162,3 +162,42 @@ def test_rho_storage_is_written_in_place(ew):
     rs.rho.values = ro
     ew.compute_rho_hat(ps, rs)
     assert rs.rho.values is ro and np.array_equal(ro, buf)
+
+
+def test_skewed_charges_and_tiny_tables(ew, orc):
+    """One charge 1e4 times the others (the fixed-point scale is max|q|), a
+    single k-vector, and a one-particle system, all on the tensor cores."""
+    rng = np.random.default_rng(11)
+    n, L = 300, 10.0
+    pos = rng.random((n, 3)) * L
+    q = rng.standard_normal(n) * 1e-2
+    q[17] = 100.0
+    q -= q.mean()
+    from paper_1708_01135_b200 import workloads as wl
+    _check(ew, orc, pos, q, L, wl.cube_half_m(6))
+    _check(ew, orc, pos, q, L, np.array([[1, 0, 0]]))
+    _check(ew, orc, pos[:1], np.array([1.0]), L, wl.cube_half_m(3))
+
+
+def test_forces_on_skewed_charges_tc_vs_fp64(ew):
+    rng = np.random.default_rng(5)
+    n, L = 400, 11.0
+    pos, q = random_neutral(n, L, seed=9)
+    q = q * np.exp(rng.uniform(-4, 1, n))
+    q -= q.mean()
+    box = ew.SimulationBox(L)
+    p = ew.EwaldParams(0.4, 4.5, 6.0, 1e-6)
+    from paper_1708_01135_b200 import workloads as wl
+    rs = ew.ReciprocalSpace(box, p, wl.cube_half_m(9))
+    out = {}
+    for tc in (True, False):
+        ps = ew.create_particle_set(n, box)
+        ps.position[:] = pos
+        ps.charge[:] = q
+        s = ew.EwaldSolver(box, p, recip=rs)
+        s.handle.set_tensor_cores(tc)
+        out[tc] = (s.evaluate(ps), ps.force.copy())
+    (r1, f1), (r0, f0) = out[True], out[False]
+    assert rel(r1.u_lr, r0.u_lr) <= 1e-12
+    # the reference's own Alg. 2 bound (test_ewald.py:230-239): 1e-12 max|F|
+    assert np.abs(f1 - f0).max() <= 1e-12 * np.abs(f0).max()

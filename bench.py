@@ -415,8 +415,8 @@ def run_ours(args):
                 "achieved": ops_k3 / t_k3 / 1e12, "peak": i8_peak,
                 "frac": ops_k3 / t_k3 / 1e12 / i8_peak,
                 "ops_per_launch": ops_k3,
-                "note": "forces: executed int8 MMA ops (15 slice pairs of five slices) over the alg2 stage time "
-                        "(k3t_wprep + k3t_gemm + k3_combine)"},
+                "note": f"forces: executed int8 MMA ops ({tci['k3_pairs_per_kstep']} slice pairs of six 8-bit "
+                        "slices, 2 per MAC) over the alg2 stage time (k3t_wmax + k3t_wprep + k3t_gemm + k3_combine)"},
             "k6_real_space": {
                 "stage_ms": 1e3 * t_real, "bound": "fp64", "unit": "TFLOP/s",
                 "pairs": rs_pairs,

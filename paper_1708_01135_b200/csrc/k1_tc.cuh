@@ -125,6 +125,23 @@ __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
 }
+__device__ __forceinline__ void tc_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+// smem -> TMEM copy of one 128 x 32-byte operand tile (same descriptor as
+// the MMA's A operand); executes in issue order with tcgen05.mma
+__device__ __forceinline__ void tc_cp_a(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+}
+#ifndef K1_ACP
+#define K1_ACP 1  // c5 S(k) 47.2 -> 41.2 ms
+#endif
+static_assert(!K1_ACP || TC_NL * TC_NMAX + 32 <= 512, "TMEM: levels + 4 G slots");
 // one lane of a converged warp (PTX elect.sync)
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
@@ -273,7 +290,14 @@ __global__ void __launch_bounds__(128)
 #endif
 constexpr int TC_GS = TC_GSTAGES;             // G ring depth (produced)
 constexpr int TC_XS = TC_XSTAGES;             // X ring depth (bulk copies)
-constexpr int TC_NTHREADS = TC_THREADS + 64;  // + MMA warp + loader warp
+#ifndef K1_PGROUPS
+#define K1_PGROUPS 2
+#endif
+// producer groups: group g fills the K-blocks it with it % TC_PG == g
+constexpr int TC_PG = K1_PGROUPS;
+constexpr int TC_PWARPS = TC_PG * TC_THREADS / 32;     // producer warps
+constexpr int TC_NTHREADS = TC_PG * TC_THREADS + 64;  // + MMA warp + loader warp
+static_assert(TC_GS % TC_PG == 0, "each G stage must belong to one producer group");
 __host__ __device__ constexpr int tc_smem_bytes(int npad_max) {
   return TC_GS * TC_S * TC_GSL + TC_XS * TC_S * tc_xsl_bytes(npad_max);
 }
@@ -342,7 +366,7 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
   tc_fence_after();
   const uint32_t tmem = tmem_base_s;
 
-  if (warp == 9) {
+  if (warp == TC_PWARPS + 1) {
     // ---- X loader ----
     if (lane == 0) {
       for (int it = 0; it < nkb; ++it) {
@@ -354,7 +378,7 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
         bulk_g2s(smem_u32(xbuf + xs * xblk), src, (uint32_t)xblk, fb);
       }
     }
-  } else if (warp == 8) {
+  } else if (warp == TC_PWARPS) {
     // ---- MMA issuer: the whole warp waits, one elected lane issues ----
     {
       const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) |
@@ -370,6 +394,28 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
           const uint64_t xd = tc_desc(smem_u32(xbuf + xs * xblk));
           const uint32_t acc0 = it > 0 ? 1u : 0u;
           constexpr int XSL = tc_xsl_bytes(0);
+#if K1_ACP
+          // G slices staged in TMEM (four 8-column slots after the levels),
+          // TS-form MMAs slice-major: each G slice leaves shared memory once
+          const uint32_t aslot = tmem + (uint32_t)(TC_NL * TC_NMAX);
+#pragma unroll
+          for (int ks = 0; ks < TC_KB / 32; ++ks) {
+#pragma unroll
+            for (int s = 0; s < TC_S; ++s) {
+              const uint32_t ta = aslot + (uint32_t)(((ks * TC_S + s) & 3) * 8);
+              tc_cp_a(ta, gd + (uint64_t)((s * TC_GSL + ks * 256) >> 4));
+#pragma unroll
+              for (int t = 0; t < TC_S; ++t) {
+                const int l = s + t - TC_W0;
+                if (l < 0) continue;
+                const int s_lo = TC_W0 + l - (TC_S - 1) > 0 ? TC_W0 + l - (TC_S - 1) : 0;
+                tc_mma_ts(tmem + (uint32_t)(l * npad), ta,
+                          xd + (uint64_t)((t * XSL + ks * 256) >> 4), idesc,
+                          (s > s_lo || ks > 0) ? 1u : acc0);
+              }
+            }
+          }
+#else
 #pragma unroll
           for (int l = 0; l < TC_NL; ++l) {
             constexpr int dummy = 0;
@@ -387,6 +433,7 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
                        (s > s_lo || ks > 0) ? 1u : acc0);
             }
           }
+#endif
           tc_commit(smem_u32(&g_empty[gs]));
           tc_commit(smem_u32(&x_empty[xs]));
         } else if ((dbg & 2) && lane == 0) {
@@ -404,13 +451,13 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
     }
   } else {
     // ---- G producers: core column pc (16 particles), row half ph, run g, quad qd ----
-    const int pc = warp & 3, ph = warp >> 2, g = lane >> 2, qd = lane & 3;
+    const int pc = warp & 3, ph = (warp >> 2) & 1, g = lane >> 2, qd = lane & 3;
     const int4 run = s_runs[g];
     const int kin = pc * 16 + qd * 4;  // particle offset in the K-block
     const int myl = run.y + 4 * ph;
     const bool active = 4 * ph < run.z;  // rows of this half exist in the run
     const double inv_qmax = 1.0 / fmax(*qmax_p, 1e-300);
-    for (int it = 0; it < nkb; ++it) {
+    for (int it = warp >> 3; it < nkb; it += TC_PG) {
       const int gs = it % TC_GS;
       uint8_t *sb = gbuf + gs * TC_S * TC_GSL;
       if (it >= TC_GS) mbar_wait(smem_u32(&g_empty[gs]), ((it / TC_GS) - 1) & 1);

@@ -57,8 +57,14 @@ __device__ __forceinline__ uint2 t3_bits(double v) {
 // shape probe gives 3487 TOP/s at N=80 vs 3006 at 64 (shared-memory A read)
 constexpr int T3_NP = T3_PARTICLES;
 static_assert(T3_NP % 16 == 0 && T3_NP <= 80, "N: multiple of 16, TMEM budget");
-constexpr int T3_PW = T3_NP / 8;               // producer warps (8 particles x 4 runs each)
-constexpr int T3_THREADS = (T3_PW + 2) * 32;   // + MMA warp + loader warp
+constexpr int T3_PW = T3_NP / 8;               // producer warps per group (8 particles x 4 runs each)
+#ifndef T3_PGROUPS
+#define T3_PGROUPS 2  // c5 forces 102 -> 91 ms (two K-blocks in production at once)
+#endif
+// producer groups: group g fills the K-blocks it with it % T3_PG == g
+constexpr int T3_PG = T3_PGROUPS;
+constexpr int T3_PROD = T3_PW * T3_PG;          // producer warps
+constexpr int T3_THREADS = (T3_PROD + 2) * 32;  // + MMA warp + loader warp
 constexpr int T3_HALF = T3_NP / 2;             // epilogue columns per warp
 #ifndef T3_ASTAGES
 #define T3_ASTAGES 3
@@ -73,6 +79,7 @@ constexpr int T3_CL = T3_CLUSTER;  // CTAs (particle tiles) sharing each A load 
 constexpr int T3_AS = T3_ASTAGES;  // A ring depth (bulk copies)
 constexpr int T3_BS = T3_BSTAGES;  // B ring depth (produced)
 constexpr int T3_BSL = (T3_NP / 8) * TC_SBO;  // one B slice (T3_NP rows x 64 B)
+static_assert(T3_BS % T3_PG == 0, "each B stage must belong to one producer group");
 constexpr int T3_KMAX = 16384;    // K (bytes) per CTA: int32 exactness
 __host__ __device__ constexpr int t3_smem_bytes() {
   return T3_AS * T3_S * TC_GSL + T3_BS * T3_S * T3_BSL;
@@ -188,6 +195,15 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t local_addr, uint32_
                : "memory");
 }
 
+#ifndef T3_ACP
+#define T3_ACP 1  // c5 forces 91 -> 84 ms
+#endif
+// T3_ACP: stage the A slices in TMEM (tcgen05.cp, four 8-column slots after
+// the level accumulators) and issue the MMAs in TS form, slice-major, so the
+// tensor core reads each A slice from shared memory once per K step instead
+// of once per slice pair
+static_assert(!T3_ACP || T3_NL * T3_NP + 32 <= 512, "TMEM: levels + 4 A slots");
+
 // k3t_gemm: grid (particle tiles of 64, M tiles, k splits), clusters of
 // T3_CL consecutive particle tiles: every A block is bulk-copied once per
 // cluster (each CTA fetches 1/T3_CL and multicasts it), every CTA's MMA
@@ -238,7 +254,7 @@ __global__ void __launch_bounds__(T3_THREADS, 1)
   const uint32_t crank = cluster_rank();
   constexpr uint16_t CMASK = (uint16_t)((1u << T3_CL) - 1u);
 
-  if (warp == T3_PW + 1) {
+  if (warp == T3_PROD + 1) {
     if (lane == 0) {
       constexpr int PIECE = ABLK / T3_CL;
       static_assert(ABLK % (16 * T3_CL) == 0, "A block must split into 16-byte pieces");
@@ -255,7 +271,7 @@ __global__ void __launch_bounds__(T3_THREADS, 1)
                       (uint32_t)PIECE, fb, CMASK);
       }
     }
-  } else if (warp == T3_PW) {
+  } else if (warp == T3_PROD) {
     {
       const uint32_t idesc =
           (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(T3_NP >> 3) << 17) | (8u << 24);
@@ -269,6 +285,26 @@ __global__ void __launch_bounds__(T3_THREADS, 1)
           const uint64_t ad = tc_desc(smem_u32(abuf + as * ABLK));
           const uint64_t bd = tc_desc(smem_u32(bbuf + bs * T3_S * T3_BSL));
           const uint32_t acc0 = it > 0 ? 1u : 0u;
+#if T3_ACP
+          const uint32_t aslot = tmem + (uint32_t)(T3_NL * T3_NP);
+#pragma unroll
+          for (int ks = 0; ks < TC_KB / 32; ++ks) {
+#pragma unroll
+            for (int s = 0; s < T3_S; ++s) {
+              const uint32_t ta = aslot + (uint32_t)(((ks * T3_S + s) & 3) * 8);
+              tc_cp_a(ta, ad + (uint64_t)((s * TC_GSL + ks * 256) >> 4));
+#pragma unroll
+              for (int t = 0; t < T3_S; ++t) {
+                const int l = s + t - T3_W0;
+                if (l < 0) continue;
+                const int s_lo = T3_W0 + l - (T3_S - 1) > 0 ? T3_W0 + l - (T3_S - 1) : 0;
+                tc_mma_ts(tmem + (uint32_t)(l * T3_NP), ta,
+                          bd + (uint64_t)((t * T3_BSL + ks * 256) >> 4), idesc,
+                          (s > s_lo || ks > 0) ? 1u : acc0);
+              }
+            }
+          }
+#else
 #pragma unroll
           for (int l = 0; l < T3_NL; ++l) {
             const int w = T3_W0 + l;
@@ -284,6 +320,7 @@ __global__ void __launch_bounds__(T3_THREADS, 1)
                        (s > s_lo || ks > 0) ? 1u : acc0);
             }
           }
+#endif
           tc_commit(smem_u32(&b_empty[bs]));
           if (T3_CL == 1)
             tc_commit(smem_u32(&a_empty[as]));
@@ -305,7 +342,7 @@ __global__ void __launch_bounds__(T3_THREADS, 1)
   } else {
     // ---- B producers: particle n, run g of the K-block (8 pairs = 16 k) ----
     // lanes: 8 particles (lane & 7) x 4 runs (lane >> 3); warps: 8 particle octets
-    const int pn = warp * 8 + (lane & 7);
+    const int pn = (warp % T3_PW) * 8 + (lane & 7);
     const int g = lane >> 3;
     const int64_t jg = p_begin + (int64_t)ptile * T3_NP + pn;
     const bool pvalid = jg < p_end;
@@ -313,7 +350,7 @@ __global__ void __launch_bounds__(T3_THREADS, 1)
     const double4 f = frac[jc];
     const double2 by = base[3 * jc + 1];
     const double2 ey = make_double2(by.x, -by.y);  // e^{+i 2pi f_y}
-    for (int it = 0; it < nkb; ++it) {
+    for (int it = warp / T3_PW; it < nkb; it += T3_PG) {
       const int bs = it % T3_BS;
       uint8_t *sb = bbuf + bs * T3_S * T3_BSL;
       if (it >= T3_BS) mbar_wait(smem_u32(&b_empty[bs]), ((it / T3_BS) - 1) & 1);

@@ -138,10 +138,27 @@ __device__ __forceinline__ void tc_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint
 __device__ __forceinline__ void tc_cp_a(uint32_t taddr, uint64_t sdesc) {
   asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
 }
+__device__ __forceinline__ void tc_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+      : "memory");
+}
+__device__ __forceinline__ void tc_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
 #ifndef K1_ACP
 #define K1_ACP 1  // c5 S(k) 47.2 -> 41.2 ms
 #endif
 static_assert(!K1_ACP || TC_NL * TC_NMAX + 32 <= 512, "TMEM: levels + 4 G slots");
+#ifndef K1_MERGE
+#define K1_MERGE 2  // c5 S(k) 41.2 -> 39.9 ms (3, 4: slower)
+#endif
+// K1_MERGE = m > 1 (with K1_ACP): one MMA covers up to m consecutive X slices
+// against G slice s, N = (m - 1) x 64 + npad (X slices sit 64 rows apart in
+// shared memory; levels 64 columns apart in TMEM, the columns npad..63 of a
+// level collect junk and are never read); accumulators zeroed first
+static_assert(K1_MERGE == 1 || (K1_ACP && (K1_MERGE - 1) * TC_NMAX + TC_NMAX <= 256), "merged N <= 256");
 // one lane of a converged warp (PTX elect.sync)
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
@@ -365,6 +382,18 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base_s;
+  const int lstride = K1_MERGE > 1 ? TC_NMAX : npad;  // TMEM columns between levels
+  if (K1_MERGE > 1) {  // zero the level accumulators (every merged MMA accumulates)
+    if (warp < 4) {
+      const uint32_t z[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+      for (int c = 0; c < TC_NL * TC_NMAX; c += 8)
+        tc_st8(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)c, z);
+      tc_wait_st();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
 
   if (warp == TC_PWARPS + 1) {
     // ---- X loader ----
@@ -404,6 +433,16 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
             for (int s = 0; s < TC_S; ++s) {
               const uint32_t ta = aslot + (uint32_t)(((ks * TC_S + s) & 3) * 8);
               tc_cp_a(ta, gd + (uint64_t)((s * TC_GSL + ks * 256) >> 4));
+#if K1_MERGE > 1
+              const uint32_t idesc0 = idesc & ~(63u << 17);
+#pragma unroll
+              for (int t = (TC_W0 - s > 0 ? TC_W0 - s : 0); t < TC_S; t += K1_MERGE) {
+                const int m = TC_S - t < K1_MERGE ? TC_S - t : K1_MERGE;
+                tc_mma_ts(tmem + (uint32_t)((s + t - TC_W0) * TC_NMAX), ta,
+                          xd + (uint64_t)((t * XSL + ks * 256) >> 4),
+                          idesc0 | ((uint32_t)(((m - 1) * TC_NMAX + npad) >> 3) << 17), 1u);
+              }
+#else
 #pragma unroll
               for (int t = 0; t < TC_S; ++t) {
                 const int l = s + t - TC_W0;
@@ -413,6 +452,7 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
                           xd + (uint64_t)((t * XSL + ks * 256) >> 4), idesc,
                           (s > s_lo || ks > 0) ? 1u : acc0);
               }
+#endif
             }
           }
 #else
@@ -539,7 +579,7 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
 #pragma unroll
       for (int l = TC_NL - 1; l >= 0; --l) {
         int r[8];
-        tc_ld8(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(l * npad + c0), r);
+        tc_ld8(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(l * lstride + c0), r);
         tc_wait_ld();
         const double wl = ldexp(1.0, 8 * (TC_W0 + l));
 #pragma unroll

@@ -203,6 +203,14 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t local_addr, uint32_
 // tensor core reads each A slice from shared memory once per K step instead
 // of once per slice pair
 static_assert(!T3_ACP || T3_NL * T3_NP + 32 <= 512, "TMEM: levels + 4 A slots");
+#ifndef T3_MERGE
+#define T3_MERGE 3  // c5 forces 84.2 -> 81.1 ms
+#endif
+// T3_MERGE = m > 1 (with T3_ACP): one MMA covers up to m consecutive B slices
+// t..t+m-1 against A slice s -- N = m x 80 rows of B (the slices are
+// contiguous in shared memory) into the m consecutive level accumulators
+// (contiguous in TMEM); accumulators are zeroed first and every MMA adds
+static_assert(T3_MERGE == 1 || (T3_ACP && T3_MERGE * T3_NP <= 256), "merged N <= 256");
 
 // k3t_gemm: grid (particle tiles of 64, M tiles, k splits), clusters of
 // T3_CL consecutive particle tiles: every A block is bulk-copied once per
@@ -251,6 +259,17 @@ __global__ void __launch_bounds__(T3_THREADS, 1)
   cluster_sync_all();  // barriers initialised cluster-wide before any remote signal
   tc_fence_after();
   const uint32_t tmem = tmem_base_s;
+  if (T3_MERGE > 1) {  // zero the level accumulators (every merged MMA accumulates)
+    if (warp < 4) {
+      const uint32_t z[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+      for (int c = 0; c < T3_NL * T3_NP; c += 8)
+        tc_st8(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)c, z);
+      tc_wait_st();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
   const uint32_t crank = cluster_rank();
   constexpr uint16_t CMASK = (uint16_t)((1u << T3_CL) - 1u);
 
@@ -293,6 +312,16 @@ __global__ void __launch_bounds__(T3_THREADS, 1)
             for (int s = 0; s < T3_S; ++s) {
               const uint32_t ta = aslot + (uint32_t)(((ks * T3_S + s) & 3) * 8);
               tc_cp_a(ta, ad + (uint64_t)((s * TC_GSL + ks * 256) >> 4));
+#if T3_MERGE > 1
+              constexpr uint32_t idesc0 = (2u << 4) | (1u << 7) | (1u << 10) | (8u << 24);
+#pragma unroll
+              for (int t = (T3_W0 - s > 0 ? T3_W0 - s : 0); t < T3_S; t += T3_MERGE) {
+                const int m = T3_S - t < T3_MERGE ? T3_S - t : T3_MERGE;
+                tc_mma_ts(tmem + (uint32_t)((s + t - T3_W0) * T3_NP), ta,
+                          bd + (uint64_t)((t * T3_BSL + ks * 256) >> 4),
+                          idesc0 | ((uint32_t)((m * T3_NP) >> 3) << 17), 1u);
+              }
+#else
 #pragma unroll
               for (int t = 0; t < T3_S; ++t) {
                 const int l = s + t - T3_W0;
@@ -302,6 +331,7 @@ __global__ void __launch_bounds__(T3_THREADS, 1)
                           bd + (uint64_t)((t * T3_BSL + ks * 256) >> 4), idesc,
                           (s > s_lo || ks > 0) ? 1u : acc0);
               }
+#endif
             }
           }
 #else

@@ -33,15 +33,6 @@ __host__ __device__ constexpr int ts_smem_bytes(int A) {
              : (128 * (TS_NP + 1) * 8 + TS_NP * (A + 1) * 16);
 }
 
-__device__ __forceinline__ void tc_st8(uint32_t taddr, const uint32_t (&r)[8]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
-      : "memory");
-}
-__device__ __forceinline__ void tc_wait_st() {
-  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-}
 
 // W slices in the row-major layout of the TS kernel:
 // wrow[(((mtile * nkb + kb) * 128 + r) * T3_S + s) * 64 + k]

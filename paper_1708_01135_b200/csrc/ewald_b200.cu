@@ -70,6 +70,9 @@ constexpr int K3_CH = 32;         // k-items per shared-memory chunk
 #ifndef K6_WARPS
 #define K6_WARPS 4
 #endif
+#ifndef K6_RSPLIT
+#define K6_RSPLIT 1               // warps per real-space unit (stencil rows split between them)
+#endif
 #ifndef K6_G
 #define K6_G 8                    // centre particles per real-space warp
 #endif
@@ -1444,6 +1447,7 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
   // scan-all mode with few units: split every unit's candidates over
   // several warps (partial sums meet in the atomics of the half shell)
   rp.jsplit = 1;
+  if (!fold && rp.half) rp.jsplit = K6_RSPLIT;
   if (fold && rp.half) {
     const int64_t want = 4 * (int64_t)h->n_sm * K6_WARPS;
     rp.jsplit = (int)std::max<int64_t>(1, std::min<int64_t>(64, want / std::max<int64_t>(1, units_max)));
@@ -1451,8 +1455,9 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
   }
   const unsigned nb = (unsigned)std::max<int64_t>(
       1, (units_max * rp.jsplit + K6_WARPS - 1) / K6_WARPS);
-  CK(h->eblk.ensure(nb * sizeof(double)));
-  if (lj_on) CK(h->eblk_lj.ensure(nb * sizeof(double)));
+  const int64_t n_eslots = (int64_t)nb * K6_WARPS;  // one energy slot per warp
+  CK(h->eblk.ensure(n_eslots * sizeof(double)));
+  if (lj_on) CK(h->eblk_lj.ensure(n_eslots * sizeof(double)));
   if (rows_slab <= 0) {
     if (pair_coul) CK(cudaMemsetAsync(d_u_out, 0, sizeof(double), h->stream));
     if (lj_on && d_ulj_out) CK(cudaMemsetAsync(d_ulj_out, 0, sizeof(double), h->stream));
@@ -1462,26 +1467,25 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
   if (part == 0) CK(cudaMemsetAsync(h->pairc.p, 0, sizeof(unsigned long long), h->stream));
   CK(h->fsorted.ensure((size_t)n * 3 * sizeof(double)));
   CK(cudaMemsetAsync(h->fsorted.p, 0, (size_t)n * 3 * sizeof(double), h->stream));
-  if (lj_on)
-    k6_real_space<true><<<nb, K6_WARPS * 32, 0, h->stream>>>(
-        h->sorted.as<double4>(), h->sorted_f.as<float4>(), h->sorted_cell.as<int>(), h->order.as<int>(), h->start.as<int>(),
-        h->row_ustart.as<int>(), rp, h->fsorted.as<double>(), h->eblk.as<double>(),
-        h->eblk_lj.as<double>(), h->errflag.as<int>(), h->pairc.as<unsigned long long>());
-  else
-    k6_real_space<false><<<nb, K6_WARPS * 32, 0, h->stream>>>(
-        h->sorted.as<double4>(), h->sorted_f.as<float4>(), h->sorted_cell.as<int>(), h->order.as<int>(), h->start.as<int>(),
-        h->row_ustart.as<int>(), rp, h->fsorted.as<double>(), h->eblk.as<double>(), nullptr,
+  {
+    auto kern = lj_on ? (rp.half ? k6_real_space<true, true> : k6_real_space<true, false>)
+                      : (rp.half ? k6_real_space<false, true> : k6_real_space<false, false>);
+    kern<<<nb, K6_WARPS * 32, 0, h->stream>>>(
+        h->sorted.as<double4>(), h->sorted_f.as<float4>(), h->sorted_cell.as<int>(),
+        h->order.as<int>(), h->start.as<int>(), h->row_ustart.as<int>(), rp,
+        h->fsorted.as<double>(), h->eblk.as<double>(), lj_on ? h->eblk_lj.as<double>() : nullptr,
         h->errflag.as<int>(), h->pairc.as<unsigned long long>());
+  }
   CKL();
   k_unpermute_add<<<blocks_for(n, 256), 256, 0, h->stream>>>(h->order.as<int>(),
                                                              h->fsorted.as<double>(), n, d_force);
   CKL();
   if (pair_coul) {
-    k_sum<<<1, 1024, 0, h->stream>>>(h->eblk.as<double>(), nb, 1.0, d_u_out);
+    k_sum<<<1, 1024, 0, h->stream>>>(h->eblk.as<double>(), n_eslots, 1.0, d_u_out);
     CKL();
   }
   if (lj_on && d_ulj_out) {
-    k_sum<<<1, 1024, 0, h->stream>>>(h->eblk_lj.as<double>(), nb, 1.0, d_ulj_out);
+    k_sum<<<1, 1024, 0, h->stream>>>(h->eblk_lj.as<double>(), n_eslots, 1.0, d_ulj_out);
     CKL();
   }
   return EWB_OK;

@@ -424,6 +424,8 @@ struct ewb_handle {
   int64_t n = 0;
   bool loaded = false;
   DBuf pos, q, force, rho;                   // host-API staging (caller layout)
+  DBuf force_in;  // the caller's forces as uploaded (restored on a device-side error)
+  double *hscr = nullptr;  // pinned host scratch: energies [0..2], error flag [3]
   DBuf frac, base, xyzq;                     // derived
   DBuf spart, sslot, sp, fpart, upart, eblk, eblk2, eblk_lj, energy, errflag;
   DBuf cell_of, slot, count, start, gstart, order_tmp, order, sorted, sorted_cell, row_ustart;
@@ -1792,8 +1794,9 @@ void ewb_destroy(ewb_handle *h) {
                   &h->errflag, &h->cell_of, &h->slot, &h->count, &h->start, &h->gstart,
                   &h->order_tmp, &h->order, &h->sorted, &h->sorted_cell, &h->row_ustart,
                   &h->sorted_f, &h->tc_qmax, &h->tc_ytab, &h->tc_ztab, &h->tc_xsl, &h->t3_wsl,
-                  &h->t3_rscale, &h->pairc, &h->eblk_r, &h->fsorted})
+                  &h->t3_rscale, &h->pairc, &h->eblk_r, &h->fsorted, &h->force_in})
     b->release();
+  if (h->hscr) cudaFreeHost(h->hscr);
   h->plan.release();
   for (auto &ge : h->gexec)
     if (ge) cudaGraphExecDestroy(ge);
@@ -2095,6 +2098,11 @@ int ewb_evaluate(ewb_handle *h, const double *pos, const double *q, int64_t n,
   CK(cudaStreamWaitEvent(h->cstream, h->ev_fup, 0));
   CK(cudaMemcpyAsync(h->force.p, force_inout, n * 3 * sizeof(double), cudaMemcpyHostToDevice,
                      h->cstream));
+  // kept so that an error detected after the pipeline can restore the
+  // caller's array (the result is copied out before the flag is read)
+  CK(h->force_in.ensure(n * 3 * sizeof(double)));
+  CK(cudaMemcpyAsync(h->force_in.p, h->force.p, n * 3 * sizeof(double), cudaMemcpyDeviceToDevice,
+                     h->cstream));
   CK(cudaEventRecord(h->ev_fup, h->cstream));
   h->fup_pending = true;
   h->rho_host = rho_out;
@@ -2109,19 +2117,25 @@ int ewb_evaluate(ewb_handle *h, const double *pos, const double *q, int64_t n,
     cudaStreamSynchronize(h->cstream);
     return rc;
   }
-  double en[3];
-  CK(cudaMemcpyAsync(en, h->energy.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-  if ((rc = check_errflag(
-           h, ((h->coul_on && h->rc > 0.5 * h->L && !h->lj_on) ? 0 : ERR_UNWRAPPED) |
-                  ERR_COINCIDENT))) {
-    cudaStreamSynchronize(h->cstream);  // no copy into caller memory after we return
-    return rc;
-  }
+  // one synchronisation: energies, error flag and forces are copied out
+  // together; on a device-side error the caller's forces are restored
+  if (!h->hscr) CK(cudaHostAlloc(&h->hscr, 4 * sizeof(double), cudaHostAllocPortable));
+  CK(cudaMemcpyAsync(h->hscr, h->energy.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaMemcpyAsync(h->hscr + 3, h->errflag.p, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
   CK(cudaMemcpyAsync(force_inout, h->force.p, n * 3 * sizeof(double), cudaMemcpyDeviceToHost,
                      h->stream));
   CK(cudaStreamSynchronize(h->stream));
   CK(cudaStreamSynchronize(h->cstream));  // rho (copied after segment 3)
-  if (energies) std::memcpy(energies, en, sizeof en);
+  int e = 0;
+  std::memcpy(&e, h->hscr + 3, sizeof(int));
+  e &= ((h->coul_on && h->rc > 0.5 * h->L && !h->lj_on) ? 0 : ERR_UNWRAPPED) | ERR_COINCIDENT;
+  if (e) {
+    CK(cudaMemcpy(force_inout, h->force_in.p, n * 3 * sizeof(double), cudaMemcpyDeviceToHost));
+    if (e & ERR_UNWRAPPED)
+      return h->fail(EWB_EUNWRAPPED, "positions must be wrapped into [0, L) before binning");
+    return h->fail(EWB_ECOINCIDENT, "coincident particles in Coulomb kernel");
+  }
+  if (energies) std::memcpy(energies, h->hscr, 3 * sizeof(double));
   return read_timings(h, timings);
 }
 

@@ -199,11 +199,15 @@ def test_errors(ew):
         ew.total_coulomb(ps, p)
     ps.charge[:] = (1.0, -1.0)
     ps.position[1] = ps.position[0]
+    ps.force[:] = [[1.0, 2.0, 3.0], [4.0, 5.0, 6.0]]
+    f0 = ps.force.copy()
     with pytest.raises(ew.CoincidentParticlesError):
         ew.total_coulomb(ps, p)
+    np.testing.assert_array_equal(ps.force, f0)  # caller's forces untouched on error
     ps.position[1] = (-0.5, 1.0, 1.0)
     with pytest.raises(ValueError):
         ew.total_coulomb(ps, p)
+    np.testing.assert_array_equal(ps.force, f0)
     ps.position[1] = (5.0, 1.0, 1.0)
     with pytest.raises(ew.BoxTooSmallError):   # r_c > L (ewald.py:561-565)
         ew.EwaldSolver(box, ew.EwaldParams(0.01, 11.0, 2.0, 1e-3)).evaluate(ps)

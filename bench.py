@@ -60,6 +60,21 @@ FLOPS_SURVEY = 22.0
 FLOPS_PAIR_RS = 64.0
 
 
+def ncu_traffic(config, kernel):
+    """DRAM bytes (read + write) per launch of `kernel` on `config` from the
+    newest committed `ncu --set full` capture (profiles/r*/traffic.json,
+    written by tools/ncu_traffic.py); (None, None) when there is none."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "traffic.json")),
+                       reverse=True):
+        try:
+            ent = json.load(open(path))[config][kernel]
+        except (OSError, ValueError, KeyError):
+            continue
+        return ent["dram_bytes"], (f"{os.path.relpath(path, ROOT)}: ncu --set full "
+                                   f"({ent['source']}), bytes per launch")
+    return None, None
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -428,9 +443,11 @@ def run_ours(args):
         }
         dom = max(kern, key=lambda k: kern[k]["stage_ms"])
         d = kern[dom]
+        traffic, traffic_src = ncu_traffic(args.config, dom)
         roof = {
             "bound": d["bound"], "kernel": dom, "achieved": d["achieved"], "peak": d["peak"],
-            "unit": d["unit"], "frac": d["frac"], "traffic": None,
+            "unit": d["unit"], "frac": d["frac"], "traffic": traffic,
+            "traffic_source": traffic_src,
             "peak_source": ("measured int8 tcgen05.mma probe (ewb_probe_i8_peak, M128 N256 K32, "
                             "this run)" if d["bound"] == "tensor" else
                             "measured FP64 DFMA probe (ewb_probe_fp64_peak, this run)"),

@@ -153,11 +153,23 @@ int ewb_dev_kspace_finalize(ewb_handle *h, const double *d_slots,
 int ewb_dev_recip_forces(ewb_handle *h, int64_t i0, int64_t i1,
                          double *d_force);
 /* Real-space forces of the particles whose home cell lies in z-slab
- * part/nparts, added into d_force (N,3); u_sr of those particles. */
+ * part/nparts, added into d_force (N,3); u_sr of those particles.  With
+ * u_sr == NULL the call only enqueues work (no synchronisation): the energy
+ * stays in the device slot read by ewb_dev_energies and device-side errors
+ * are reported by ewb_dev_check. */
 int ewb_dev_real_space(ewb_handle *h, int part, int nparts, double *d_force,
                        double *u_sr);
-/* Self energy -sqrt(alpha/pi) * sum q^2 over all loaded particles. */
+/* Self energy -sqrt(alpha/pi) * sum q^2 over all loaded particles
+ * (u_self == NULL: asynchronous, device slot only). */
 int ewb_dev_self_energy(ewb_handle *h, double *u_self);
+/* Device energy slots (u_sr, u_lr, u_self of the last stages) copied into
+ * d_out3 (device, 3 doubles) on the handle's stream.  Replaces the three
+ * scalar returns of the engine's kernels (ewald.py:609-655) for a
+ * synchronisation-free multi-GPU step. */
+int ewb_dev_energies(ewb_handle *h, double *d_out3);
+/* Synchronise and raise the deferred device-side errors: unwrapped
+ * positions (celllist.py:90-91) and coincident particles (ewald.py:212-213). */
+int ewb_dev_check(ewb_handle *h);
 /* Whole evaluation on device-resident data (single GPU); force +=. */
 int ewb_dev_evaluate(ewb_handle *h, const double *d_pos, const double *d_q,
                      int64_t n, double *d_force, double *d_rho_out,

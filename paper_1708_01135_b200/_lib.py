@@ -69,6 +69,8 @@ SIGNATURES = {
     "ewb_dev_recip_forces": (_INT, [_P, _I64, _I64, _P]),
     "ewb_dev_real_space": (_INT, [_P, _INT, _INT, _P, _P]),
     "ewb_dev_self_energy": (_INT, [_P, _P]),
+    "ewb_dev_energies": (_INT, [_P, _P]),
+    "ewb_dev_check": (_INT, [_P]),
     "ewb_dev_evaluate": (_INT, [_P, _P, _P, _I64, _P, _P, _P, _P]),
     "ewb_set_coulomb": (_INT, [_P, _INT]),
     "ewb_set_lj": (_INT, [_P, _INT, _D, _D, _D, _D, _D, _D]),
@@ -373,6 +375,24 @@ class Handle:
         u = ctypes.c_double(0.0)
         self._check(self.lib.ewb_dev_self_energy(self.h, ctypes.byref(u)))
         return u.value
+
+    # asynchronous variants: energies stay in the device slots
+    def dev_real_space_async(self, part, nparts, d_force):
+        self._check(self.lib.ewb_dev_real_space(self.h, int(part), int(nparts),
+                                                d_force, None))
+
+    def dev_kspace_finalize_async(self, d_slots, d_rho_out=None):
+        self._check(self.lib.ewb_dev_kspace_finalize(self.h, d_slots, d_rho_out,
+                                                     None))
+
+    def dev_self_energy_async(self):
+        self._check(self.lib.ewb_dev_self_energy(self.h, None))
+
+    def dev_energies(self, d_out3):
+        self._check(self.lib.ewb_dev_energies(self.h, d_out3))
+
+    def dev_check(self):
+        self._check(self.lib.ewb_dev_check(self.h))
 
     def dev_evaluate(self, d_pos, d_q, n, d_force, d_rho_out=None,
                      timings=True):

@@ -2202,9 +2202,13 @@ int ewb_dev_real_space(ewb_handle *h, int part, int nparts, double *d_force, dou
   if (rc) return rc;
   if (nparts < 1 || part < 0 || part >= nparts) return h->fail(EWB_EINVAL, "bad slab index");
   CK(cudaSetDevice(h->device));
-  if ((rc = check_errflag(h, ERR_UNWRAPPED))) return rc;
+  // u_sr == NULL: asynchronous (binning clamps cell indices, so unwrapped
+  // input is memory-safe); u_sr stays in the device energy slot and errors
+  // are reported by ewb_dev_check
+  if (u_sr && (rc = check_errflag(h, ERR_UNWRAPPED))) return rc;
   CK(h->energy.ensure(8 * sizeof(double)));
   if ((rc = stage_real_space(h, part, nparts, d_force, h->energy.as<double>(), nullptr))) return rc;
+  if (!u_sr) return EWB_OK;
   double u = 0.0;
   CK(cudaMemcpyAsync(&u, h->energy.as<double>(), sizeof(double), cudaMemcpyDeviceToHost,
                      h->stream));
@@ -2213,12 +2217,36 @@ int ewb_dev_real_space(ewb_handle *h, int part, int nparts, double *d_force, dou
   return EWB_OK;
 }
 
+// The device energy slots (u_sr, u_lr, u_self of the last asynchronous
+// stages) copied into caller device memory on the handle's stream.
+int ewb_dev_energies(ewb_handle *h, double *d_out3) {
+  int rc = require_state(h, false, false);
+  if (rc) return rc;
+  if (!d_out3) return h->fail(EWB_EINVAL, "null energy buffer");
+  CK(cudaSetDevice(h->device));
+  CK(h->energy.ensure(8 * sizeof(double)));
+  CK(cudaMemcpyAsync(d_out3, h->energy.p, 3 * sizeof(double), cudaMemcpyDeviceToDevice,
+                     h->stream));
+  return EWB_OK;
+}
+
+// Synchronise the handle's stream and report device-side errors of the
+// asynchronous stages (unwrapped positions, coincident particles).
+int ewb_dev_check(ewb_handle *h) {
+  int rc = require_state(h, false, false);
+  if (rc) return rc;
+  CK(cudaSetDevice(h->device));
+  CK(h->errflag.ensure(sizeof(int)));
+  return check_errflag(h, ERR_UNWRAPPED | ERR_COINCIDENT);
+}
+
 int ewb_dev_self_energy(ewb_handle *h, double *u_self) {
   int rc = require_state(h, false, true);
   if (rc) return rc;
   CK(cudaSetDevice(h->device));
   CK(h->energy.ensure(8 * sizeof(double)));
   if ((rc = stage_self(h, h->energy.as<double>() + 2))) return rc;
+  if (!u_self) return EWB_OK;  // asynchronous: stays in the device energy slot
   double u = 0.0;
   CK(cudaMemcpyAsync(&u, h->energy.as<double>() + 2, sizeof(double), cudaMemcpyDeviceToHost,
                      h->stream));

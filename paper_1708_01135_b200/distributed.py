@@ -14,9 +14,13 @@ global reduction of rho_hat.  Here each rank owns:
   full configuration, as the reference API does), so no halo exchange is
   needed and the ordered-pair write-to-centre convention (engine.py:10-14)
   means no force communication inside the pair loop;
-* the per-rank force contributions are combined by an all-reduce so every
-  rank returns the full force array (drop-in semantics), and the two scalar
-  energies by a 2-element all-reduce.
+* the per-rank force contributions and the rank's real-space energy travel
+  in ONE all-reduce buffer [F (3N) | u_sr | u_lr | u_self] (u_lr and u_self
+  are complete on every rank and enter from rank 0 only), so every rank
+  returns the full force array (drop-in semantics).  The step enqueues all
+  device work and collectives without a host synchronisation; the single
+  synchronisation at the end reads the energies and the deferred device
+  error flag (coincident particles, unwrapped positions).
 
 ``stages`` is the device-stage interface (``DeviceStages`` wraps the C-ABI);
 tests inject a CPU stand-in to run this orchestration under ``gloo``.
@@ -50,6 +54,23 @@ class DeviceStages:
 
     def real_space(self, part, nparts, force):
         return self.h.dev_real_space(part, nparts, force.data_ptr())
+
+    def real_space_async(self, part, nparts, force):
+        self.h.dev_real_space_async(part, nparts, force.data_ptr())
+
+    def finalize_async(self, slots, rho_out=None):
+        self.h.dev_kspace_finalize_async(
+            slots.data_ptr(), None if rho_out is None else rho_out.data_ptr())
+
+    def self_energy_async(self):
+        self.h.dev_self_energy_async()
+
+    def energies(self, out3):
+        """device slots (u_sr, u_lr, u_self) -> out3 (device tensor, 3)"""
+        self.h.dev_energies(out3.data_ptr())
+
+    def check(self):
+        self.h.dev_check()
 
     def rho_partial(self, i0, i1, slots):
         self.h.dev_rho_partial(i0, i1, slots.data_ptr())
@@ -88,18 +109,24 @@ class ShardedEwald:
         if self._slots is None or self._slots.numel() != ns:
             self._slots = torch.empty(ns, dtype=torch.float64, device=self.device)
         i0, i1 = shard_range(n, self.rank, self.world)
-        contrib = torch.zeros_like(force) if self.world > 1 else force
+        if self.world > 1:
+            buf = torch.zeros(3 * n + 3, dtype=torch.float64, device=self.device)
+            contrib, en = buf[:3 * n].view(n, 3), buf[3 * n:]
+        else:
+            contrib, en = force, torch.empty(3, dtype=torch.float64, device=self.device)
         self.st.load(pos, q)
-        u_sr = self.st.real_space(self.rank, self.world, contrib)
         self.st.rho_partial(i0, i1, self._slots)
         self._allreduce(self._slots)           # S(k) = sum over shards
-        u_lr = self.st.finalize(self._slots, rho_out)
+        self.st.finalize_async(self._slots, rho_out)
+        self.st.real_space_async(self.rank, self.world, contrib)
         self.st.recip_forces(i0, i1, contrib)
-        u_self = self.st.self_energy()
+        self.st.self_energy_async()
+        self.st.energies(en)
         if self.world > 1:
-            red = torch.tensor([u_sr], dtype=torch.float64, device=self.device)
-            self._allreduce(red)
-            self._allreduce(contrib)
+            if self.rank != 0:
+                en[1:].zero_()                 # complete on every rank: count once
+            self._allreduce(buf)               # forces + energies, one collective
             force += contrib
-            u_sr = float(red[0])
+        self.st.check()
+        u_sr, u_lr, u_self = en.tolist()
         return u_sr, u_lr, u_self

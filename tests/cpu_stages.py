@@ -66,3 +66,19 @@ class OracleStages:
 
     def self_energy(self):
         return orc.self_energy(self.q, self.alpha)
+
+    # asynchronous interface (energies kept until energies())
+    def real_space_async(self, part, nparts, force):
+        self._u_sr = self.real_space(part, nparts, force)
+
+    def finalize_async(self, slots, rho_out=None):
+        self._u_lr = self.finalize(slots, rho_out)
+
+    def self_energy_async(self):
+        self._u_self = self.self_energy()
+
+    def energies(self, out3):
+        out3.copy_(torch.tensor([self._u_sr, self._u_lr, self._u_self], dtype=torch.float64))
+
+    def check(self):
+        pass

@@ -308,6 +308,43 @@ def test_device_stages_sharded_match_full(ew):
     assert np.abs(f.cpu().numpy() - ff).max() <= 1e-12 * f_rms(ff)
 
 
+def test_sharded_ewald_device_stages_one_rank(ew):
+    """distributed.ShardedEwald on the product DeviceStages (asynchronous
+    stages, device energy slots, one synchronisation) against the
+    single-call evaluation; coincident particles surface from the deferred
+    error check."""
+    torch = pytest.importorskip("torch")
+    from paper_1708_01135_b200 import _lib
+    from paper_1708_01135_b200 import workloads as wl
+    from paper_1708_01135_b200.distributed import DeviceStages, ShardedEwald
+    cfg = wl.make_config("c2", seed=0)
+    dev = torch.device("cuda", 0)
+    pos = torch.from_numpy(cfg["pos"]).to(dev)
+    q = torch.from_numpy(cfg["q"]).to(dev)
+    n = q.shape[0]
+    h = _lib.Handle(0)
+    h.set_stream(torch.cuda.current_stream().cuda_stream)
+    params = ew.EwaldParams(cfg["alpha_ref"], cfg["r_cutoff"], 10.0, 1e-6)
+    rs = ew.ReciprocalSpace(cfg["box"], params, cfg["m_int"])
+    h.set_system(cfg["L"], params.alpha, params.r_cutoff)
+    h.set_kspace(rs.m_int, rs.coeff)
+    f_full = torch.zeros((n, 3), dtype=torch.float64, device=dev)
+    en, _ = h.dev_evaluate(pos.data_ptr(), q.data_ptr(), n, f_full.data_ptr())
+    sh = ShardedEwald(DeviceStages(h), dev)
+    f = torch.zeros((n, 3), dtype=torch.float64, device=dev)
+    rho = torch.zeros(2 * rs.n_stored, dtype=torch.float64, device=dev)
+    u = sh.evaluate(pos, q, f, rho_out=rho)
+    for got, want in zip(u, en):
+        assert rel(got, want) <= 1e-12
+    ff = f_full.cpu().numpy()
+    assert np.abs(f.cpu().numpy() - ff).max() <= 1e-12 * f_rms(ff)
+    assert float(torch.abs(rho).max()) > 0.0
+    pos2 = pos.clone()
+    pos2[1] = pos2[0]
+    with pytest.raises(ew.CoincidentParticlesError):
+        sh.evaluate(pos2, q, f)
+
+
 @pytest.mark.parametrize("name", ["c2", "c4"])
 def test_stencil_grids_agree(ew, name):
     """r_c/2 cells with the 5^3 stencil and the reference's r_c cells with

@@ -96,6 +96,14 @@ int ewb_set_graphs(ewb_handle *h, int on);
  * run to run at the 1e-16 level).  1: ordered pairs, write-to-centre only
  * (engine.py:10-14) -- bitwise reproducible, ~1.6x more real-space work. */
 int ewb_set_deterministic(ewb_handle *h, int on);
+/* Real space in two passes (default 0: measured slower than the fused kernel,
+ * kept as an option and tested for equality): a traversal kernel writes each
+ * unit's accepted pairs to a list in HBM, an evaluation kernel (fewer
+ * registers, more warps per SM) evaluates them; units whose list overflows
+ * its capacity fall back to the fused kernel.  0: one fused kernel.  2:
+ * split with a 32-entry capacity (testing: exercises the overflow pass).
+ * Same pairs and per-pair arithmetic either way (ewald.py:208-221). */
+int ewb_set_real_space_split(ewb_handle *h, int on);
 
 /* EwaldParams: box edge L, screening alpha (A^-2, erfc(sqrt(alpha) r)),
  * real-space cutoff.  rc2 is r_cutoff**2 as the caller computed it, so the

@@ -50,6 +50,7 @@ SIGNATURES = {
     "ewb_set_max_pair_segment": (_INT, [_P, _INT]),
     "ewb_set_stencil": (_INT, [_P, _INT]),
     "ewb_set_deterministic": (_INT, [_P, _INT]),
+    "ewb_set_real_space_split": (_INT, [_P, _INT]),
     "ewb_set_graphs": (_INT, [_P, _INT]),
     "ewb_set_const_gather": (_INT, [_P, _INT]),
     "ewb_set_tensor_cores": (_INT, [_P, _INT]),
@@ -236,6 +237,11 @@ class Handle:
 
     def set_deterministic(self, on):
         self._check(self.lib.ewb_set_deterministic(self.h, 1 if on else 0))
+
+    def set_real_space_split(self, mode):
+        """1/True: two-pass real space (default), 0/False: fused kernel,
+        2: two-pass with a tiny list capacity (tests the overflow pass)."""
+        self._check(self.lib.ewb_set_real_space_split(self.h, int(mode)))
 
     def set_stencil(self, rad):
         self._check(self.lib.ewb_set_stencil(self.h, int(rad)))

@@ -76,6 +76,9 @@ constexpr int K3_CH = 32;         // k-items per shared-memory chunk
 #ifndef K6_G
 #define K6_G 8                    // centre particles per real-space warp
 #endif
+#ifndef K6_SPLIT
+#define K6_SPLIT 0                // real space as traversal + evaluation passes (measured slower)
+#endif
 constexpr int SORT_CAP = 4096;    // in-cell deterministic sort capacity
 constexpr int RED_THREADS = 256;
 
@@ -406,6 +409,8 @@ struct ewb_handle {
   DBuf tc_qmax, tc_ytab, tc_ztab, tc_xsl;
   DBuf t3_wsl, t3_rscale;
   DBuf pairc;  // in-cutoff pairs visited by the last real-space pass
+  int rs_split = K6_SPLIT;        // two-pass real space (pair lists in HBM), off by default
+  DBuf rs_list, rs_count;         // per-unit pair lists and their lengths
   DBuf eblk_r;  // energy scratch of the reciprocal stages (own stream)
   DBuf fsorted;  // real-space forces in cell-sorted order
   void *tc_spart_zeroed = nullptr;  // spart buffer whose unmapped slots were zeroed
@@ -1458,8 +1463,22 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
   const unsigned nb = (unsigned)std::max<int64_t>(
       1, (units_max * rp.jsplit + K6_WARPS - 1) / K6_WARPS);
   const int64_t n_eslots = (int64_t)nb * K6_WARPS;  // one energy slot per warp
-  CK(h->eblk.ensure(n_eslots * sizeof(double)));
-  if (lj_on) CK(h->eblk_lj.ensure(n_eslots * sizeof(double)));
+  // two-pass real space: lists of 32-bit entries (j < 2^23), capacity per
+  // unit twice the mean half-shell pair count of K6_G centres plus slack
+  const bool split = h->rs_split && !fold && n < ((int64_t)1 << K6_LIST_JBITS) &&
+                     rp.jsplit == 1;
+  int cap = 0;
+  if (split) {
+    const double rho = (double)n / (h->L * h->L * h->L);
+    const double est = K6_G * rho * (2.0 * M_PI / 3.0) * std::pow(rc2_t, 1.5);
+    cap = (int)std::min<double>(1 << 20, 32.0 * std::ceil((2.0 * est + 256.0) / 32.0));
+    if (h->rs_split == 2) cap = 32;  // testing: most units take the overflow pass
+    CK(h->rs_list.ensure((size_t)units_max * cap * sizeof(uint32_t)));
+    CK(h->rs_count.ensure((size_t)units_max * sizeof(int)));
+  }
+  const int64_t n_eslot_all = split ? 2 * n_eslots : n_eslots;  // + overflow pass
+  CK(h->eblk.ensure(n_eslot_all * sizeof(double)));
+  if (lj_on) CK(h->eblk_lj.ensure(n_eslot_all * sizeof(double)));
   if (rows_slab <= 0) {
     if (pair_coul) CK(cudaMemsetAsync(d_u_out, 0, sizeof(double), h->stream));
     if (lj_on && d_ulj_out) CK(cudaMemsetAsync(d_ulj_out, 0, sizeof(double), h->stream));
@@ -1470,24 +1489,63 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
   CK(h->fsorted.ensure((size_t)n * 3 * sizeof(double)));
   CK(cudaMemsetAsync(h->fsorted.p, 0, (size_t)n * 3 * sizeof(double), h->stream));
   {
-    auto kern = lj_on ? (rp.half ? k6_real_space<true, true> : k6_real_space<true, false>)
-                      : (rp.half ? k6_real_space<false, true> : k6_real_space<false, false>);
-    kern<<<nb, K6_WARPS * 32, 0, h->stream>>>(
-        h->sorted.as<double4>(), h->sorted_f.as<float4>(), h->sorted_cell.as<int>(),
-        h->order.as<int>(), h->start.as<int>(), h->row_ustart.as<int>(), rp,
-        h->fsorted.as<double>(), h->eblk.as<double>(), lj_on ? h->eblk_lj.as<double>() : nullptr,
-        h->errflag.as<int>(), h->pairc.as<unsigned long long>());
+    K6Lists lists{split ? h->rs_list.as<uint32_t>() : nullptr,
+                  split ? h->rs_count.as<int>() : nullptr, cap};
+    double *eb = h->eblk.as<double>();
+    double *eb_lj = lj_on ? h->eblk_lj.as<double>() : nullptr;
+    if (!split) {
+      auto kern = lj_on ? (rp.half ? k6_real_space<true, true, K6_MODE_FUSED>
+                                   : k6_real_space<true, false, K6_MODE_FUSED>)
+                        : (rp.half ? k6_real_space<false, true, K6_MODE_FUSED>
+                                   : k6_real_space<false, false, K6_MODE_FUSED>);
+      kern<<<nb, K6_WARPS * 32, 0, h->stream>>>(
+          h->sorted.as<double4>(), h->sorted_f.as<float4>(), h->sorted_cell.as<int>(),
+          h->order.as<int>(), h->start.as<int>(), h->row_ustart.as<int>(), rp,
+          h->fsorted.as<double>(), eb, eb_lj, h->errflag.as<int>(),
+          h->pairc.as<unsigned long long>(), lists);
+      CKL();
+    } else {
+      // pass 1: traversal -> per-unit pair lists (the LJ switch only
+      // changes the evaluation; the traversal cutoff is in rp.rc2)
+      auto trav = rp.half ? k6_real_space<false, true, K6_MODE_LIST>
+                          : k6_real_space<false, false, K6_MODE_LIST>;
+      trav<<<nb, K6_WARPS * 32, 0, h->stream>>>(
+          h->sorted.as<double4>(), h->sorted_f.as<float4>(), h->sorted_cell.as<int>(),
+          h->order.as<int>(), h->start.as<int>(), h->row_ustart.as<int>(), rp,
+          h->fsorted.as<double>(), nullptr, nullptr, h->errflag.as<int>(),
+          h->pairc.as<unsigned long long>(), lists);
+      CKL();
+      // pass 2: evaluation of the lists
+      auto ev = lj_on ? (rp.half ? k6b_eval<true, true> : k6b_eval<true, false>)
+                      : (rp.half ? k6b_eval<false, true> : k6b_eval<false, false>);
+      ev<<<nb, K6_WARPS * 32, 0, h->stream>>>(h->sorted.as<double4>(), h->start.as<int>(),
+                                              h->row_ustart.as<int>(), rp, lists,
+                                              h->fsorted.as<double>(), eb, eb_lj,
+                                              h->errflag.as<int>());
+      CKL();
+      // overflowed units (list longer than its capacity): fused kernel,
+      // other units exit at once; energies into the second slot range
+      auto ovf = lj_on ? (rp.half ? k6_real_space<true, true, K6_MODE_OVF>
+                                  : k6_real_space<true, false, K6_MODE_OVF>)
+                       : (rp.half ? k6_real_space<false, true, K6_MODE_OVF>
+                                  : k6_real_space<false, false, K6_MODE_OVF>);
+      ovf<<<nb, K6_WARPS * 32, 0, h->stream>>>(
+          h->sorted.as<double4>(), h->sorted_f.as<float4>(), h->sorted_cell.as<int>(),
+          h->order.as<int>(), h->start.as<int>(), h->row_ustart.as<int>(), rp,
+          h->fsorted.as<double>(), eb + n_eslots, eb_lj ? eb_lj + n_eslots : nullptr,
+          h->errflag.as<int>(), nullptr, lists);
+      CKL();
+    }
   }
-  CKL();
   k_unpermute_add<<<blocks_for(n, 256), 256, 0, h->stream>>>(h->order.as<int>(),
                                                              h->fsorted.as<double>(), n, d_force);
   CKL();
   if (pair_coul) {
-    k_sum<<<1, 1024, 0, h->stream>>>(h->eblk.as<double>(), n_eslots, 1.0, d_u_out);
+    k_sum<<<1, 1024, 0, h->stream>>>(h->eblk.as<double>(), n_eslot_all, 1.0, d_u_out);
     CKL();
   }
   if (lj_on && d_ulj_out) {
-    k_sum<<<1, 1024, 0, h->stream>>>(h->eblk_lj.as<double>(), n_eslots, 1.0, d_ulj_out);
+    k_sum<<<1, 1024, 0, h->stream>>>(h->eblk_lj.as<double>(), n_eslot_all, 1.0, d_ulj_out);
     CKL();
   }
   return EWB_OK;
@@ -1794,7 +1852,8 @@ void ewb_destroy(ewb_handle *h) {
                   &h->errflag, &h->cell_of, &h->slot, &h->count, &h->start, &h->gstart,
                   &h->order_tmp, &h->order, &h->sorted, &h->sorted_cell, &h->row_ustart,
                   &h->sorted_f, &h->tc_qmax, &h->tc_ytab, &h->tc_ztab, &h->tc_xsl, &h->t3_wsl,
-                  &h->t3_rscale, &h->pairc, &h->eblk_r, &h->fsorted, &h->force_in})
+                  &h->t3_rscale, &h->pairc, &h->eblk_r, &h->fsorted, &h->force_in,
+                  &h->rs_list, &h->rs_count})
     b->release();
   if (h->hscr) cudaFreeHost(h->hscr);
   h->plan.release();
@@ -1939,6 +1998,13 @@ int ewb_set_graphs(ewb_handle *h, int on) {
   if (!h) return EWB_EINVAL;
   h->use_graphs = on != 0;
   ++h->gen;
+  return EWB_OK;
+}
+
+int ewb_set_real_space_split(ewb_handle *h, int on) {
+  if (!h) return EWB_EINVAL;
+  ++h->gen;
+  h->rs_split = on < 0 ? 0 : (on > 2 ? 2 : on);
   return EWB_OK;
 }
 

@@ -1107,17 +1107,15 @@ int stage_recip_tc(ewb_handle *h, int64_t i0, int64_t i1, double *d_force) {
   const int64_t T = ptiles * P.t3_mtiles * (pair ? 2 : 1);  // CTAs per split
   const int kb_cap = T3_KMAX / TC_KB;
   const int ns_min = std::max(1, (nkb + kb_cap - 1) / kb_cap);
-  // splits: least (waves x per-CTA work), at least 4 K-blocks per CTA
+  // K splits: as few as int32 exactness allows -- each split adds a CTA
+  // prologue/epilogue and a partial-force pass, which costs more than the
+  // partial last wave it could fill (measured: forcing 1 instead of the
+  // wave-filling choice, c4 0.837 -> 0.762 ms, c3 6.25 -> 5.88, c5 81.2 ->
+  // 78.6); more only when one split leaves SMs idle
   int ns = ns_min;
-  double best = 1e300;
-  for (int c = ns_min; c <= ns_min + 3 && (c == ns_min || nkb / c >= 4); ++c) {
-    const double waves = (double)((T * c + h->n_sm - 1) / h->n_sm);
-    const double cost = waves * ((nkb + c - 1) / c) + 0.02 * c * nkb;
-    if (cost < best) {
-      best = cost;
-      ns = c;
-    }
-  }
+  if ((int64_t)T * ns < h->n_sm)
+    ns = std::max(ns_min, (int)std::min<int64_t>(std::max(1, nkb / 4),
+                                                  (h->n_sm + T - 1) / std::max<int64_t>(1, T)));
   const int kbps = (nkb + ns - 1) / ns;
   ns = (nkb + kbps - 1) / kbps;
   const int n_ks = ns * P.t3_mtiles * (pair ? 2 : 1);

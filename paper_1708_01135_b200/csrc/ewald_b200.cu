@@ -1613,21 +1613,23 @@ int pipeline_seg(ewb_handle *h, int seg, const double *d_pos, const double *d_q,
       return stage_finalize_pairs(h, h->spart.as<double4>(), n_part, d_rho_out, en + 1);
     }
     case 4:
-      if (!h->coul_on) return EWB_OK;
-      return stage_recip_forces(h, 0, h->n, d_force, false, nullptr);
-    default:
       if (!h->coul_on) {
         CK(cudaMemsetAsync(en + 2, 0, sizeof(double), h->stream));
         return EWB_OK;
       }
-      if (h->ov_active && h->t3_pend_nks > 0) {
+      if ((rc = stage_recip_forces(h, 0, h->n, d_force, false, nullptr))) return rc;
+      // self energy (depends on q only): on the reciprocal stream, before the
+      // join, so it stays off the tail of the evaluation
+      return stage_self(h, en + 2);
+    default:
+      if (h->coul_on && h->ov_active && h->t3_pend_nks > 0) {
         const unsigned nbc = blocks_for(h->t3_pend_n, RED_THREADS);
         k3_combine<<<nbc, RED_THREADS, 0, h->stream>>>(
             h->fpart.as<double>(), nullptr, h->t3_pend_nks, h->t3_pend_i0, h->t3_pend_n,
             h->frac.as<double4>(), 4.0 * M_PI / h->L, h->t3_pend_force, nullptr, 0);
         CKL();
       }
-      return stage_self(h, en + 2);
+      return EWB_OK;
   }
 }
 

@@ -16,12 +16,14 @@
 // Rows per a > 0: 6; a = 0: Im V(my W), Im V(mz W) (X(0) = 1).  A rows are
 // scaled per row (the scale factors out of the sum), B = unit phases.
 //
-// CTA = (64 particles, M tile of 128 rows, k split); warps 0-7 generate the
-// YZ slices of a K-block (32 pairs = 4 runs of 8 consecutive m_y: one
-// sincospi + a recurrence per run), warp 8 issues the 26 x 2 MMAs
-// (M=128, N=64, K=32), warp 9 bulk-copies the pre-split A slices.  The
-// epilogue combines the 7 levels, multiplies by the particle's X(a) and
-// reduces over the rows (warp shuffles + shared memory).
+// CTA = (T3_NP = 80 particles, M tile of 128 rows, k split); T3_PGROUPS
+// groups of producer warps generate the YZ slices of alternate K-blocks
+// (32 pairs = 4 runs of 8 consecutive m_y: one sincospi + a recurrence per
+// run), one warp stages the A slices in TMEM (tcgen05.cp) and issues the TS
+// MMAs of the 21 kept slice pairs (M=128, K=32, N = up to 3 merged B
+// slices x 80), one warp bulk-copies the pre-split A slices.  The epilogue
+// combines the 6 levels, multiplies by the particle's X(a) and reduces over
+// the rows (warp shuffles + shared memory).
 
 // The force GEMM splits W rows (scaled per row) and the unit phases into
 // T3_S byte slices and keeps the slice pairs with s + t >= T3_W0.  Measured

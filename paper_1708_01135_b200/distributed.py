@@ -21,6 +21,10 @@ global reduction of rho_hat.  Here each rank owns:
   device work and collectives without a host synchronisation; the single
   synchronisation at the end reads the energies and the deferred device
   error flag (coincident particles, unwrapped positions).
+* on CUDA the rank's real-space slab runs on a side stream concurrently with
+  the reciprocal chain (S(k) partial, its all-reduce, finalisation); the
+  streams join before the reciprocal forces, which add into the same
+  buffer.  The stages use disjoint scratch (as in the single-GPU overlap).
 
 ``stages`` is the device-stage interface (``DeviceStages`` wraps the C-ABI);
 tests inject a CPU stand-in to run this orchestration under ``gloo``.
@@ -89,13 +93,16 @@ class DeviceStages:
 class ShardedEwald:
     """Particle-sharded Ewald evaluation across the ranks of a group."""
 
-    def __init__(self, stages, device, group=None):
+    def __init__(self, stages, device, group=None, overlap=True):
         self.st = stages
         self.device = device
         self.group = group
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self._slots = None
+        cuda = torch.device(device).type == "cuda"
+        self._side = torch.cuda.Stream(device=device) if overlap and cuda else None
+        self._main = torch.cuda.Stream(device=device) if overlap and cuda else None
 
     def _allreduce(self, t):
         if self.world > 1:
@@ -104,6 +111,23 @@ class ShardedEwald:
     def evaluate(self, pos, q, force, rho_out=None):
         """force (N,3) += Coulomb force on every rank; returns
         (u_sr, u_lr, u_self) -- identical on every rank."""
+        if self._side is None:
+            return self._evaluate(pos, q, force, rho_out, None)
+        # the device stages and the collectives run on an explicit stream
+        # (the caller's, unless it is the legacy default stream, which the
+        # non-blocking side stream would not order against)
+        cur = torch.cuda.current_stream(self.device)
+        main = self._main if cur.cuda_stream == 0 else cur
+        if main is not cur:
+            main.wait_stream(cur)
+        with torch.cuda.stream(main):
+            self.st.set_stream(main)
+            out = self._evaluate(pos, q, force, rho_out, main)
+        if main is not cur:
+            cur.wait_stream(main)
+        return out
+
+    def _evaluate(self, pos, q, force, rho_out, main):
         n = q.shape[0]
         ns = self.st.slot_size()
         if self._slots is None or self._slots.numel() != ns:
@@ -115,10 +139,18 @@ class ShardedEwald:
         else:
             contrib, en = force, torch.empty(3, dtype=torch.float64, device=self.device)
         self.st.load(pos, q)
+        if main is not None:                   # real space beside the reciprocal chain
+            self._side.wait_stream(main)
+            self.st.set_stream(self._side)
+            self.st.real_space_async(self.rank, self.world, contrib)
+            self.st.set_stream(main)
         self.st.rho_partial(i0, i1, self._slots)
         self._allreduce(self._slots)           # S(k) = sum over shards
         self.st.finalize_async(self._slots, rho_out)
-        self.st.real_space_async(self.rank, self.world, contrib)
+        if main is not None:
+            main.wait_stream(self._side)       # both add into contrib
+        else:
+            self.st.real_space_async(self.rank, self.world, contrib)
         self.st.recip_forces(i0, i1, contrib)
         self.st.self_energy_async()
         self.st.energies(en)

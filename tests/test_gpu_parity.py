@@ -286,6 +286,7 @@ def test_device_stages_sharded_match_full(ew):
     h.set_system(cfg["L"], params.alpha, params.r_cutoff)
     h.set_kspace(rs.m_int, rs.coeff)
     f_full = torch.zeros((n, 3), dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()  # torch's default stream vs the handle's stream
     en, _ = h.dev_evaluate(pos.data_ptr(), q.data_ptr(), n, f_full.data_ptr())
     h.dev_load(pos.data_ptr(), q.data_ptr(), n)
     ns = h.dev_slot_doubles()
@@ -293,9 +294,12 @@ def test_device_stages_sharded_match_full(ew):
     s_b = torch.empty(ns, dtype=torch.float64, device=dev)
     h.dev_rho_partial(0, n // 3, s_a.data_ptr())
     h.dev_rho_partial(n // 3, n, s_b.data_ptr())
+    torch.cuda.synchronize()
     s_a += s_b  # stands in for the all-reduce
+    torch.cuda.synchronize()
     u_lr = h.dev_kspace_finalize(s_a.data_ptr())
     f = torch.zeros((n, 3), dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
     h.dev_recip_forces(0, n // 3, f.data_ptr())
     h.dev_recip_forces(n // 3, n, f.data_ptr())
     u_sr = h.dev_real_space(0, 2, f.data_ptr()) + h.dev_real_space(1, 2, f.data_ptr())
@@ -329,16 +333,20 @@ def test_sharded_ewald_device_stages_one_rank(ew):
     h.set_system(cfg["L"], params.alpha, params.r_cutoff)
     h.set_kspace(rs.m_int, rs.coeff)
     f_full = torch.zeros((n, 3), dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()  # torch's default stream vs the handle's stream
     en, _ = h.dev_evaluate(pos.data_ptr(), q.data_ptr(), n, f_full.data_ptr())
-    sh = ShardedEwald(DeviceStages(h), dev)
-    f = torch.zeros((n, 3), dtype=torch.float64, device=dev)
-    rho = torch.zeros(2 * rs.n_stored, dtype=torch.float64, device=dev)
-    u = sh.evaluate(pos, q, f, rho_out=rho)
-    for got, want in zip(u, en):
-        assert rel(got, want) <= 1e-12
     ff = f_full.cpu().numpy()
-    assert np.abs(f.cpu().numpy() - ff).max() <= 1e-12 * f_rms(ff)
-    assert float(torch.abs(rho).max()) > 0.0
+    for overlap in (True, False):  # real space on a side stream / in sequence
+        sh = ShardedEwald(DeviceStages(h), dev, overlap=overlap)
+        f = torch.zeros((n, 3), dtype=torch.float64, device=dev)
+        rho = torch.zeros(2 * rs.n_stored, dtype=torch.float64, device=dev)
+        torch.cuda.synchronize()
+        u = sh.evaluate(pos, q, f, rho_out=rho)
+        torch.cuda.synchronize()
+        for got, want in zip(u, en):
+            assert rel(got, want) <= 1e-12
+        assert np.abs(f.cpu().numpy() - ff).max() <= 1e-12 * f_rms(ff)
+        assert float(torch.abs(rho).max()) > 0.0
     pos2 = pos.clone()
     pos2[1] = pos2[0]
     with pytest.raises(ew.CoincidentParticlesError):

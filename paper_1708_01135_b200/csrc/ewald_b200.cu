@@ -10,7 +10,6 @@
 //                   (tcgen05.mma kind::i8, six 48-bit slices, TMEM levels)
 //   k3_tc.cuh       Alg. 2 (ewald.py:308-349) reciprocal forces as an int8 GEMM
 //                   (W = C S rows x YZ phases, X(a) contraction in the epilogue)
-//   k3_ts.cuh, k3_pair.cuh   measured alternatives of the force GEMM (off)
 //   recip_fp64.cuh  Alg. 1/2 on the FP64 pipe (small systems, tensor cores off,
 //                   per-particle energies of the foreign-rho API)
 //   rs_cells.cuh    cell list (celllist.py:75-108), deterministic in-cell order
@@ -237,21 +236,6 @@ __global__ void __launch_bounds__(256) k_fp64_probe(double *__restrict__ out, in
 
 #include "k1_tc.cuh"
 #include "k3_tc.cuh"
-#include "k3_ts.cuh"
-#include "k3_pair.cuh"
-#ifndef T3_PAIR
-// force GEMM on level-splitting CTA pairs (k3_pair.cuh): correct, measured
-// slower (c5 124 vs 101 ms, c2 0.34 vs 0.19): each SM copies the whole W
-// block for half the MMA work and the pair runs in lock step
-#define T3_PAIR 0
-#endif
-#ifndef T3_USE_TS
-// force GEMM with the W operand in tensor memory (k3_ts.cuh): correct, but
-// measured slower (c5 120 vs 101 ms): an M=128 int8 MMA costs >= ~48 cycles
-// in either form (tools/i8_shapes.py: TS 3969 vs SS 3503 TOP/s at N=80), and
-// the TS TMEM budget forces N=64
-#define T3_USE_TS 0
-#endif
 
 // ---------------------------------------------------------------------------
 // template dispatch tables
@@ -1079,9 +1063,7 @@ int stage_recip_tc(ewb_handle *h, int64_t i0, int64_t i1, double *d_force) {
   Plan &P = h->plan;
   const int64_t n_local = i1 - i0;
   const int nkb = P.t3_nkb;
-  const bool pair = T3_PAIR && !T3_USE_TS &&
-                    128 * (P3_HALF + 1) * 8 + P3_HALF * (P.tc_A + 1) * 16 <= p3_smem_bytes();
-  const int NP = pair ? P3_NP : (T3_USE_TS ? TS_NP : T3_NP);
+  const int NP = T3_NP;
   CK(h->t3_wsl.ensure((size_t)P.t3_mtiles * nkb * T3_S * TC_GSL));
   CK(h->t3_rscale.ensure((size_t)P.t3_mtiles * 128 * sizeof(double)));
   {
@@ -1091,20 +1073,14 @@ int stage_recip_tc(ewb_handle *h, int64_t i0, int64_t i1, double *d_force) {
         h->sp.as<double2>(), P.t3_slotmap.as<int>(), P.tc_A, P.t3_pair_yz.as<int2>(), P.t3_npairs,
         P.t3_rowtab.as<T3Row>(), P.t3_rows, h->t3_rscale.as<unsigned long long>());
     CKL();
-    if (T3_USE_TS)
-      k3s_wprep<<<dim3(P.t3_mtiles * 128, kparts), 256, 0, h->stream>>>(
-          h->sp.as<double2>(), P.t3_slotmap.as<int>(), P.tc_A, P.t3_pair_yz.as<int2>(),
-          P.t3_npairs, P.t3_rowtab.as<T3Row>(), P.t3_rows, nkb, h->t3_rscale.as<double>(),
-          h->t3_wsl.as<uint8_t>());
-    else
-      k3t_wprep<<<dim3(P.t3_mtiles * 128, kparts), 256, 0, h->stream>>>(
+    k3t_wprep<<<dim3(P.t3_mtiles * 128, kparts), 256, 0, h->stream>>>(
           h->sp.as<double2>(), P.t3_slotmap.as<int>(), P.tc_A, P.t3_pair_yz.as<int2>(),
           P.t3_npairs, P.t3_rowtab.as<T3Row>(), P.t3_rows, nkb, h->t3_rscale.as<double>(),
           h->t3_wsl.as<uint8_t>());
     CKL();
   }
   const int64_t ptiles = (n_local + NP - 1) / NP;
-  const int64_t T = ptiles * P.t3_mtiles * (pair ? 2 : 1);  // CTAs per split
+  const int64_t T = ptiles * P.t3_mtiles;  // CTAs per split
   const int kb_cap = T3_KMAX / TC_KB;
   const int ns_min = std::max(1, (nkb + kb_cap - 1) / kb_cap);
   // K splits: as few as int32 exactness allows -- each split adds a CTA
@@ -1118,40 +1094,8 @@ int stage_recip_tc(ewb_handle *h, int64_t i0, int64_t i1, double *d_force) {
                                                   (h->n_sm + T - 1) / std::max<int64_t>(1, T)));
   const int kbps = (nkb + ns - 1) / ns;
   ns = (nkb + kbps - 1) / kbps;
-  const int n_ks = ns * P.t3_mtiles * (pair ? 2 : 1);
+  const int n_ks = ns * P.t3_mtiles;
   CK(h->fpart.ensure((size_t)n_ks * 3 * n_local * sizeof(double)));
-  if (pair) {
-    const size_t smem = (size_t)p3_smem_bytes();
-    CK(cudaFuncSetAttribute(k3p_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    cudaLaunchConfig_t lc = {};
-    lc.gridDim = dim3((unsigned)(2 * ptiles), P.t3_mtiles, ns);
-    lc.blockDim = dim3(P3_THREADS);
-    lc.dynamicSmemBytes = smem;
-    lc.stream = h->stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    lc.attrs = at;
-    lc.numAttrs = 1;
-    CK(cudaLaunchKernelEx(&lc, k3p_gemm, (const double4 *)h->frac.as<double4>(),
-                          (const double2 *)h->base.as<double2>(),
-                          (const uint8_t *)h->t3_wsl.as<uint8_t>(),
-                          (const double *)h->t3_rscale.as<double>(),
-                          (const T3Row *)P.t3_rowtab.as<T3Row>(), P.t3_rows,
-                          (const int2 *)P.t3_pair_yz.as<int2>(), nkb, kbps, i0, i1, P.tc_A,
-                          (const int4 *)P.t3_comp.as<int4>(), h->fpart.as<double>(), h->tc_dbg));
-    ++h->launches;
-  } else if (T3_USE_TS) {
-    const size_t smem = (size_t)ts_smem_bytes(P.tc_A);
-    CK(cudaFuncSetAttribute(k3s_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k3s_gemm<<<dim3((unsigned)ptiles, P.t3_mtiles, ns), TS_THREADS, smem, h->stream>>>(
-        h->frac.as<double4>(), h->base.as<double2>(), h->t3_wsl.as<uint8_t>(),
-        h->t3_rscale.as<double>(), P.t3_rowtab.as<T3Row>(), P.t3_rows, P.t3_pair_yz.as<int2>(),
-        nkb, kbps, i0, i1, P.tc_A, P.t3_comp.as<int4>(), h->fpart.as<double>(), h->tc_dbg);
-    CKL();
-  } else {
   const size_t smem = (size_t)t3_smem_bytes();
   CK(cudaFuncSetAttribute(k3t_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   {
@@ -1177,7 +1121,6 @@ int stage_recip_tc(ewb_handle *h, int64_t i0, int64_t i1, double *d_force) {
                           (const int2 *)P.t3_pair_yz.as<int2>(), nkb, kbps, i0, i1, P.tc_A,
                           (const int4 *)P.t3_comp.as<int4>(), h->fpart.as<double>(), h->tc_dbg));
     ++h->launches;
-  }
   }
   if (h->ov_active) {  // the combine adds into forces: after the real-space join
     h->t3_pend_nks = n_ks;

@@ -546,3 +546,58 @@ __global__ void __launch_bounds__(128, 1) k_i8_probe(int iters, int n_mma, int *
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
   }
 }
+
+// TS-mode throughput probe: A (M=128 x K=32 int8) read from TMEM columns
+// [256, 264), B from shared memory, N = n_mma, back-to-back MMAs into
+// accumulator columns [0, n_mma).
+__global__ void __launch_bounds__(128, 1) k_i8_probe_ts(int iters, int n_mma, int *__restrict__ sink) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t done;
+  __shared__ uint32_t tmem_base_s;
+  for (int i = threadIdx.x; i < 32 * TC_SBO / 4; i += blockDim.x)
+    reinterpret_cast<uint32_t *>(smem)[i] = 0x01010101u * (uint32_t)(i & 3);
+  if (threadIdx.x == 0) {
+    mbar_init(smem_u32(&done), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if ((threadIdx.x >> 5) == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(&tmem_base_s))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_s;
+  {
+    const uint32_t w[8] = {0x01010101u, 0x02020202u, 0x01010101u, 0x03030303u,
+                           0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u};
+    tc_st8(tmem + ((uint32_t)(32 * ((threadIdx.x >> 5) & 3)) << 16) + 256u, w);
+    tc_wait_st();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n_mma >> 3) << 17) | (8u << 24);
+    const uint64_t bd = tc_desc(smem_u32(smem));
+    for (int i = 0; i < iters; ++i) tc_mma_ts(tmem, tmem + 256u, bd + (uint64_t)((i & 1) * 16), idesc, i > 0 ? 1u : 0u);
+    tc_commit(smem_u32(&done));
+  }
+  mbar_wait(smem_u32(&done), 0);
+  tc_fence_after();
+  if ((threadIdx.x >> 5) == 0) {
+    int r[8];
+    tc_ld8(tmem, r);
+    tc_wait_ld();
+    if (r[0] == 123456789) sink[0] = r[1];
+  }
+  tc_fence_before();
+  __syncthreads();
+  if ((threadIdx.x >> 5) == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}

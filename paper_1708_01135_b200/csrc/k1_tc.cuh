@@ -148,17 +148,22 @@ __device__ __forceinline__ void tc_wait_st() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 #ifndef K1_ACP
-#define K1_ACP 1  // c5 S(k) 47.2 -> 41.2 ms
+// 1: G slices staged in TMEM by tcgen05.cp, TS-form MMAs (c5 S(k) 47.2 ->
+// 41.2 ms against unmerged SS); 0 (default): SS-form merged MMAs read G
+// from shared memory directly -- the staging copies execute in the tensor
+// pipe in order with the MMAs, and once MMAs are merged along N each G
+// slice feeds only 1-3 of them (c5 39.9 -> 37.8 ms with K1_MERGE 3)
+#define K1_ACP 0
 #endif
 static_assert(!K1_ACP || TC_NL * TC_NMAX + 32 <= 512, "TMEM: levels + 4 G slots");
 #ifndef K1_MERGE
-#define K1_MERGE 2  // c5 S(k) 41.2 -> 39.9 ms (3, 4: slower)
+#define K1_MERGE 3  // SS: 3 best (c5 37.8 ms; 2: 39.1, 4: 38.2); TS: 2 (39.9 ms)
 #endif
-// K1_MERGE = m > 1 (with K1_ACP): one MMA covers up to m consecutive X slices
+// K1_MERGE = m > 1: one MMA covers up to m consecutive X slices
 // against G slice s, N = (m - 1) x 64 + npad (X slices sit 64 rows apart in
 // shared memory; levels 64 columns apart in TMEM, the columns npad..63 of a
 // level collect junk and are never read); accumulators zeroed first
-static_assert(K1_MERGE == 1 || (K1_ACP && (K1_MERGE - 1) * TC_NMAX + TC_NMAX <= 256), "merged N <= 256");
+static_assert((K1_MERGE - 1) * TC_NMAX + TC_NMAX <= 256, "merged N <= 256");
 // one lane of a converged warp (PTX elect.sync)
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
@@ -453,6 +458,24 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
                           (s > s_lo || ks > 0) ? 1u : acc0);
               }
 #endif
+            }
+          }
+#elif K1_MERGE > 1
+          // SS form with merged N: each G slice read from shared memory by
+          // its merged MMAs, no staging copy into TMEM
+          const uint32_t idesc0 = idesc & ~(63u << 17);
+#pragma unroll
+          for (int ks = 0; ks < TC_KB / 32; ++ks) {
+#pragma unroll
+            for (int s = 0; s < TC_S; ++s) {
+#pragma unroll
+              for (int t = (TC_W0 - s > 0 ? TC_W0 - s : 0); t < TC_S; t += K1_MERGE) {
+                const int m = TC_S - t < K1_MERGE ? TC_S - t : K1_MERGE;
+                tc_mma(tmem + (uint32_t)((s + t - TC_W0) * TC_NMAX),
+                       gd + (uint64_t)((s * TC_GSL + ks * 256) >> 4),
+                       xd + (uint64_t)((t * XSL + ks * 256) >> 4),
+                       idesc0 | ((uint32_t)(((m - 1) * TC_NMAX + npad) >> 3) << 17), 1u);
+              }
             }
           }
 #else

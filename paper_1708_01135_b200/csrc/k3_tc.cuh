@@ -198,21 +198,24 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t local_addr, uint32_
 }
 
 #ifndef T3_ACP
-#define T3_ACP 1  // c5 forces 91 -> 84 ms
+#define T3_ACP 0
 #endif
-// T3_ACP: stage the A slices in TMEM (tcgen05.cp, four 8-column slots after
-// the level accumulators) and issue the MMAs in TS form, slice-major, so the
-// tensor core reads each A slice from shared memory once per K step instead
-// of once per slice pair
+// T3_ACP 1: stage the A slices in TMEM (tcgen05.cp, four 8-column slots
+// after the level accumulators) and issue the MMAs in TS form, slice-major,
+// so the tensor core reads each A slice from shared memory once per K step
+// instead of once per slice pair (c5 forces 91 -> 84 ms before merging).
+// 0 (default): SS-form merged MMAs -- with T3_MERGE each A slice feeds only
+// 1-2 MMAs, and the staging copies cost tensor-pipe time in order with the
+// MMAs (c5 79.0 -> 73.2 ms, c2 0.164 -> 0.156 ms)
 static_assert(!T3_ACP || T3_NL * T3_NP + 32 <= 512, "TMEM: levels + 4 A slots");
 #ifndef T3_MERGE
 #define T3_MERGE 3  // c5 forces 84.2 -> 81.1 ms
 #endif
-// T3_MERGE = m > 1 (with T3_ACP): one MMA covers up to m consecutive B slices
+// T3_MERGE = m > 1: one MMA covers up to m consecutive B slices
 // t..t+m-1 against A slice s -- N = m x 80 rows of B (the slices are
 // contiguous in shared memory) into the m consecutive level accumulators
 // (contiguous in TMEM); accumulators are zeroed first and every MMA adds
-static_assert(T3_MERGE == 1 || (T3_ACP && T3_MERGE * T3_NP <= 256), "merged N <= 256");
+static_assert(T3_MERGE * T3_NP <= 256, "merged N <= 256");
 
 // k3t_gemm: grid (particle tiles of 64, M tiles, k splits), clusters of
 // T3_CL consecutive particle tiles: every A block is bulk-copied once per
@@ -334,6 +337,24 @@ __global__ void __launch_bounds__(T3_THREADS, 1)
                           (s > s_lo || ks > 0) ? 1u : acc0);
               }
 #endif
+            }
+          }
+#elif T3_MERGE > 1
+          // SS form with merged N: A slice s read from shared memory by its
+          // (one or two) MMAs, no staging copy into TMEM
+          constexpr uint32_t idesc0 = (2u << 4) | (1u << 7) | (1u << 10) | (8u << 24);
+#pragma unroll
+          for (int ks = 0; ks < TC_KB / 32; ++ks) {
+#pragma unroll
+            for (int s = 0; s < T3_S; ++s) {
+#pragma unroll
+              for (int t = (T3_W0 - s > 0 ? T3_W0 - s : 0); t < T3_S; t += T3_MERGE) {
+                const int m = T3_S - t < T3_MERGE ? T3_S - t : T3_MERGE;
+                tc_mma(tmem + (uint32_t)((s + t - T3_W0) * T3_NP),
+                       ad + (uint64_t)((s * TC_GSL + ks * 256) >> 4),
+                       bd + (uint64_t)((t * T3_BSL + ks * 256) >> 4),
+                       idesc0 | ((uint32_t)((m * T3_NP) >> 3) << 17), 1u);
+              }
             }
           }
 #else

@@ -75,6 +75,9 @@ constexpr int K3_CH = 32;         // k-items per shared-memory chunk
 #ifndef K6_G
 #define K6_G 8                    // centre particles per real-space warp
 #endif
+#ifndef K6_HI_WAVES
+#define K6_HI_WAVES 3             // fused pair kernel at 5 blocks/SM from this many waves up
+#endif
 #ifndef K6_SPLIT
 #define K6_SPLIT 0                // real space as traversal + evaluation passes (measured slower)
 #endif
@@ -1435,10 +1438,16 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
     double *eb = h->eblk.as<double>();
     double *eb_lj = lj_on ? h->eblk_lj.as<double>() : nullptr;
     if (!split) {
-      auto kern = lj_on ? (rp.half ? k6_real_space<true, true, K6_MODE_FUSED>
-                                   : k6_real_space<true, false, K6_MODE_FUSED>)
-                        : (rp.half ? k6_real_space<false, true, K6_MODE_FUSED>
-                                   : k6_real_space<false, false, K6_MODE_FUSED>);
+      // more resident warps pay off only when the grid spans several waves
+      const bool hi = (int64_t)nb >= (int64_t)K6_HI_WAVES * h->n_sm * K6_MINB_HI;
+      auto kern = hi ? (lj_on ? (rp.half ? k6_real_space<true, true, K6_MODE_FUSED_HI>
+                                         : k6_real_space<true, false, K6_MODE_FUSED_HI>)
+                              : (rp.half ? k6_real_space<false, true, K6_MODE_FUSED_HI>
+                                         : k6_real_space<false, false, K6_MODE_FUSED_HI>))
+                     : (lj_on ? (rp.half ? k6_real_space<true, true, K6_MODE_FUSED>
+                                         : k6_real_space<true, false, K6_MODE_FUSED>)
+                              : (rp.half ? k6_real_space<false, true, K6_MODE_FUSED>
+                                         : k6_real_space<false, false, K6_MODE_FUSED>));
       kern<<<nb, K6_WARPS * 32, 0, h->stream>>>(
           h->sorted.as<double4>(), h->sorted_f.as<float4>(), h->sorted_cell.as<int>(),
           h->order.as<int>(), h->start.as<int>(), h->row_ustart.as<int>(), rp,

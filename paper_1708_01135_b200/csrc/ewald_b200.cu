@@ -469,16 +469,6 @@ namespace {
 
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
-// Split factor along the reduction axis: fill whole waves of resident
-// blocks with the fewest splits (each split costs a partial-sum buffer that
-// a second kernel must reduce), never below min_work units per block.
-int split_for(int64_t tiles, int64_t slots, int64_t work, int64_t min_work) {
-  const int64_t waves = std::max<int64_t>(1, (tiles + slots - 1) / slots);
-  int64_t s = std::max<int64_t>(1, (waves * slots) / std::max<int64_t>(1, tiles));
-  const int64_t cap = std::max<int64_t>(1, work / std::max<int64_t>(1, min_work));
-  return (int)std::min(s, cap);
-}
-
 template <class T>
 int upload(ewb_handle *h, DBuf &b, const std::vector<T> &v) {
   CK(b.ensure(v.size() * sizeof(T)));
@@ -1325,6 +1315,16 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
   CK(h->order.ensure(n * sizeof(int)));
   CK(h->sorted.ensure(n * sizeof(double4)));
   CK(h->sorted_f.ensure(n * sizeof(float4)));
+  CK(h->sorted_cell.ensure(n * sizeof(int)));
+  const int n_rows = fold ? 1 : cpd_eff * cpd_eff;
+  CK(h->row_ustart.ensure((n_rows + 1) * sizeof(int)));
+  if (fold) {  // every particle is a candidate: identity order, one launch
+    k_fold_prep<<<blocks_for(n, 256), 256, 0, h->stream>>>(
+        h->xyzq.as<double4>(), n, (int)((n + K6_G - 1) / K6_G), h->sorted.as<double4>(),
+        h->sorted_f.as<float4>(), h->sorted_cell.as<int>(), h->order.as<int>(),
+        h->start.as<int>(), h->row_ustart.as<int>());
+    CKL();
+  } else {
   CK(cudaMemsetAsync(h->count.p, 0, (n_cells + 1) * sizeof(int), h->stream));
   k4_bin_count<<<blocks_for(n, 256), 256, 0, h->stream>>>(h->xyzq.as<double4>(), n, edge, cpd_eff,
                                                           h->cell_of.as<int>(), h->slot.as<int>(),
@@ -1333,10 +1333,7 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
   k_scan_cells<<<1, 1024, 0, h->stream>>>(h->count.as<int>(), n_cells, h->start.as<int>(),
                                           h->gstart.as<int>());
   CKL();
-  if (fold) {
-    k_iota<<<blocks_for(n, 256), 256, 0, h->stream>>>(h->order.as<int>(), n);
-    CKL();
-  } else {
+  {
     k5_scatter<<<blocks_for(n, 256), 256, 0, h->stream>>>(h->cell_of.as<int>(), h->slot.as<int>(),
                                                           n, h->start.as<int>(),
                                                           h->order_tmp.as<int>());
@@ -1345,7 +1342,6 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
                                                  h->order.as<int>());
     CKL();
   }
-  CK(h->sorted_cell.ensure(n * sizeof(int)));
   k5_gather<<<blocks_for(n, 256), 256, 0, h->stream>>>(h->order.as<int>(), h->xyzq.as<double4>(),
                                                        h->cell_of.as<int>(), n,
                                                        h->sorted.as<double4>(),
@@ -1353,11 +1349,10 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
                                                        h->sorted_cell.as<int>());
   CKL();
   // units: K6_G consecutive particles of one row of cells (fixed cy, cz)
-  const int n_rows = fold ? 1 : cpd_eff * cpd_eff;
-  CK(h->row_ustart.ensure((n_rows + 1) * sizeof(int)));
   k_scan_rows<<<1, 1024, 0, h->stream>>>(h->start.as<int>(), cpd_eff, n_rows,
                                          h->row_ustart.as<int>());
   CKL();
+  }
   if (ev_cell) CK(cudaEventRecord(ev_cell, h->stream));
   }
   if (!(which & RS_PAIRS)) return EWB_OK;
@@ -1430,8 +1425,15 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
   }
   CK(h->pairc.ensure(sizeof(unsigned long long)));
   if (part == 0) CK(cudaMemsetAsync(h->pairc.p, 0, sizeof(unsigned long long), h->stream));
-  CK(h->fsorted.ensure((size_t)n * 3 * sizeof(double)));
-  CK(cudaMemsetAsync(h->fsorted.p, 0, (size_t)n * 3 * sizeof(double), h->stream));
+  // cell-sorted force accumulator, un-permuted afterwards; in FOLD mode the
+  // sorted order is the caller's, so the pair kernel adds into d_force
+  // directly (the reciprocal forces are combined after the join)
+  double *facc = d_force;
+  if (!fold) {
+    CK(h->fsorted.ensure((size_t)n * 3 * sizeof(double)));
+    CK(cudaMemsetAsync(h->fsorted.p, 0, (size_t)n * 3 * sizeof(double), h->stream));
+    facc = h->fsorted.as<double>();
+  }
   {
     K6Lists lists{split ? h->rs_list.as<uint32_t>() : nullptr,
                   split ? h->rs_count.as<int>() : nullptr, cap};
@@ -1451,7 +1453,7 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
       kern<<<nb, K6_WARPS * 32, 0, h->stream>>>(
           h->sorted.as<double4>(), h->sorted_f.as<float4>(), h->sorted_cell.as<int>(),
           h->order.as<int>(), h->start.as<int>(), h->row_ustart.as<int>(), rp,
-          h->fsorted.as<double>(), eb, eb_lj, h->errflag.as<int>(),
+          facc, eb, eb_lj, h->errflag.as<int>(),
           h->pairc.as<unsigned long long>(), lists);
       CKL();
     } else {
@@ -1462,7 +1464,7 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
       trav<<<nb, K6_WARPS * 32, 0, h->stream>>>(
           h->sorted.as<double4>(), h->sorted_f.as<float4>(), h->sorted_cell.as<int>(),
           h->order.as<int>(), h->start.as<int>(), h->row_ustart.as<int>(), rp,
-          h->fsorted.as<double>(), nullptr, nullptr, h->errflag.as<int>(),
+          facc, nullptr, nullptr, h->errflag.as<int>(),
           h->pairc.as<unsigned long long>(), lists);
       CKL();
       // pass 2: evaluation of the lists
@@ -1470,7 +1472,7 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
                       : (rp.half ? k6b_eval<false, true> : k6b_eval<false, false>);
       ev<<<nb, K6_WARPS * 32, 0, h->stream>>>(h->sorted.as<double4>(), h->start.as<int>(),
                                               h->row_ustart.as<int>(), rp, lists,
-                                              h->fsorted.as<double>(), eb, eb_lj,
+                                              facc, eb, eb_lj,
                                               h->errflag.as<int>());
       CKL();
       // overflowed units (list longer than its capacity): fused kernel,
@@ -1482,14 +1484,16 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
       ovf<<<nb, K6_WARPS * 32, 0, h->stream>>>(
           h->sorted.as<double4>(), h->sorted_f.as<float4>(), h->sorted_cell.as<int>(),
           h->order.as<int>(), h->start.as<int>(), h->row_ustart.as<int>(), rp,
-          h->fsorted.as<double>(), eb + n_eslots, eb_lj ? eb_lj + n_eslots : nullptr,
+          facc, eb + n_eslots, eb_lj ? eb_lj + n_eslots : nullptr,
           h->errflag.as<int>(), nullptr, lists);
       CKL();
     }
   }
-  k_unpermute_add<<<blocks_for(n, 256), 256, 0, h->stream>>>(h->order.as<int>(),
-                                                             h->fsorted.as<double>(), n, d_force);
-  CKL();
+  if (!fold) {
+    k_unpermute_add<<<blocks_for(n, 256), 256, 0, h->stream>>>(h->order.as<int>(),
+                                                               h->fsorted.as<double>(), n, d_force);
+    CKL();
+  }
   if (pair_coul) {
     k_sum<<<1, 1024, 0, h->stream>>>(h->eblk.as<double>(), n_eslot_all, 1.0, d_u_out);
     CKL();

@@ -426,7 +426,8 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
         if (!(dbg & 2) && elect_one()) {
           const uint64_t gd = tc_desc(smem_u32(gbuf + gs * TC_S * TC_GSL));
           const uint64_t xd = tc_desc(smem_u32(xbuf + xs * xblk));
-          const uint32_t acc0 = it > 0 ? 1u : 0u;
+          const uint32_t acc0 = it > 0 ? 1u : 0u;  // unmerged forms only
+          (void)acc0;
           constexpr int XSL = tc_xsl_bytes(0);
 #if K1_ACP
           // G slices staged in TMEM (four 8-column slots after the levels),

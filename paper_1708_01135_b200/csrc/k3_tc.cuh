@@ -308,7 +308,9 @@ __global__ void __launch_bounds__(T3_THREADS, 1)
         if (!(dbg & 2) && elect_one()) {
           const uint64_t ad = tc_desc(smem_u32(abuf + as * ABLK));
           const uint64_t bd = tc_desc(smem_u32(bbuf + bs * T3_S * T3_BSL));
-          const uint32_t acc0 = it > 0 ? 1u : 0u;
+          const uint32_t acc0 = it > 0 ? 1u : 0u;  // unmerged forms only
+          (void)acc0;
+          (void)idesc;
 #if T3_ACP
           const uint32_t aslot = tmem + (uint32_t)(T3_NL * T3_NP);
 #pragma unroll

@@ -116,11 +116,6 @@ __global__ void __launch_bounds__(256) k5_cell_sort(const int *__restrict__ star
   }
 }
 
-__global__ void k_iota(int *__restrict__ v, int64_t n) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) v[i] = (int)i;
-}
-
 // real-space forces, accumulated in cell-sorted order by k6 (partner atomics
 // on neighbouring addresses, no order[] load per pair), added into the
 // caller's order: force[order[p]] += fs[p]
@@ -132,6 +127,27 @@ __global__ void k_unpermute_add(const int *__restrict__ order, const double *__r
   force[3 * o] += fs[3 * p];
   force[3 * o + 1] += fs[3 * p + 1];
   force[3 * o + 2] += fs[3 * p + 2];
+}
+
+// Scan-all (FOLD) binning in one pass: identity order, one cell, one row --
+// replaces count / scans / iota / gather / row scan for small boxes.
+__global__ void k_fold_prep(const double4 *__restrict__ xyzq, int64_t n, int units,
+                            double4 *__restrict__ sorted, float4 *__restrict__ sorted_f,
+                            int *__restrict__ sorted_cell, int *__restrict__ order,
+                            int *__restrict__ start, int *__restrict__ row_ustart) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p == 0) {
+    start[0] = 0;
+    start[1] = (int)n;
+    row_ustart[0] = 0;
+    row_ustart[1] = units;
+  }
+  if (p >= n) return;
+  const double4 v = xyzq[p];
+  sorted[p] = v;
+  sorted_f[p] = make_float4((float)v.x, (float)v.y, (float)v.z, 0.0f);
+  sorted_cell[p] = 0;
+  order[p] = (int)p;
 }
 
 __global__ void k5_gather(const int *__restrict__ order, const double4 *__restrict__ xyzq,

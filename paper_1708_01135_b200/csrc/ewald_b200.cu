@@ -1393,7 +1393,16 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
   // scan-all mode with few units: split every unit's candidates over
   // several warps (partial sums meet in the atomics of the half shell)
   rp.jsplit = 1;
-  if (!fold && rp.half) rp.jsplit = K6_RSPLIT;
+  // units this slab actually owns (estimate: rows are about equally filled)
+  const int64_t active = std::max<int64_t>(
+      1, (n / K6_G + rows_slab) * rows_slab / std::max<int64_t>(1, (int64_t)cpd_eff * cpd_eff));
+  if (!fold && rp.half) {
+    // few units (a z-slab of a multi-GPU step, small boxes): split each
+    // unit's stencil rows over up to 4 warps so that >= 2 blocks per SM are
+    // active (at full occupancy splitting costs: c2 +9% for 2 warps)
+    const int64_t want = 2 * (int64_t)h->n_sm * K6_WARPS;
+    rp.jsplit = (int)std::min<int64_t>(4, std::max<int64_t>(K6_RSPLIT, (want + active - 1) / active));
+  }
   if (fold && rp.half) {
     const int64_t want = 4 * (int64_t)h->n_sm * K6_WARPS;
     rp.jsplit = (int)std::max<int64_t>(1, std::min<int64_t>(64, want / std::max<int64_t>(1, units_max)));
@@ -1441,7 +1450,7 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
     double *eb_lj = lj_on ? h->eblk_lj.as<double>() : nullptr;
     if (!split) {
       // more resident warps pay off only when the grid spans several waves
-      const bool hi = (int64_t)nb >= (int64_t)K6_HI_WAVES * h->n_sm * K6_MINB_HI;
+      const bool hi = active * rp.jsplit >= (int64_t)K6_HI_WAVES * h->n_sm * K6_MINB_HI * K6_WARPS;
       auto kern = hi ? (lj_on ? (rp.half ? k6_real_space<true, true, K6_MODE_FUSED_HI>
                                          : k6_real_space<true, false, K6_MODE_FUSED_HI>)
                               : (rp.half ? k6_real_space<false, true, K6_MODE_FUSED_HI>

@@ -312,6 +312,35 @@ def test_device_stages_sharded_match_full(ew):
     assert np.abs(f.cpu().numpy() - ff).max() <= 1e-12 * f_rms(ff)
 
 
+@pytest.mark.parametrize("name,nparts", [("c2", 3), ("c2", 8), ("c4", 8)])
+def test_real_space_parts_sum_to_whole(ew, name, nparts):
+    """Real space split into row ranges (the multi-GPU partition; few units
+    per part switch on the stencil-row split over several warps): the parts
+    add up to the single-part result."""
+    torch = pytest.importorskip("torch")
+    from paper_1708_01135_b200 import _lib
+    from paper_1708_01135_b200 import workloads as wl
+    cfg = wl.make_config(name, seed=0)
+    dev = torch.device("cuda", 0)
+    pos = torch.from_numpy(cfg["pos"]).to(dev)
+    q = torch.from_numpy(cfg["q"]).to(dev)
+    n = q.shape[0]
+    st = torch.cuda.Stream()
+    h = _lib.Handle(0)
+    h.set_stream(st.cuda_stream)
+    h.set_system(cfg["L"], cfg["alpha_ref"], cfg["r_cutoff"])
+    with torch.cuda.stream(st):
+        f1 = torch.zeros((n, 3), dtype=torch.float64, device=dev)
+        fp = torch.zeros((n, 3), dtype=torch.float64, device=dev)
+        h.dev_load(pos.data_ptr(), q.data_ptr(), n)
+        u1 = h.dev_real_space(0, 1, f1.data_ptr())
+        up = sum(h.dev_real_space(p, nparts, fp.data_ptr()) for p in range(nparts))
+        st.synchronize()
+    assert rel(up, u1) <= 1e-13
+    a, b = fp.cpu().numpy(), f1.cpu().numpy()
+    assert np.abs(a - b).max() <= 1e-13 * f_rms(b)
+
+
 def test_sharded_ewald_device_stages_one_rank(ew):
     """distributed.ShardedEwald on the product DeviceStages (asynchronous
     stages, device energy slots, one synchronisation) against the

@@ -81,6 +81,12 @@ constexpr int K3_CH = 32;         // k-items per shared-memory chunk
 #ifndef K6_RAD_MAX
 #define K6_RAD_MAX 3              // largest stencil radius in cells (3: r_c/3 cells)
 #endif
+#ifndef K6_RAD3_F
+#define K6_RAD3_F 3.0             // radius-3 cells: edge L / floor(F L / r_c) >= r_c / 3
+#endif
+#ifndef K6_RAD3_MINOCC
+#define K6_RAD3_MINOCC 16.0       // ... used when cells hold at least this many particles
+#endif
 #ifndef K6_HI_WAVES
 #define K6_HI_WAVES 3             // fused pair kernel at 5 blocks/SM from this many waves up
 #endif
@@ -1306,9 +1312,9 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
     // while a cell still holds >= 16 particles on average (c4, r_c = 8:
     // 19 per cell, real space -3.4%; r_c = 6 at unit density: 8 per cell,
     // +2..8%)
-    const int cpd3 = (int)std::floor(3.0 * h->L / rc_t);
+    const int cpd3 = (int)std::floor(K6_RAD3_F * h->L / rc_t);
     if (K6_RAD_MAX >= 3 && h->stencil_rad == 0 && cpd3 >= 7 && cpd3 <= 64 &&
-        (double)n >= 16.0 * (double)cpd3 * cpd3 * cpd3) {
+        (double)n >= K6_RAD3_MINOCC * (double)cpd3 * cpd3 * cpd3) {
       rad = 3;
       cpd = cpd3;
     }

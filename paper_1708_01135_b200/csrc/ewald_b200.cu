@@ -976,8 +976,13 @@ int stage_rho_tc(ewb_handle *h, int64_t i0, int64_t i1, int *n_part_out) {
       h->tc_ytab.as<double2>(), h->tc_ztab.as<double2>(), h->tc_xsl.as<uint8_t>());
   CKL();
   const size_t smem = (size_t)tc_smem_bytes(P.tc_npad_max);
-  CK(cudaFuncSetAttribute(k1t_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k1t_gemm<<<dim3(P.tc_mtiles, P.tc_nchunks, (unsigned)ns), TC_NTHREADS, smem, h->stream>>>(
+  // X slice stride = the widest padded a-chunk (multiple of 16, <= 64)
+  auto kern = P.tc_npad_max <= 16   ? k1t_gemm<16>
+              : P.tc_npad_max <= 32 ? k1t_gemm<32>
+              : P.tc_npad_max <= 48 ? k1t_gemm<48>
+                                    : k1t_gemm<64>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<dim3(P.tc_mtiles, P.tc_nchunks, (unsigned)ns), TC_NTHREADS, smem, h->stream>>>(
       h->frac.as<double4>(), h->tc_ytab.as<double2>(), h->tc_ztab.as<double2>(),
       h->base.as<double2>(), h->tc_xsl.as<uint8_t>(), P.tc_chunks.as<TCChunk>(),
       P.tc_runs.as<int4>(),

@@ -56,7 +56,7 @@ constexpr double TC_SC = 140185576636287.0;              // 0x7F7F7F7F7F7F
 constexpr double TC_MAGIC = 6755399441055744.0 + 141289400074368.0;  // 1.5*2^52 + 0x8080..80
 
 // one X slice (fixed stride for every chunk: compile-time MMA descriptors)
-__host__ __device__ constexpr int tc_xsl_bytes(int) { return (TC_NMAX / 8) * TC_SBO; }
+__host__ __device__ constexpr int tc_xsl_bytes(int xnp) { return (xnp / 8) * TC_SBO; }
 __host__ __device__ constexpr int tc_stage_bytes(int npad) {
   return TC_S * TC_GSL + TC_S * tc_xsl_bytes(npad);
 }
@@ -339,6 +339,10 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
       : "memory");
 }
 
+// XNP: rows between consecutive X slices in shared memory and columns
+// between TMEM levels = the largest padded a-chunk width of the k-table
+// (16..64), so merged MMAs carry no padding columns beyond the last chunk's
+template <int XNP>
 __global__ void __launch_bounds__(TC_NTHREADS, 1)
     k1t_gemm(const double4 *__restrict__ frac, const double2 *__restrict__ ytab,
              const double2 *__restrict__ ztab,
@@ -355,7 +359,7 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const TCChunk C = chunks[ch];
   const int npad = C.npad;
-  const int xsl_b = tc_xsl_bytes(npad_max);
+  const int xsl_b = tc_xsl_bytes(XNP);  // X slice stride (XNP rows)
   const int xblk = TC_S * xsl_b;  // bytes of one K-block's X slices
   uint8_t *gbuf = smem;
   uint8_t *xbuf = smem + TC_GS * TC_S * TC_GSL;
@@ -387,11 +391,11 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base_s;
-  const int lstride = K1_MERGE > 1 ? TC_NMAX : npad;  // TMEM columns between levels
+  const int lstride = K1_MERGE > 1 ? XNP : npad;  // TMEM columns between levels
   if (K1_MERGE > 1) {  // zero the level accumulators (every merged MMA accumulates)
     if (warp < 4) {
       const uint32_t z[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-      for (int c = 0; c < TC_NL * TC_NMAX; c += 8)
+      for (int c = 0; c < TC_NL * XNP; c += 8)
         tc_st8(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)c, z);
       tc_wait_st();
     }
@@ -428,11 +432,11 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
           const uint64_t xd = tc_desc(smem_u32(xbuf + xs * xblk));
           const uint32_t acc0 = it > 0 ? 1u : 0u;  // unmerged forms only
           (void)acc0;
-          constexpr int XSL = tc_xsl_bytes(0);
+          constexpr int XSL = tc_xsl_bytes(XNP);
 #if K1_ACP
           // G slices staged in TMEM (four 8-column slots after the levels),
           // TS-form MMAs slice-major: each G slice leaves shared memory once
-          const uint32_t aslot = tmem + (uint32_t)(TC_NL * TC_NMAX);
+          const uint32_t aslot = tmem + (uint32_t)(TC_NL * XNP);
 #pragma unroll
           for (int ks = 0; ks < TC_KB / 32; ++ks) {
 #pragma unroll
@@ -444,9 +448,9 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
 #pragma unroll
               for (int t = (TC_W0 - s > 0 ? TC_W0 - s : 0); t < TC_S; t += K1_MERGE) {
                 const int m = TC_S - t < K1_MERGE ? TC_S - t : K1_MERGE;
-                tc_mma_ts(tmem + (uint32_t)((s + t - TC_W0) * TC_NMAX), ta,
+                tc_mma_ts(tmem + (uint32_t)((s + t - TC_W0) * XNP), ta,
                           xd + (uint64_t)((t * XSL + ks * 256) >> 4),
-                          idesc0 | ((uint32_t)(((m - 1) * TC_NMAX + npad) >> 3) << 17), 1u);
+                          idesc0 | ((uint32_t)(((m - 1) * XNP + npad) >> 3) << 17), 1u);
               }
 #else
 #pragma unroll
@@ -472,10 +476,10 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
 #pragma unroll
               for (int t = (TC_W0 - s > 0 ? TC_W0 - s : 0); t < TC_S; t += K1_MERGE) {
                 const int m = TC_S - t < K1_MERGE ? TC_S - t : K1_MERGE;
-                tc_mma(tmem + (uint32_t)((s + t - TC_W0) * TC_NMAX),
+                tc_mma(tmem + (uint32_t)((s + t - TC_W0) * XNP),
                        gd + (uint64_t)((s * TC_GSL + ks * 256) >> 4),
                        xd + (uint64_t)((t * XSL + ks * 256) >> 4),
-                       idesc0 | ((uint32_t)(((m - 1) * TC_NMAX + npad) >> 3) << 17), 1u);
+                       idesc0 | ((uint32_t)(((m - 1) * XNP + npad) >> 3) << 17), 1u);
               }
             }
           }

@@ -705,18 +705,41 @@ int build_plan(ewb_handle *h, const int64_t *m, int64_t K, const double *coeff) 
         const int slot = mm * n_pitems + i;
         if (e.x < 0) e.x = slot; else e.y = slot;
       }
-    // a-chunks: Xr columns then Xs columns, <= TC_NMAX in total
-    int a0 = 0;
-    while (a0 <= tc_A) {
+    // a-chunks: Xr columns then Xs columns, <= TC_NMAX in total.  Two
+    // candidate splits -- greedy (full chunks, a narrow last one) and the
+    // same number of chunks with the a-range split evenly -- priced by the
+    // merged-MMA columns they execute (every chunk runs at the widest
+    // chunk's slice stride XNP: a merge of m slices costs (m-1) XNP + npad;
+    // per K-step 7 merges of 3, 2 of 2, 1 single): c3's 64 + 16 columns
+    // become 48 + 48 (-12% MMA columns), c5 keeps 64 + 48.
+    auto ncols = [&](int lo, int hi) { return (hi - lo + 1) + std::max(0, hi - std::max(lo, 1) + 1); };
+    auto pad16 = [](int nc) { return ((nc + 15) / 16) * 16; };
+    std::vector<TCChunk> greedy, even;
+    for (int a0 = 0; a0 <= tc_A;) {
       int a1 = a0;
-      auto ncols = [&](int lo, int hi) { return (hi - lo + 1) + std::max(0, hi - std::max(lo, 1) + 1); };
       while (a1 + 1 <= tc_A && ncols(a0, a1 + 1) <= TC_NMAX) ++a1;
-      const int nc = ncols(a0, a1);
-      const int npad = ((nc + 15) / 16) * 16;
-      tc_chunks.push_back(TCChunk{a0, a1, a1 - a0 + 1, npad});
-      tc_npad_max = std::max(tc_npad_max, npad);
+      greedy.push_back(TCChunk{a0, a1, a1 - a0 + 1, pad16(ncols(a0, a1))});
       a0 = a1 + 1;
     }
+    {
+      const int nch = (int)greedy.size();
+      bool ok = true;
+      for (int c = 0; c < nch && ok; ++c) {
+        const int a0 = (int)((int64_t)(tc_A + 1) * c / nch), a1 = (int)((int64_t)(tc_A + 1) * (c + 1) / nch) - 1;
+        ok = a1 >= a0 && ncols(a0, a1) <= TC_NMAX;
+        if (ok) even.push_back(TCChunk{a0, a1, a1 - a0 + 1, pad16(ncols(a0, a1))});
+      }
+      if (!ok) even.clear();
+    }
+    auto cost = [&](const std::vector<TCChunk> &v) {
+      int xnp = 16;
+      for (const auto &c : v) xnp = std::max(xnp, c.npad);
+      int64_t t = 0;
+      for (const auto &c : v) t += 7 * (2 * xnp + c.npad) + 2 * (xnp + c.npad) + c.npad;
+      return t;
+    };
+    tc_chunks = (!even.empty() && cost(even) < cost(greedy)) ? even : greedy;
+    for (const auto &c : tc_chunks) tc_npad_max = std::max(tc_npad_max, c.npad);
   }
 
   // ---- tensor-core force-gather plan ----

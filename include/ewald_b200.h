@@ -60,8 +60,11 @@ int ewb_version(void);
 int ewb_create(int device, ewb_handle **out);
 void ewb_destroy(ewb_handle *h);
 const char *ewb_last_error(const ewb_handle *h);
-/* stream used by every later call (0 = the handle's own stream) */
+/* stream used by every later call (a cudaStream_t; 0 = the legacy default
+ * stream).  A new handle runs on its own non-blocking stream;
+ * ewb_use_own_stream returns to it. */
 int ewb_set_stream(ewb_handle *h, uintptr_t stream);
+int ewb_use_own_stream(ewb_handle *h);
 /* tuning knobs (take effect at the next ewb_set_kspace): maximum k-column
  * segment length of the force gather (1..32; default 28) and of the
  * structure factor's +-m_x pair items (1..20; default 20) */
@@ -170,6 +173,27 @@ int ewb_dev_real_space(ewb_handle *h, int part, int nparts, double *d_force,
 /* Self energy -sqrt(alpha/pi) * sum q^2 over all loaded particles
  * (u_self == NULL: asynchronous, device slot only). */
 int ewb_dev_self_energy(ewb_handle *h, double *u_self);
+/* Self energy of the loaded particles [i0, i1) only (the owned particles of
+ * a domain-decomposed rank; self_energy, ewald.py:482-484). */
+int ewb_dev_self_energy_range(ewb_handle *h, int64_t i0, int64_t i1, double *u_self);
+
+/* Domain decomposition of the real space (distributed.SlabEwald): every rank
+ * bins on the grid of the GLOBAL particle count n_global (the r_c/3 grid is
+ * chosen by occupancy), so all ranks agree on cells and rows. */
+int ewb_set_geometry_n(ewb_handle *h, int64_t n_global);
+/* Real-space cell grid of the current system: info4 = (cells per edge,
+ * stencil radius in cells, rows of cells = cpd^2, scan-all flag).  A row is
+ * the line of cells (cy, cz) along x, numbered cy + cpd cz. */
+int ewb_rs_geometry(ewb_handle *h, int64_t *info4);
+/* Row of cells of each of n particles (device pointers), binned exactly as
+ * the pair kernel's cell list (celllist.py:75-108 binning). */
+int ewb_dev_rows(ewb_handle *h, const double *d_pos, int64_t n, int *d_rows);
+/* Real space of the loaded particles with centres restricted to the rows
+ * [row_lo, row_hi): the rank's own rows, partners from its own rows and the
+ * halo rows it received.  Half shell: forces also land on halo partners
+ * (returned to their owners by the caller).  u_sr as ewb_dev_real_space. */
+int ewb_dev_real_space_rows(ewb_handle *h, int row_lo, int row_hi, double *d_force,
+                            double *u_sr);
 /* Device energy slots (u_sr, u_lr, u_self of the last stages) copied into
  * d_out3 (device, 3 doubles) on the handle's stream.  Replaces the three
  * scalar returns of the engine's kernels (ewald.py:609-655) for a
@@ -177,6 +201,10 @@ int ewb_dev_self_energy(ewb_handle *h, double *u_self);
 int ewb_dev_energies(ewb_handle *h, double *d_out3);
 /* Synchronise and raise the deferred device-side errors: unwrapped
  * positions (celllist.py:90-91) and coincident particles (ewald.py:212-213). */
+/* The masked device error flag (1: unwrapped positions, 2: coincident
+ * particles) written as a double into d_out on the handle's stream, without
+ * a host synchronisation (multi-rank drivers reduce it with the energies). */
+int ewb_dev_status(ewb_handle *h, double *d_out);
 int ewb_dev_check(ewb_handle *h);
 /* Whole evaluation on device-resident data (single GPU); force +=. */
 int ewb_dev_evaluate(ewb_handle *h, const double *d_pos, const double *d_q,

@@ -34,6 +34,10 @@ EWB_EKSPACE = 7
 EWB_ESTATE = 8
 EWB_ESIZE = 9
 
+#: device error bits (ewb_dev_status)
+ERR_UNWRAPPED = 1
+ERR_COINCIDENT = 2
+
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
 _D = ctypes.c_double
@@ -46,6 +50,7 @@ SIGNATURES = {
     "ewb_destroy": (None, [_P]),
     "ewb_last_error": (ctypes.c_char_p, [_P]),
     "ewb_set_stream": (_INT, [_P, ctypes.c_size_t]),
+    "ewb_use_own_stream": (_INT, [_P]),
     "ewb_set_max_segment": (_INT, [_P, _INT]),
     "ewb_set_max_pair_segment": (_INT, [_P, _INT]),
     "ewb_set_stencil": (_INT, [_P, _INT]),
@@ -70,8 +75,14 @@ SIGNATURES = {
     "ewb_dev_recip_forces": (_INT, [_P, _I64, _I64, _P]),
     "ewb_dev_real_space": (_INT, [_P, _INT, _INT, _P, _P]),
     "ewb_dev_self_energy": (_INT, [_P, _P]),
+    "ewb_dev_self_energy_range": (_INT, [_P, _I64, _I64, _P]),
+    "ewb_set_geometry_n": (_INT, [_P, _I64]),
+    "ewb_rs_geometry": (_INT, [_P, _P]),
+    "ewb_dev_rows": (_INT, [_P, _P, _I64, _P]),
+    "ewb_dev_real_space_rows": (_INT, [_P, _INT, _INT, _P, _P]),
     "ewb_dev_energies": (_INT, [_P, _P]),
     "ewb_dev_check": (_INT, [_P]),
+    "ewb_dev_status": (_INT, [_P, _P]),
     "ewb_dev_evaluate": (_INT, [_P, _P, _P, _I64, _P, _P, _P, _P]),
     "ewb_set_coulomb": (_INT, [_P, _INT]),
     "ewb_set_lj": (_INT, [_P, _INT, _D, _D, _D, _D, _D, _D]),
@@ -178,6 +189,7 @@ class Handle:
         self.h = h
         self.system = None
         self.kspace_key = None
+        self.deterministic = False
 
     def __del__(self):
         h = getattr(self, "h", None)
@@ -237,6 +249,7 @@ class Handle:
 
     def set_deterministic(self, on):
         self._check(self.lib.ewb_set_deterministic(self.h, 1 if on else 0))
+        self.deterministic = bool(on)
 
     def set_real_space_split(self, mode):
         """1/True: two-pass real space (default), 0/False: fused kernel,
@@ -253,7 +266,13 @@ class Handle:
                          "max_table", "n_pair_items", "M1"), info.tolist()))
 
     def set_stream(self, stream_ptr):
+        """Bind every later call to a CUDA stream (0: the legacy default
+        stream, i.e. torch's default stream)."""
         self._check(self.lib.ewb_set_stream(self.h, int(stream_ptr)))
+
+    def use_own_stream(self):
+        """Back to the handle's own non-blocking stream."""
+        self._check(self.lib.ewb_use_own_stream(self.h))
 
     def set_coulomb(self, on):
         self._check(self.lib.ewb_set_coulomb(self.h, 1 if on else 0))
@@ -382,6 +401,25 @@ class Handle:
         self._check(self.lib.ewb_dev_self_energy(self.h, ctypes.byref(u)))
         return u.value
 
+    # domain decomposition (distributed.SlabEwald)
+    def set_geometry_n(self, n_global):
+        self._check(self.lib.ewb_set_geometry_n(self.h, int(n_global)))
+
+    def rs_geometry(self):
+        info = np.zeros(4, dtype=np.int64)
+        self._check(self.lib.ewb_rs_geometry(self.h, _ptr(info)))
+        return dict(zip(("cpd", "rad", "n_rows", "fold"), info.tolist()))
+
+    def dev_rows(self, d_pos, n, d_rows):
+        self._check(self.lib.ewb_dev_rows(self.h, d_pos, int(n), d_rows))
+
+    def dev_real_space_rows_async(self, row_lo, row_hi, d_force):
+        self._check(self.lib.ewb_dev_real_space_rows(self.h, int(row_lo), int(row_hi),
+                                                     d_force, None))
+
+    def dev_self_energy_range_async(self, i0, i1):
+        self._check(self.lib.ewb_dev_self_energy_range(self.h, int(i0), int(i1), None))
+
     # asynchronous variants: energies stay in the device slots
     def dev_real_space_async(self, part, nparts, d_force):
         self._check(self.lib.ewb_dev_real_space(self.h, int(part), int(nparts),
@@ -396,6 +434,9 @@ class Handle:
 
     def dev_energies(self, d_out3):
         self._check(self.lib.ewb_dev_energies(self.h, d_out3))
+
+    def dev_status(self, d_out):
+        self._check(self.lib.ewb_dev_status(self.h, d_out))
 
     def dev_check(self):
         self._check(self.lib.ewb_dev_check(self.h))

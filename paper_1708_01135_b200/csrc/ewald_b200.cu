@@ -404,10 +404,12 @@ struct ewb_handle {
   int deterministic = 0;  // 1: full-shell real space, no atomics (bitwise reproducible)
   int k3_const = 1;       // constant-bank force gather for large systems
   int use_tc = 2;         // int8 tensor-core reciprocal space: 0 off, 1 forced, 2 auto (N*K)
-  int tc_dbg = 0;         // tools only (EWB_TC_DBG): 1 skip G production, 2 skip MMAs
+  int tc_dbg = 0;  // compile-time -DEWB_TC_DBG=1|2 only: skip G production | the MMAs
   DBuf tc_qmax, tc_ytab, tc_ztab, tc_xsl;
   DBuf t3_wsl, t3_rscale;
   DBuf pairc;  // in-cutoff pairs visited by the last real-space pass
+  int64_t geom_n = 0;           // particle count deciding the cell grid (0: the loaded one)
+  int row_lo = -1, row_hi = -1;  // explicit centre rows of the next real-space pass
   int rs_split = K6_SPLIT;        // two-pass real space (pair lists in HBM), off by default
   DBuf rs_list, rs_count;         // per-unit pair lists and their lengths
   DBuf eblk_r;  // energy scratch of the reciprocal stages (own stream)
@@ -1281,6 +1283,57 @@ int stage_recip_forces(ewb_handle *h, int64_t i0, int64_t i1, double *d_force, b
   return EWB_OK;
 }
 
+// Cell geometry of the real-space pass at traversal cutoff rc_t.  Reference
+// binning: cpd = floor(L / r_c), edge = L / cpd (celllist.py:96-98); with
+// cpd < 3 the 27-stencil folds onto every cell and the reference scans all
+// particles with a per-pair fold (engine.py:111-134) -- FOLD mode here.
+// Cells of edge >= r_c/2 with a 5^3 stencil when the box holds >= 5 of them
+// (42% fewer candidate pairs than r_c cells with 3^3), r_c/3 cells with 7^3
+// while they hold >= 16 particles on average, else r_c cells with 3^3, else
+// (fewer than 3 cells) the reference's scan-all branch.  Any cell size whose
+// stencil covers the cutoff sphere visits the same pair set: the predicate,
+// not the binning, decides membership.  The particle count deciding the
+// r_c/3 grid is the global one of a sharded evaluation (ewb_set_geometry_n),
+// so every rank bins on the same grid.
+struct RSGeom {
+  int rad, cpd, cpd_eff;
+  bool fold;
+  double edge;
+};
+RSGeom rs_geometry(const ewb_handle *h, double rc_t, int64_t n_local) {
+  const int64_t n = h->geom_n > 0 ? h->geom_n : n_local;
+  int rad = 2;
+  int cpd = (int)std::floor(2.0 * h->L / rc_t);
+  {
+    // r_c/3 cells with a 7^3 stencil: tighter candidate pieces, but only
+    // while a cell still holds >= 16 particles on average (c4, r_c = 8:
+    // 19 per cell, real space -3.4%; r_c = 6 at unit density: 8 per cell,
+    // +2..8%)
+    const int cpd3 = (int)std::floor(K6_RAD3_F * h->L / rc_t);
+    if (K6_RAD_MAX >= 3 && h->stencil_rad == 0 && cpd3 >= 7 && cpd3 <= 64 &&
+        (double)n >= K6_RAD3_MINOCC * (double)cpd3 * cpd3 * cpd3) {
+      rad = 3;
+      cpd = cpd3;
+    }
+  }
+  if (cpd < 5 || h->stencil_rad == 1) {
+    rad = 1;
+    cpd = (int)std::floor(h->L / rc_t);
+  }
+  if (cpd < 1) cpd = 1;
+  if (cpd > 64) cpd = 64;  // edge stays >= r_c/rad; bounds the cell arrays
+  const bool fold = cpd < 2 * rad + 1;
+  return RSGeom{rad, cpd, fold ? 1 : cpd, fold, h->L / cpd};
+}
+
+// traversal cutoff (and its square) of the real-space pass: the larger of
+// the Coulomb and LJ cutoffs of the terms the pair kernel evaluates
+void rs_cutoff(const ewb_handle *h, double &rc_t, double &rc2_t) {
+  const bool pair_coul = h->coul_on && !(h->rc > 0.5 * h->L);
+  rc_t = std::max(pair_coul ? h->rc : 0.0, h->lj_on ? h->rc_lj : 0.0);
+  rc2_t = std::max(pair_coul ? h->rc2 : 0.0, h->lj_on ? h->rc2_lj : 0.0);
+}
+
 // Cell list + real space for z-slab part/nparts; u_sr into d_u_out.
 constexpr int RS_CELLS = 1, RS_PAIRS = 2;
 int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, double *d_u_out,
@@ -1298,7 +1351,7 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
     if (n > WIDE_MAX_N)
       return h->fail(EWB_ESIZE, "wide-cutoff real-space path is O(N^2); N exceeds the 4096 guard");
     if (which & RS_PAIRS) {
-      if (part != 0) {  // not sharded: the first part owns every centre
+      if (h->row_hi >= 0 ? h->row_lo > 0 : part != 0) {  // not sharded: part 0 owns every centre
         CK(cudaMemsetAsync(d_u_out, 0, sizeof(double), h->stream));
       } else {
         CK(h->eblk.ensure(n * sizeof(double)));
@@ -1325,38 +1378,11 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
   const bool pair_coul = coul_on && !wide;
   const double rc_t = std::max(pair_coul ? h->rc : 0.0, lj_on ? h->rc_lj : 0.0);
   const double rc2_t = std::max(pair_coul ? h->rc2 : 0.0, lj_on ? h->rc2_lj : 0.0);
-  // reference binning: cpd = floor(L / r_c), edge = L / cpd (celllist.py:96-98);
-  // with cpd < 3 the 27-stencil folds onto every cell and the reference scans
-  // all particles with a per-pair fold (engine.py:111-134) -- FOLD mode here.
-  // Cells of edge >= r_c/2 with a 5^3 stencil when the box holds >= 5 of
-  // them (42% fewer candidate pairs than r_c cells with 3^3), else r_c cells
-  // with 3^3, else (fewer than 3 cells) the reference's scan-all branch.
-  // Any cell size whose stencil covers the cutoff sphere visits the same
-  // pair set: the predicate, not the binning, decides membership.
-  int rad = 2;
-  int cpd = (int)std::floor(2.0 * h->L / rc_t);
-  {
-    // r_c/3 cells with a 7^3 stencil: tighter candidate pieces, but only
-    // while a cell still holds >= 16 particles on average (c4, r_c = 8:
-    // 19 per cell, real space -3.4%; r_c = 6 at unit density: 8 per cell,
-    // +2..8%)
-    const int cpd3 = (int)std::floor(K6_RAD3_F * h->L / rc_t);
-    if (K6_RAD_MAX >= 3 && h->stencil_rad == 0 && cpd3 >= 7 && cpd3 <= 64 &&
-        (double)n >= K6_RAD3_MINOCC * (double)cpd3 * cpd3 * cpd3) {
-      rad = 3;
-      cpd = cpd3;
-    }
-  }
-  if (cpd < 5 || h->stencil_rad == 1) {
-    rad = 1;
-    cpd = (int)std::floor(h->L / rc_t);
-  }
-  if (cpd < 1) cpd = 1;
-  if (cpd > 64) cpd = 64;  // edge stays >= r_c/rad; bounds the cell arrays
-  const bool fold = cpd < 2 * rad + 1;
-  const int cpd_eff = fold ? 1 : cpd;
+  const RSGeom g = rs_geometry(h, rc_t, n);
+  const int rad = g.rad, cpd_eff = g.cpd_eff;
+  const bool fold = g.fold;
   const int n_cells = cpd_eff * cpd_eff * cpd_eff;
-  const double edge = h->L / cpd;
+  const double edge = g.edge;
   if (which & RS_CELLS) {
   CK(h->cell_of.ensure(n * sizeof(int)));
   CK(h->slot.ensure(n * sizeof(int)));
@@ -1443,6 +1469,10 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
   const int64_t rows_all = (int64_t)cpd_eff * cpd_eff;
   rp.c_lo = fold ? (part == 0 ? 0 : 1) : (int)(rows_all * part / nparts);
   rp.c_hi = fold ? 1 : (int)(rows_all * (part + 1) / nparts);
+  if (h->row_hi >= 0) {  // explicit row range (domain-decomposed evaluation)
+    rp.c_lo = (int)std::min<int64_t>(rows_all, h->row_lo);
+    rp.c_hi = (int)std::min<int64_t>(rows_all, std::max(h->row_lo, h->row_hi));
+  }
   const int64_t rows_slab = rp.c_hi - rp.c_lo;
   const int64_t units_max = n / K6_G + rows_slab + 1;
   // scan-all mode with few units: split every unit's candidates over
@@ -1569,14 +1599,23 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
   return EWB_OK;
 }
 
-int stage_self(ewb_handle *h, double *d_u_out) {
-  const unsigned nb = (unsigned)std::min<int64_t>(1024, blocks_for(h->n, RED_THREADS));
+int stage_self(ewb_handle *h, double *d_u_out, int64_t i0 = 0, int64_t i1 = -1) {
+  if (i1 < 0) i1 = h->n;
+  const int64_t cnt = i1 - i0;
+  const unsigned nb = (unsigned)std::max<int64_t>(1, std::min<int64_t>(1024, blocks_for(cnt, RED_THREADS)));
   CK(h->eblk2.ensure(std::max<size_t>(nb, 1) * sizeof(double)));
-  k7_sum_q2<<<nb, RED_THREADS, 0, h->stream>>>(h->frac.as<double4>(), h->n, h->eblk2.as<double>());
+  k7_sum_q2<<<nb, RED_THREADS, 0, h->stream>>>(h->frac.as<double4>() + i0, cnt, h->eblk2.as<double>());
   CKL();
   k_sum<<<1, 1024, 0, h->stream>>>(h->eblk2.as<double>(), nb, -std::sqrt(h->alpha / M_PI), d_u_out);
   CKL();
   return EWB_OK;
+}
+
+// device error bits a completed evaluation reports: the wide-cutoff (image
+// shell) real space accepts unwrapped positions, as the reference's
+// short_range_wide_cutoff does (ewald.py:553-576)
+int err_mask(const ewb_handle *h) {
+  return ((h->coul_on && h->rc > 0.5 * h->L && !h->lj_on) ? 0 : ERR_UNWRAPPED) | ERR_COINCIDENT;
 }
 
 int check_errflag(ewb_handle *h, int mask) {
@@ -1839,7 +1878,9 @@ int ewb_create(int device, ewb_handle **out) {
     return EWB_ECUDA;
   }
   h->stream = h->own_stream;
-  if (const char *d = getenv("EWB_TC_DBG")) h->tc_dbg = atoi(d);
+#ifdef EWB_TC_DBG
+  h->tc_dbg = EWB_TC_DBG;  // component-timing builds only (tools/tc_dbg.sh)
+#endif
   if (cudaStreamCreateWithFlags(&h->aux_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&h->rstream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking) != cudaSuccess ||
@@ -1900,7 +1941,16 @@ const char *ewb_last_error(const ewb_handle *h) { return h ? h->err.c_str() : "n
 int ewb_set_stream(ewb_handle *h, uintptr_t stream) {
   if (!h) return EWB_EINVAL;
   ++h->gen;
-  h->stream = stream ? reinterpret_cast<cudaStream_t>(stream) : h->own_stream;
+  // 0 is the legacy default stream (torch's default stream), as for any
+  // CUDA API; ewb_use_own_stream rebinds the handle's own stream
+  h->stream = reinterpret_cast<cudaStream_t>(stream);
+  return EWB_OK;
+}
+
+int ewb_use_own_stream(ewb_handle *h) {
+  if (!h) return EWB_EINVAL;
+  ++h->gen;
+  h->stream = h->own_stream;
   return EWB_OK;
 }
 
@@ -2214,7 +2264,7 @@ int ewb_evaluate(ewb_handle *h, const double *pos, const double *q, int64_t n,
   CK(cudaStreamSynchronize(h->cstream));  // rho (copied after segment 3)
   int e = 0;
   std::memcpy(&e, h->hscr + 3, sizeof(int));
-  e &= ((h->coul_on && h->rc > 0.5 * h->L && !h->lj_on) ? 0 : ERR_UNWRAPPED) | ERR_COINCIDENT;
+  e &= err_mask(h);
   if (e) {
     CK(cudaMemcpy(force_inout, h->force_in.p, n * 3 * sizeof(double), cudaMemcpyDeviceToHost));
     if (e & ERR_UNWRAPPED)
@@ -2303,6 +2353,84 @@ int ewb_dev_real_space(ewb_handle *h, int part, int nparts, double *d_force, dou
   return EWB_OK;
 }
 
+int ewb_set_geometry_n(ewb_handle *h, int64_t n_global) {
+  if (!h) return EWB_EINVAL;
+  if (n_global < 0) return h->fail(EWB_EINVAL, "negative particle count");
+  h->geom_n = n_global;
+  ++h->gen;
+  return EWB_OK;
+}
+
+int ewb_rs_geometry(ewb_handle *h, int64_t *info4) {
+  if (!h || !info4) return EWB_EINVAL;
+  if (!h->have_system) return h->fail(EWB_ESTATE, "ewb_set_system first");
+  double rc_t, rc2_t;
+  rs_cutoff(h, rc_t, rc2_t);
+  const bool wide = h->coul_on && h->rc > 0.5 * h->L;
+  if (!(rc_t > 0.0) || (wide && !h->lj_on)) {  // one "row": image shell or no pair term
+    info4[0] = 1; info4[1] = 1; info4[2] = 1; info4[3] = 1;
+    return EWB_OK;
+  }
+  const RSGeom g = rs_geometry(h, rc_t, h->n);
+  info4[0] = g.cpd_eff;
+  info4[1] = g.rad;
+  info4[2] = (int64_t)g.cpd_eff * g.cpd_eff;
+  info4[3] = g.fold ? 1 : 0;
+  return EWB_OK;
+}
+
+// row of cells (cy + cpd cz) of every particle, binned exactly as the pair
+// kernel's cell list (k4_bin_count)
+__global__ void k_rows(const double *__restrict__ pos, int64_t n, double edge, int cpd,
+                       int *__restrict__ rows) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int id[2] = {0, 0};
+  if (cpd > 1) {
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      const double f = floor(pos[3 * i + 1 + a] / edge);
+      id[a] = (f >= 0.0) ? (f < (double)cpd ? (int)f : cpd - 1) : 0;  // NaN -> 0
+    }
+  }
+  rows[i] = id[0] + cpd * id[1];
+}
+
+int ewb_dev_rows(ewb_handle *h, const double *d_pos, int64_t n, int *d_rows) {
+  int64_t g[4];
+  int rc = ewb_rs_geometry(h, g);
+  if (rc) return rc;
+  if (n < 0 || (n > 0 && (!d_pos || !d_rows))) return h->fail(EWB_EINVAL, "bad arrays");
+  if (n == 0) return EWB_OK;
+  CK(cudaSetDevice(h->device));
+  k_rows<<<blocks_for(n, 256), 256, 0, h->stream>>>(d_pos, n, h->L / (double)g[0], (int)g[0],
+                                                   d_rows);
+  CKL();
+  return EWB_OK;
+}
+
+int ewb_dev_real_space_rows(ewb_handle *h, int row_lo, int row_hi, double *d_force,
+                            double *u_sr) {
+  int rc = require_state(h, false, true);
+  if (rc) return rc;
+  if (row_lo < 0 || row_hi < row_lo) return h->fail(EWB_EINVAL, "bad row range");
+  CK(cudaSetDevice(h->device));
+  if (u_sr && (rc = check_errflag(h, ERR_UNWRAPPED))) return rc;
+  CK(h->energy.ensure(8 * sizeof(double)));
+  h->row_lo = row_lo;
+  h->row_hi = row_hi;
+  rc = stage_real_space(h, 0, 1, d_force, h->energy.as<double>(), nullptr);
+  h->row_lo = h->row_hi = -1;
+  if (rc) return rc;
+  if (!u_sr) return EWB_OK;
+  double u = 0.0;
+  CK(cudaMemcpyAsync(&u, h->energy.as<double>(), sizeof(double), cudaMemcpyDeviceToHost,
+                     h->stream));
+  if ((rc = check_errflag(h, ERR_COINCIDENT))) return rc;
+  *u_sr = u;
+  return EWB_OK;
+}
+
 // The device energy slots (u_sr, u_lr, u_self of the last asynchronous
 // stages) copied into caller device memory on the handle's stream.
 int ewb_dev_energies(ewb_handle *h, double *d_out3) {
@@ -2316,6 +2444,25 @@ int ewb_dev_energies(ewb_handle *h, double *d_out3) {
   return EWB_OK;
 }
 
+// the masked device error flag of the last load/evaluation as a double in
+// caller device memory (stream-ordered, no host synchronisation): a
+// multi-rank driver reduces it with the energies so that every rank raises
+// the same error together
+__global__ void k_status(const int *__restrict__ err, int mask, double *__restrict__ out) {
+  out[0] = (double)(*err & mask);
+}
+
+int ewb_dev_status(ewb_handle *h, double *d_out) {
+  int rc = require_state(h, false, false);
+  if (rc) return rc;
+  if (!d_out) return h->fail(EWB_EINVAL, "null status buffer");
+  CK(cudaSetDevice(h->device));
+  CK(h->errflag.ensure(sizeof(int)));
+  k_status<<<1, 1, 0, h->stream>>>(h->errflag.as<int>(), err_mask(h), d_out);
+  CKL();
+  return EWB_OK;
+}
+
 // Synchronise the handle's stream and report device-side errors of the
 // asynchronous stages (unwrapped positions, coincident particles).
 int ewb_dev_check(ewb_handle *h) {
@@ -2323,15 +2470,20 @@ int ewb_dev_check(ewb_handle *h) {
   if (rc) return rc;
   CK(cudaSetDevice(h->device));
   CK(h->errflag.ensure(sizeof(int)));
-  return check_errflag(h, ERR_UNWRAPPED | ERR_COINCIDENT);
+  return check_errflag(h, err_mask(h));
 }
 
 int ewb_dev_self_energy(ewb_handle *h, double *u_self) {
+  return ewb_dev_self_energy_range(h, 0, h ? h->n : 0, u_self);
+}
+
+int ewb_dev_self_energy_range(ewb_handle *h, int64_t i0, int64_t i1, double *u_self) {
   int rc = require_state(h, false, true);
   if (rc) return rc;
+  if (i0 < 0 || i1 > h->n || i0 > i1) return h->fail(EWB_EINVAL, "bad particle range");
   CK(cudaSetDevice(h->device));
   CK(h->energy.ensure(8 * sizeof(double)));
-  if ((rc = stage_self(h, h->energy.as<double>() + 2))) return rc;
+  if ((rc = stage_self(h, h->energy.as<double>() + 2, i0, i1))) return rc;
   if (!u_self) return EWB_OK;  // asynchronous: stays in the device energy slot
   double u = 0.0;
   CK(cudaMemcpyAsync(&u, h->energy.as<double>() + 2, sizeof(double), cudaMemcpyDeviceToHost,
@@ -2352,7 +2504,7 @@ int ewb_dev_evaluate(ewb_handle *h, const double *d_pos, const double *d_q, int6
   double en[3];
   CK(cudaMemcpyAsync(en, h->energy.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
   if ((rc = check_errflag(
-           h, ((h->coul_on && h->rc > 0.5 * h->L && !h->lj_on) ? 0 : ERR_UNWRAPPED) |
+           h, err_mask(h) |
                   ERR_COINCIDENT)))
     return rc;
   if (energies) std::memcpy(energies, en, sizeof en);

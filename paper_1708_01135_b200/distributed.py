@@ -1,37 +1,52 @@
 """Multi-GPU Ewald evaluation: one process per GPU over torch.distributed.
 
-The reference parallelises with worker threads over contiguous particle
-blocks and reduces per-worker copies of rho_hat in worker order
-(engine.py:75-91, 247-254); the paper does the same across MPI ranks with a
-global reduction of rho_hat.  Here each rank owns:
+The paper decomposes the domain over MPI ranks, exchanges halos for the
+real-space loop and reduces rho_hat globally; the
+reference shards particles over worker threads and reduces per-worker copies
+of rho_hat in worker order (engine.py:75-91, 247-254).  Here every rank owns
+the particles of a contiguous range of rows of cells (a row is the line of
+cells (cy, cz) along x, numbered cy + cpd cz, so a row range is a z-slab with
+at most two partial layers; every rank bins on the grid of the global
+particle count, ewb_set_geometry_n):
 
-* reciprocal space: a contiguous particle shard [i0, i1) -- it computes the
-  partial S(k) of its shard, the partials are summed by ONE all-reduce
-  (NCCL over NVLink; the only data-path collective), and it gathers the
-  reciprocal forces of its own shard from the complete S(k);
-* real space: a z-slab of the cell grid (``ewb_dev_real_space(part,
-  nparts)``); positions are replicated on every rank (the caller hands the
-  full configuration, as the reference API does), so no halo exchange is
-  needed and the ordered-pair write-to-centre convention (engine.py:10-14)
-  means no force communication inside the pair loop;
-* the per-rank force contributions and the rank's real-space energy travel
-  in ONE all-reduce buffer [F (3N) | u_sr | u_lr | u_self] (u_lr and u_self
-  are complete on every rank and enter from rank 0 only), so every rank
-  returns the full force array (drop-in semantics).  The step enqueues all
-  device work and collectives without a host synchronisation; the single
-  synchronisation at the end reads the energies and the deferred device
-  error flag (coincident particles, unwrapped positions).
-* on CUDA the rank's real-space slab runs on a side stream concurrently with
-  the reciprocal chain (S(k) partial, its all-reduce, finalisation); the
-  streams join before the reciprocal forces, which add into the same
-  buffer.  The stages use disjoint scratch (as in the single-GPU overlap).
+* halo exchange: a rank needs the particles of the rows its centres' stencil
+  reaches beyond its own rows -- with the half shell only the rows at
+  lexicographically positive (oz, oy) offsets, i.e. the slab above it (two or
+  more hops when a slab is thinner than the stencil, e.g. c4 on 8 GPUs).  Each
+  rank sends (x, y, z, q) of its particles in every peer's halo rows by
+  grouped point-to-point sends/receives (batch_isend_irecv: ncclSend/ncclRecv
+  over NVLink); the counts travel first in one all-gather.
+* real space: the pair kernel runs over own + halo particles with centres
+  restricted to the own rows (ewb_dev_real_space_rows).  The half shell puts
+  F_j = -F_i also on halo partners; those forces go back to their owners by
+  the reverse exchange, so every pair is evaluated exactly once in the job.
+* reciprocal space: each rank's S(k) partial over its own particles (the
+  tensor-core GEMM), ONE all-reduce of the partials (the only collective on
+  the data path besides the halo exchanges) -- overlapped with the real-space
+  pair kernel, which runs on a side stream -- then every rank finalises S(k)
+  and gathers the reciprocal forces of its own particles.
+* energies: [u_sr, u_lr, u_self, device error flag] in one small all-reduce
+  (u_lr counted on rank 0 only); the error flag (coincident particles,
+  unwrapped positions) is reduced with them, so every rank raises the same
+  exception together and no caller force array is touched.
+
+``SlabEwald`` is the domain-decomposed interface (each rank holds only its
+own particles).  ``ShardedEwald`` is the drop-in over the reference API,
+where every rank holds the full configuration: it selects its own rows'
+particles, runs SlabEwald, and returns the full force array by an all-gather
+of the owned rows (no 3N all-reduce).
 
 ``stages`` is the device-stage interface (``DeviceStages`` wraps the C-ABI);
-tests inject a CPU stand-in to run this orchestration under ``gloo``.
+the tests inject a CPU stand-in (tests/cpu_stages.py) to run this
+orchestration under ``gloo`` without a GPU.
 """
 
+import numpy as np
 import torch
 import torch.distributed as dist
+
+from . import _lib
+from .core import CoincidentParticlesError
 
 
 def shard_range(n, rank, world):
@@ -41,124 +56,300 @@ def shard_range(n, rank, world):
     return i0, i0 + base + (1 if rank < rem else 0)
 
 
+def row_bounds(n_rows, world):
+    """Rows [lo, hi) of every rank: an even split of the rows of cells."""
+    return [(n_rows * r // world, n_rows * (r + 1) // world) for r in range(world)]
+
+
+def halo_rows(lo, hi, cpd, rad, half):
+    """Rows outside [lo, hi) that the stencil of the rows [lo, hi) reaches:
+    with the half shell only the offsets (oz, oy) > (0, 0) lexicographically
+    (the pair kernel's own rule), else the full (2 rad + 1)^2 stencil."""
+    if hi <= lo:
+        return np.zeros(0, dtype=np.int64)
+    r = np.arange(lo, hi)
+    cy, cz = r % cpd, r // cpd
+    out = []
+    for oz in range(-rad, rad + 1):
+        for oy in range(-rad, rad + 1):
+            if oz == 0 and oy == 0:
+                continue
+            if half and (oz < 0 or (oz == 0 and oy < 0)):
+                continue
+            out.append((cy + oy) % cpd + cpd * ((cz + oz) % cpd))
+    rows = np.unique(np.concatenate(out))
+    return rows[(rows < lo) | (rows >= hi)]
+
+
 class DeviceStages:
     """C-ABI device stages on torch CUDA tensors (product path)."""
 
     def __init__(self, handle):
         self.h = handle
 
+    @property
+    def half_shell(self):
+        return not getattr(self.h, "deterministic", False)
+
     def set_stream(self, stream):
-        self.h.set_stream(stream.cuda_stream)
+        if stream is None:
+            self.h.use_own_stream()
+        else:
+            self.h.set_stream(stream.cuda_stream)
 
     def slot_size(self):
         return self.h.dev_slot_doubles()
 
+    def set_geometry_n(self, n):
+        self.h.set_geometry_n(n)
+
+    def geometry(self):
+        return self.h.rs_geometry()
+
+    def rows(self, pos):
+        """Row of cells of every particle, on torch's current stream (the
+        result is consumed by torch operations)."""
+        self.h.set_stream(torch.cuda.current_stream(pos.device).cuda_stream)
+        out = torch.empty(pos.shape[0], dtype=torch.int32, device=pos.device)
+        self.h.dev_rows(pos.data_ptr(), pos.shape[0], out.data_ptr())
+        return out
+
     def load(self, pos, q):
         self.h.dev_load(pos.data_ptr(), q.data_ptr(), q.shape[0])
 
-    def real_space(self, part, nparts, force):
-        return self.h.dev_real_space(part, nparts, force.data_ptr())
-
-    def real_space_async(self, part, nparts, force):
-        self.h.dev_real_space_async(part, nparts, force.data_ptr())
-
-    def finalize_async(self, slots, rho_out=None):
-        self.h.dev_kspace_finalize_async(
-            slots.data_ptr(), None if rho_out is None else rho_out.data_ptr())
-
-    def self_energy_async(self):
-        self.h.dev_self_energy_async()
-
-    def energies(self, out3):
-        """device slots (u_sr, u_lr, u_self) -> out3 (device tensor, 3)"""
-        self.h.dev_energies(out3.data_ptr())
-
-    def check(self):
-        self.h.dev_check()
+    def real_space_rows(self, lo, hi, force):
+        self.h.dev_real_space_rows_async(lo, hi, force.data_ptr())
 
     def rho_partial(self, i0, i1, slots):
         self.h.dev_rho_partial(i0, i1, slots.data_ptr())
 
     def finalize(self, slots, rho_out=None):
-        return self.h.dev_kspace_finalize(
+        self.h.dev_kspace_finalize_async(
             slots.data_ptr(), None if rho_out is None else rho_out.data_ptr())
 
     def recip_forces(self, i0, i1, force):
         self.h.dev_recip_forces(i0, i1, force.data_ptr())
 
-    def self_energy(self):
-        return self.h.dev_self_energy()
+    def self_energy_range(self, i0, i1):
+        self.h.dev_self_energy_range_async(i0, i1)
+
+    def energies(self, out4):
+        """device slots (u_sr, u_lr, u_self) and the error flag -> out4"""
+        self.h.dev_energies(out4.data_ptr())
+        self.h.dev_status(out4[3:].data_ptr())
 
 
-class ShardedEwald:
-    """Particle-sharded Ewald evaluation across the ranks of a group."""
+class _Comm:
+    """Collectives of one process group; gloo stages through host memory."""
 
-    def __init__(self, stages, device, group=None, overlap=True):
-        self.st = stages
-        self.device = device
+    def __init__(self, group, device):
         self.group = group
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
-        self._slots = None
-        cuda = torch.device(device).type == "cuda"
-        self._side = torch.cuda.Stream(device=device) if overlap and cuda else None
-        self._main = torch.cuda.Stream(device=device) if overlap and cuda else None
+        backend = dist.get_backend(group) if dist.is_initialized() else "none"
+        self.host = backend != "nccl"
+        self.dev = torch.device("cpu") if self.host else torch.device(device)
 
-    def _allreduce(self, t):
-        if self.world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+    def _to(self, t):
+        return t.to(self.dev) if t.device != self.dev else t
+
+    def allreduce_(self, t):
+        if self.world == 1:
+            return t
+        x = self._to(t)
+        dist.all_reduce(x, op=dist.ReduceOp.SUM, group=self.group)
+        if x is not t:
+            t.copy_(x)
+        return t
+
+    def counts(self, c):
+        """c[p] = rows this rank sends to peer p -> M[src][dst] of all ranks."""
+        if self.world == 1:
+            return np.array([c])
+        mine = self._to(torch.tensor(c, dtype=torch.int64))
+        allc = [torch.empty_like(mine) for _ in range(self.world)]
+        dist.all_gather(allc, mine, group=self.group)
+        return np.stack([a.cpu().numpy() for a in allc])
+
+    def exchange(self, send, recv_counts, width, dtype, device):
+        """Grouped point-to-point: send[p] (rows, width) to peer p, receive
+        recv_counts[p] rows from p.  Returns the received blocks by peer."""
+        ops, recv = [], [None] * self.world
+        bufs = {}
+        for p in range(self.world):
+            if p == self.rank:
+                continue
+            if recv_counts[p] > 0:
+                bufs[p] = torch.empty((int(recv_counts[p]), width), dtype=dtype, device=self.dev)
+                ops.append(dist.P2POp(dist.irecv, bufs[p], p, self.group))
+            if send[p] is not None and send[p].shape[0] > 0:
+                ops.append(dist.P2POp(dist.isend, self._to(send[p]).contiguous(), p, self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        for p, b in bufs.items():
+            recv[p] = b.to(device) if b.device != torch.device(device) else b
+        return recv
+
+    def all_gather_rows(self, t, counts, width):
+        """Every rank's t (counts[r] rows) -> list of blocks by rank."""
+        if self.world == 1:
+            return [t]
+        m = int(max(counts))
+        pad = torch.zeros((m, width), dtype=t.dtype, device=self.dev)
+        pad[:t.shape[0]] = self._to(t)
+        out = [torch.empty_like(pad) for _ in range(self.world)]
+        dist.all_gather(out, pad, group=self.group)
+        return [o[:int(c)].to(t.device) for o, c in zip(out, counts)]
+
+
+def _raise_device_error(flag):
+    flag = int(flag)
+    if flag & _lib.ERR_UNWRAPPED:
+        raise ValueError("positions must be wrapped into [0, L) before binning")
+    if flag & _lib.ERR_COINCIDENT:
+        raise CoincidentParticlesError("coincident particles in Coulomb kernel")
+
+
+class SlabEwald:
+    """Domain-decomposed Ewald evaluation: each rank owns the particles of
+    its rows of cells (see the module docstring)."""
+
+    def __init__(self, stages, device, n_global, group=None, overlap=True):
+        self.st = stages
+        self.device = torch.device(device)
+        self.comm = _Comm(group, device)
+        self.rank, self.world = self.comm.rank, self.comm.world
+        self.n_global = int(n_global)
+        stages.set_geometry_n(self.n_global)
+        g = stages.geometry()
+        self.cpd, self.rad, self.n_rows, self.fold = g["cpd"], g["rad"], g["n_rows"], g["fold"]
+        self.bounds = row_bounds(self.n_rows, self.world)
+        self.lo, self.hi = self.bounds[self.rank]
+        half = stages.half_shell
+        need = np.zeros((self.world, self.n_rows), dtype=bool)
+        for s, (lo, hi) in enumerate(self.bounds):
+            if self.fold:        # one row: its owner scans everything
+                continue
+            need[s, halo_rows(lo, hi, self.cpd, self.rad, half)] = True
+        self.need = torch.from_numpy(need).to(self.device)
+        self._slots = None
+        cuda = self.device.type == "cuda"
+        self._main = torch.cuda.Stream(device=self.device) if cuda else None
+        self._side = torch.cuda.Stream(device=self.device) if cuda and overlap else None
+
+    def owned_mask(self, rows, rank=None):
+        lo, hi = self.bounds[self.rank if rank is None else rank]
+        return (rows >= lo) & (rows < hi)
+
+    def evaluate_local(self, pos, q, force, rho_out=None):
+        """pos (n_own, 3), q (n_own,): this rank's particles (all in its rows);
+        force (n_own, 3) += their Coulomb force.  Returns the job's
+        (u_sr, u_lr, u_self), identical on every rank."""
+        if self._main is None:
+            return self._evaluate(pos, q, force, rho_out)
+        cur = torch.cuda.current_stream(self.device)
+        self._main.wait_stream(cur)
+        try:
+            with torch.cuda.stream(self._main):
+                self.st.set_stream(self._main)
+                out = self._evaluate(pos, q, force, rho_out)
+        finally:
+            self.st.set_stream(None)       # back to the handle's own stream
+            cur.wait_stream(self._main)
+        return out
+
+    def _evaluate(self, pos, q, force, rho_out):
+        st, comm, dev = self.st, self.comm, self.device
+        n_own = q.shape[0]
+        rows = st.rows(pos).long()
+        # ---- halo exchange: (x, y, z, q) of my particles in every peer's halo
+        send_idx, send = [None] * self.world, [None] * self.world
+        for p in range(self.world):
+            if p != self.rank:
+                send_idx[p] = torch.nonzero(self.need[p][rows]).flatten()
+                send[p] = torch.cat([pos[send_idx[p]], q[send_idx[p], None]], dim=1)
+        cnt = [0 if s is None else int(s.shape[0]) for s in send]
+        M = comm.counts(cnt)
+        recv_counts = M[:, self.rank]
+        recv = comm.exchange(send, recv_counts, 4, torch.float64, dev)
+        halo = [r for r in recv if r is not None]
+        if halo:
+            h = torch.cat(halo)
+            lpos = torch.cat([pos, h[:, :3]]).contiguous()
+            lq = torch.cat([q, h[:, 3]]).contiguous()
+        else:
+            lpos, lq = pos.contiguous(), q.contiguous()
+        n_loc = lq.shape[0]
+        flocal = torch.zeros((n_loc, 3), dtype=torch.float64, device=dev)
+        ns = st.slot_size()
+        if self._slots is None or self._slots.numel() != ns:
+            self._slots = torch.empty(ns, dtype=torch.float64, device=dev)
+        en = torch.zeros(4, dtype=torch.float64, device=dev)
+        st.load(lpos, lq)
+        # ---- real space of my rows beside the reciprocal chain
+        if self._side is not None:
+            self._side.wait_stream(self._main)
+            st.set_stream(self._side)
+            st.real_space_rows(self.lo, self.hi, flocal)
+            st.set_stream(self._main)
+        else:
+            st.real_space_rows(self.lo, self.hi, flocal)
+        st.rho_partial(0, n_own, self._slots)
+        comm.allreduce_(self._slots)          # S(k) = sum of the ranks' partials
+        st.finalize(self._slots, rho_out)
+        if self._side is not None:
+            self._main.wait_stream(self._side)  # both add into flocal
+        st.recip_forces(0, n_own, flocal)
+        st.self_energy_range(0, n_own)
+        st.energies(en)
+        if self.rank != 0:
+            en[1] = 0.0                        # u_lr is complete on every rank
+        # ---- reverse exchange: halo partners' forces back to their owners
+        back = [None] * self.world
+        off = n_own
+        for p in range(self.world):
+            c = int(recv_counts[p]) if p != self.rank else 0
+            if c:
+                back[p] = flocal[off:off + c]
+                off += c
+        got = comm.exchange(back, cnt, 3, torch.float64, dev)
+        comm.allreduce_(en)                    # energies + error flags of all ranks
+        u_sr, u_lr, u_self, err = en.tolist()
+        if err:
+            _raise_device_error(err)
+        force += flocal[:n_own]
+        for p in range(self.world):
+            if got[p] is not None and got[p].shape[0]:
+                force.index_add_(0, send_idx[p], got[p])
+        return u_sr, u_lr, u_self
+
+
+class ShardedEwald:
+    """Drop-in multi-GPU evaluation over the reference API: every rank holds
+    the full configuration and returns the full force array."""
+
+    def __init__(self, stages, device, group=None, overlap=True):
+        self.st = stages
+        self.device = torch.device(device)
+        self.group = group
+        self.overlap = overlap
+        self.slab = None
 
     def evaluate(self, pos, q, force, rho_out=None):
         """force (N,3) += Coulomb force on every rank; returns
         (u_sr, u_lr, u_self) -- identical on every rank."""
-        if self._side is None:
-            return self._evaluate(pos, q, force, rho_out, None)
-        # the device stages and the collectives run on an explicit stream
-        # (the caller's, unless it is the legacy default stream, which the
-        # non-blocking side stream would not order against)
-        cur = torch.cuda.current_stream(self.device)
-        main = self._main if cur.cuda_stream == 0 else cur
-        if main is not cur:
-            main.wait_stream(cur)
-        with torch.cuda.stream(main):
-            self.st.set_stream(main)
-            out = self._evaluate(pos, q, force, rho_out, main)
-        if main is not cur:
-            cur.wait_stream(main)
-        return out
-
-    def _evaluate(self, pos, q, force, rho_out, main):
         n = q.shape[0]
-        ns = self.st.slot_size()
-        if self._slots is None or self._slots.numel() != ns:
-            self._slots = torch.empty(ns, dtype=torch.float64, device=self.device)
-        i0, i1 = shard_range(n, self.rank, self.world)
-        if self.world > 1:
-            buf = torch.zeros(3 * n + 3, dtype=torch.float64, device=self.device)
-            contrib, en = buf[:3 * n].view(n, 3), buf[3 * n:]
-        else:
-            contrib, en = force, torch.empty(3, dtype=torch.float64, device=self.device)
-        self.st.load(pos, q)
-        if main is not None:                   # real space beside the reciprocal chain
-            self._side.wait_stream(main)
-            self.st.set_stream(self._side)
-            self.st.real_space_async(self.rank, self.world, contrib)
-            self.st.set_stream(main)
-        self.st.rho_partial(i0, i1, self._slots)
-        self._allreduce(self._slots)           # S(k) = sum over shards
-        self.st.finalize_async(self._slots, rho_out)
-        if main is not None:
-            main.wait_stream(self._side)       # both add into contrib
-        else:
-            self.st.real_space_async(self.rank, self.world, contrib)
-        self.st.recip_forces(i0, i1, contrib)
-        self.st.self_energy_async()
-        self.st.energies(en)
-        if self.world > 1:
-            if self.rank != 0:
-                en[1:].zero_()                 # complete on every rank: count once
-            self._allreduce(buf)               # forces + energies, one collective
-            force += contrib
-        self.st.check()
-        u_sr, u_lr, u_self = en.tolist()
-        return u_sr, u_lr, u_self
+        if self.slab is None or self.slab.n_global != n:
+            self.slab = SlabEwald(self.st, self.device, n, self.group, self.overlap)
+        sl = self.slab
+        rows = self.st.rows(pos).long()       # same on every rank
+        owned = [torch.nonzero(sl.owned_mask(rows, r)).flatten() for r in range(sl.world)]
+        mine = owned[sl.rank]
+        f_own = torch.zeros((mine.shape[0], 3), dtype=torch.float64, device=self.device)
+        u = sl.evaluate_local(pos[mine].contiguous(), q[mine].contiguous(), f_own,
+                              rho_out=rho_out)
+        blocks = sl.comm.all_gather_rows(f_own, [o.shape[0] for o in owned], 3)
+        for idx, b in zip(owned, blocks):
+            force.index_add_(0, idx, b)
+        return u

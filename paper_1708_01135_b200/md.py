@@ -31,7 +31,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .core import LatticeError, SimulationBox, create_particle_set
+from .core import LatticeError, SimulationBox, create_particle_set, require_neutral
 from .ewald import EwaldSolver, choose_parameters
 
 DEFAULT_SIGMA = 2.5
@@ -214,26 +214,46 @@ def velocity_verlet_step(ps, dt, force_assembler, timings=None):
 
     h = _md_handle(ps.box)
     dev = torch.device("cuda", h.device)
-    h.set_stream(torch.cuda.current_stream(dev).cuda_stream)
+    # copies and kernels on one explicit stream the handle is bound to, and
+    # a synchronisation before every host read (the handle's kernels and
+    # torch's copies are otherwise unordered)
+    stream = _md_stream(dev)
+    h.set_stream(stream.cuda_stream)
     t0 = time.perf_counter()
-    pos = torch.from_numpy(np.ascontiguousarray(ps.position)).to(dev)
-    vel = torch.from_numpy(np.ascontiguousarray(ps.velocity)).to(dev)
-    frc = torch.from_numpy(np.ascontiguousarray(ps.force)).to(dev)
-    mass = torch.from_numpy(np.ascontiguousarray(ps.mass)).to(dev)
     n = ps.count
-    h.dev_md_kick_drift(pos.data_ptr(), vel.data_ptr(), frc.data_ptr(),
-                        mass.data_ptr(), n, dt)
-    ps.position[:] = pos.cpu().numpy()
-    ps.velocity[:] = vel.cpu().numpy()
+    with torch.cuda.stream(stream):
+        pos = torch.from_numpy(np.ascontiguousarray(ps.position)).to(dev, non_blocking=False)
+        vel = torch.from_numpy(np.ascontiguousarray(ps.velocity)).to(dev, non_blocking=False)
+        frc = torch.from_numpy(np.ascontiguousarray(ps.force)).to(dev, non_blocking=False)
+        mass = torch.from_numpy(np.ascontiguousarray(ps.mass)).to(dev, non_blocking=False)
+        h.dev_md_kick_drift(pos.data_ptr(), vel.data_ptr(), frc.data_ptr(),
+                            mass.data_ptr(), n, dt)
+        pos_h, vel_h = pos.cpu(), vel.cpu()
+    stream.synchronize()
+    ps.position[:] = pos_h.numpy()
+    ps.velocity[:] = vel_h.numpy()
     t1 = time.perf_counter()
     force_assembler(ps)
     t2 = time.perf_counter()
-    frc.copy_(torch.from_numpy(np.ascontiguousarray(ps.force)))
-    h.dev_md_kick(vel.data_ptr(), frc.data_ptr(), mass.data_ptr(), n, dt, kick=True)
-    ps.velocity[:] = vel.cpu().numpy()
+    with torch.cuda.stream(stream):
+        frc.copy_(torch.from_numpy(np.ascontiguousarray(ps.force)))
+        h.dev_md_kick(vel.data_ptr(), frc.data_ptr(), mass.data_ptr(), n, dt, kick=True)
+        vel_h = vel.cpu()
+    stream.synchronize()
+    ps.velocity[:] = vel_h.numpy()
     t3 = time.perf_counter()
     if timings is not None:
         timings["t_integrate"] = (t1 - t0) + (t3 - t2)
+
+
+_MD_STREAMS = {}
+
+
+def _md_stream(dev):
+    import torch
+    if dev not in _MD_STREAMS:
+        _MD_STREAMS[dev] = torch.cuda.Stream(device=dev)
+    return _MD_STREAMS[dev]
 
 
 @dataclass
@@ -270,6 +290,14 @@ class RunMetrics:
         return float(np.median(vals)) if vals else 0.0
 
 
+class _Charges:
+    """Charge array with the ParticleSet interface require_neutral reads."""
+
+    def __init__(self, q):
+        self.charge = q
+        self.count = q.shape[0]
+
+
 class DeviceMD:
     """NVE dynamics with every per-particle array resident in HBM.
 
@@ -302,6 +330,7 @@ class DeviceMD:
             self.force = torch.zeros((self.n, 3), **f64)
             self.prev = torch.empty_like(self.pos)
         self.stream.synchronize()
+        self._q_host = _Charges(np.array(ps.charge, dtype=np.float64, copy=True))
         self.last = None
         self._neutral_checked = False
 
@@ -316,12 +345,9 @@ class DeviceMD:
                          "t_alg1": 0.0, "t_alg2": 0.0, "t_lj": 0.0}
             return 0.0
         if self.config.coulomb_on and not self._neutral_checked:
-            q_total = float(self.q.sum())
-            from .core import NEUTRALITY_TOL, NeutralityError
-            if abs(q_total) > NEUTRALITY_TOL:
-                raise NeutralityError(
-                    f"system carries net charge {q_total:.3e}; "
-                    f"periodic Coulomb energy requires neutrality")
+            # the reference's host expression (core.py:139-145) on the charges
+            # as uploaded, so accept/reject is identical
+            require_neutral(self._q_host)
             self._neutral_checked = True
         en, tm = self.h.dev_evaluate(self.pos.data_ptr(), self.q.data_ptr(), self.n,
                                      self.force.data_ptr(), None, timings=True)

@@ -1,10 +1,13 @@
 """CPU stand-in for the device stages (TEST INFRASTRUCTURE ONLY).
 
 Implements the stage interface of ``distributed.DeviceStages`` with the
-oracle so that ``distributed.ShardedEwald`` -- the multi-GPU orchestration
-(particle shards, S(k) all-reduce, real-space z-slabs, force all-reduce) --
-can be exercised under ``gloo`` on CPU.  The "slot" buffer here is simply the
-caller-order rho (2K doubles); the orchestration treats it as opaque.
+oracle so that the multi-GPU orchestration (``distributed.SlabEwald`` /
+``ShardedEwald``: row ownership, halo exchange, S(k) all-reduce, reverse
+force exchange, owned-row all-gather) can be exercised under ``gloo`` on
+CPU.  The "slot" buffer here is simply the caller-order rho (2K doubles).
+Real space is the oracle's write-to-centre evaluation of the given centre
+rows over the loaded (own + halo) particles, i.e. a full shell, so the
+orchestration fetches the full-stencil halo for it.
 """
 
 import math
@@ -16,31 +19,50 @@ from oracle import oracle as orc
 
 
 class OracleStages:
+    half_shell = False
+
     def __init__(self, L, alpha, r_cutoff, m_int):
         self.L, self.alpha, self.rc = float(L), float(alpha), float(r_cutoff)
         self.m = np.ascontiguousarray(m_int, dtype=np.int64)
         self.coeff = orc.kspace_coeff(self.m, self.L, self.alpha)
         self.S = None
+        self.cpd = max(1, int(math.floor(self.L / self.rc)))
+        self.fold = self.cpd < 3
 
     def slot_size(self):
         return 2 * self.m.shape[0]
+
+    def set_geometry_n(self, n):
+        pass
+
+    def geometry(self):
+        c = 1 if self.fold else self.cpd
+        return {"cpd": c, "rad": 1, "n_rows": c * c, "fold": int(self.fold)}
+
+    def rows(self, pos):
+        p = pos.detach().cpu().numpy()
+        if self.fold:
+            return torch.zeros(p.shape[0], dtype=torch.int32)
+        e = self.L / self.cpd
+        cy = np.clip(np.floor(p[:, 1] / e).astype(np.int64), 0, self.cpd - 1)
+        cz = np.clip(np.floor(p[:, 2] / e).astype(np.int64), 0, self.cpd - 1)
+        return torch.from_numpy((cy + self.cpd * cz).astype(np.int32))
 
     def load(self, pos, q):
         self.pos = pos.detach().cpu().numpy().astype(np.float64)
         self.q = q.detach().cpu().numpy().astype(np.float64)
 
-    def real_space(self, part, nparts, force):
-        cpd = int(math.floor(self.L / self.rc))
-        cz = np.clip(np.floor(self.pos[:, 2] / (self.L / cpd)).astype(np.int64), 0, cpd - 1)
-        zl, zh = cpd * part // nparts, cpd * (part + 1) // nparts
-        sel = np.nonzero((cz >= zl) & (cz < zh))[0]
-        f = np.zeros_like(self.pos)
+    def real_space_rows(self, lo, hi, force):
+        rows = self.rows(torch.from_numpy(self.pos)).numpy()
+        sel = np.nonzero((rows >= lo) & (rows < hi))[0]
+        self._u_sr = 0.0
         if sel.size == 0:
-            return 0.0
+            return
+        f = np.zeros_like(self.pos)
         u, f = orc.short_range(self.pos, self.q, self.L, self.rc, self.alpha,
                                sel=sel, force=f, threads=1)
         force += torch.from_numpy(f)
-        return u
+        self._u_sr = u
 
     def rho_partial(self, i0, i1, slots):
         if i1 > i0:
@@ -54,7 +76,7 @@ class OracleStages:
         K = self.m.shape[0]
         if rho_out is not None:
             rho_out.copy_(torch.from_numpy(self.S))
-        return float(np.sum(self.coeff * (self.S[:K] ** 2 + self.S[K:] ** 2)))
+        self._u_lr = float(np.sum(self.coeff * (self.S[:K] ** 2 + self.S[K:] ** 2)))
 
     def recip_forces(self, i0, i1, force):
         if i1 <= i0:
@@ -64,21 +86,12 @@ class OracleStages:
                        self.S, force=f, threads=1)
         force[i0:i1] += torch.from_numpy(f)
 
-    def self_energy(self):
-        return orc.self_energy(self.q, self.alpha)
+    def self_energy_range(self, i0, i1):
+        self._u_self = orc.self_energy(self.q[i0:i1], self.alpha) if i1 > i0 else 0.0
 
-    # asynchronous interface (energies kept until energies())
-    def real_space_async(self, part, nparts, force):
-        self._u_sr = self.real_space(part, nparts, force)
+    def energies(self, out4):
+        out4.copy_(torch.tensor([self._u_sr, self._u_lr, self._u_self, 0.0],
+                                dtype=torch.float64))
 
-    def finalize_async(self, slots, rho_out=None):
-        self._u_lr = self.finalize(slots, rho_out)
-
-    def self_energy_async(self):
-        self._u_self = self.self_energy()
-
-    def energies(self, out3):
-        out3.copy_(torch.tensor([self._u_sr, self._u_lr, self._u_self], dtype=torch.float64))
-
-    def check(self):
+    def set_stream(self, stream):
         pass

@@ -95,22 +95,27 @@ def test_configs_match_reference_golden(ew, name):
     K = rs.n_stored
     k = g["k_idx"]
     rmax = max(np.abs(g["rho_re_sample"]).max(), np.abs(g["rho_im_sample"]).max())
-    assert np.abs(rs.rho.values[k] - g["rho_re_sample"]).max() <= RHO_TOL * rmax * 10
-    assert np.abs(rs.rho.values[K + k] - g["rho_im_sample"]).max() <= RHO_TOL * rmax * 10
+    assert np.abs(rs.rho.values[k] - g["rho_re_sample"]).max() <= RHO_TOL * rmax
+    assert np.abs(rs.rho.values[K + k] - g["rho_im_sample"]).max() <= RHO_TOL * rmax
     # size-independent properties: net force ~ 0 (momentum), F_rms agrees
     assert abs(f_rms(ps.force) - fr) <= 1e-9 * fr
     if "force" in g:
         assert np.abs(ps.force - g["force"]).max() <= F_TOL * fr
 
 
-def test_c2_full_forces_vs_oracle(ew, orc):
-    cfg, ps, rs, res = _config_run(ew, "c2")
+@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
+def test_config_full_arrays_vs_oracle(ew, orc, name):
+    """Every force and every rho_hat entry of c2-c4 against the oracle (C
+    restatement pinned to the reference; all host threads): c3 exercises the
+    r_c/2 grid with several a-chunks of the S(k) GEMM and force-GEMM K
+    splits, c4 the r_c/3 grid with the 7^3 stencil and Gaussian charges."""
+    cfg, ps, rs, res = _config_run(ew, name)
     ref = orc.evaluate(cfg["pos"], cfg["q"], cfg["L"], cfg["alpha_ref"],
                        cfg["r_cutoff"], cfg["m_int"], coeff=rs.coeff)
     fr = f_rms(ref["force"])
-    assert np.abs(ps.force - ref["force"]).max() <= F_TOL * fr
-    assert np.abs(rs.rho.values - ref["rho"]).max() <= RHO_TOL * np.abs(ref["rho"]).max() * 10
     check_energies(res, ref["u_sr"], ref["u_lr"], ref["u_self"])
+    assert np.abs(ps.force - ref["force"]).max() <= F_TOL * fr
+    assert np.abs(rs.rho.values - ref["rho"]).max() <= RHO_TOL * np.abs(ref["rho"]).max()
 
 
 def test_rho_hat_alone(ew, orc):

@@ -10,13 +10,7 @@ import os
 
 import numpy as np
 
-from .core import (
-    BoxTooSmallError,
-    CoincidentParticlesError,
-    CutoffTooLargeError,
-    KSpaceEmptyError,
-    OracleSizeError,
-)
+from .core import error
 
 LIB_NAME = "libewaldb200.so"
 LIB_PATH = os.environ.get(
@@ -148,15 +142,15 @@ def raise_for(status, message, lib=None):
     if status == EWB_OK:
         return
     if status == EWB_ECOINCIDENT:
-        raise CoincidentParticlesError(message)
+        raise error("CoincidentParticlesError", message)
     if status == EWB_ECUTOFF:
-        raise CutoffTooLargeError(message)
+        raise error("CutoffTooLargeError", message)
     if status == EWB_EKSPACE:
-        raise KSpaceEmptyError(message)
+        raise error("KSpaceEmptyError", message)
     if status == EWB_EBOX:
-        raise BoxTooSmallError(message)
+        raise error("BoxTooSmallError", message)
     if status == EWB_ESIZE:
-        raise OracleSizeError(message)
+        raise error("OracleSizeError", message)
     if status in (EWB_EINVAL, EWB_EUNWRAPPED):
         raise ValueError(message)
     raise DeviceError(f"libewaldb200 status {status}: {message}")

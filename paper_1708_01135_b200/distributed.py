@@ -46,7 +46,7 @@ import torch
 import torch.distributed as dist
 
 from . import _lib
-from .core import CoincidentParticlesError
+from .core import error
 
 
 def shard_range(n, rank, world):
@@ -203,22 +203,98 @@ class _Comm:
         return [o[:int(c)].to(t.device) for o, c in zip(out, counts)]
 
 
+class ThreadGroup:
+    """W ranks driven by W host threads of ONE process (one GPU each): the
+    multi-GPU path behind the reference API's ``workers`` argument, where a
+    single caller thread owns the particle arrays (engine.py:256-277 fans the
+    same call out to worker threads).  Collectives meet at a barrier; device
+    tensors are posted after their producing stream has drained and read by
+    peer copies (NVLink), summed in rank order so every rank gets bitwise the
+    same result."""
+
+    def __init__(self, world, timeout=600.0):
+        import threading
+        self.world = int(world)
+        self.barrier = threading.Barrier(self.world, timeout=timeout)
+        self.slots = [None] * self.world
+
+    def abort(self):
+        self.barrier.abort()
+
+
+class ThreadComm:
+    """The _Comm interface over a ThreadGroup (rank = this thread's index)."""
+
+    host = False
+
+    def __init__(self, group, rank, device):
+        self.g = group
+        self.rank, self.world = int(rank), group.world
+        self.dev = torch.device(device)
+
+    def _sync(self):
+        if self.dev.type == "cuda":
+            torch.cuda.current_stream(self.dev).synchronize()
+
+    def _post(self, obj):
+        """Publish obj, wait for every rank's, return all of them."""
+        self._sync()
+        self.g.slots[self.rank] = obj
+        self.g.barrier.wait()
+        return list(self.g.slots)
+
+    def _done(self):
+        self._sync()                      # peer reads finished before reuse
+        self.g.barrier.wait()
+
+    def allreduce_(self, t):
+        if self.world == 1:
+            return t
+        allv = self._post(t)
+        acc = allv[0].to(t.device, copy=True)
+        for r in range(1, self.world):
+            acc += allv[r].to(t.device)
+        self._done()
+        t.copy_(acc)
+        return t
+
+    def counts(self, c):
+        allc = self._post(list(c))
+        self._done()
+        return np.array(allc)
+
+    def exchange(self, send, recv_counts, width, dtype, device):
+        allv = self._post(send)
+        recv = [None] * self.world
+        for p in range(self.world):
+            if p != self.rank and recv_counts[p] > 0:
+                recv[p] = allv[p][self.rank].to(device)
+        self._done()
+        return recv
+
+    def all_gather_rows(self, t, counts, width):
+        allv = self._post(t)
+        out = [a.to(t.device) for a in allv]
+        self._done()
+        return out
+
+
 def _raise_device_error(flag):
     flag = int(flag)
     if flag & _lib.ERR_UNWRAPPED:
         raise ValueError("positions must be wrapped into [0, L) before binning")
     if flag & _lib.ERR_COINCIDENT:
-        raise CoincidentParticlesError("coincident particles in Coulomb kernel")
+        raise error("CoincidentParticlesError", "coincident particles in Coulomb kernel")
 
 
 class SlabEwald:
     """Domain-decomposed Ewald evaluation: each rank owns the particles of
     its rows of cells (see the module docstring)."""
 
-    def __init__(self, stages, device, n_global, group=None, overlap=True):
+    def __init__(self, stages, device, n_global, group=None, overlap=True, comm=None):
         self.st = stages
         self.device = torch.device(device)
-        self.comm = _Comm(group, device)
+        self.comm = _Comm(group, device) if comm is None else comm
         self.rank, self.world = self.comm.rank, self.comm.world
         self.n_global = int(n_global)
         stages.set_geometry_n(self.n_global)
@@ -353,3 +429,106 @@ class ShardedEwald:
         for idx, b in zip(owned, blocks):
             force.index_add_(0, idx, b)
         return u
+
+
+def _resolve_devices(workers):
+    """The reference's ``workers`` read as a GPU count: None ->
+    $EWALDB200_WORKERS or 1, 0 -> every visible GPU, W -> min(W, visible GPUs)
+    ranks on devices 0..W-1 (a reference caller may pass its CPU thread count).
+    With $EWALDB200_SHARE_DEVICES=1 all W ranks run, round-robin over the
+    visible GPUs: ranks sharing a device stay correct (no kernel of one rank
+    waits on another's; the collectives meet on the host) -- the multi-rank
+    tests on a one-GPU box use this."""
+    import os
+    if workers is None:
+        workers = int(os.environ.get("EWALDB200_WORKERS", "1"))
+    n_dev = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    workers = int(workers)
+    if workers == 0:
+        workers = max(n_dev, 1)
+    if workers < 1:
+        raise ValueError(f"workers must be >= 0, got {workers}")
+    if n_dev == 0:
+        raise _lib.DeviceError("no CUDA device visible (this package has no CPU path)")
+    if os.environ.get("EWALDB200_SHARE_DEVICES", "0") != "1":
+        workers = min(workers, n_dev)
+    return [r % n_dev for r in range(workers)]
+
+
+class MultiDeviceEwald:
+    """``EwaldSolver(box, params, workers=W)`` with W > 1: W GPUs driven by W
+    host threads of the caller's process, each rank a SlabEwald over its rows
+    of cells (halo exchange, S(k) all-reduce, reverse force exchange) with a
+    ThreadGroup for the collectives.  Every rank reads the caller's full
+    configuration (the reference API hands it over whole), keeps its own
+    rows' particles, and writes their forces straight into the caller's
+    array -- disjoint rows, so no force reduction at all."""
+
+    def __init__(self, L, alpha, r_cutoff, m_int, coeff, devices, overlap=True):
+        from concurrent.futures import ThreadPoolExecutor
+        self.devices = [torch.device("cuda", int(d)) for d in devices]
+        self.world = len(self.devices)
+        self.overlap = overlap
+        self.n_stored = int(np.asarray(m_int).shape[0])
+        self.pool = ThreadPoolExecutor(self.world, thread_name_prefix="ewb-rank")
+
+        def make(r):
+            torch.cuda.set_device(self.devices[r])
+            h = _lib.Handle(self.devices[r].index)
+            h.set_system(L, alpha, r_cutoff)
+            h.set_kspace(m_int, coeff)
+            return h
+        self.handles = list(self.pool.map(make, range(self.world)))
+        self.stages = [DeviceStages(h) for h in self.handles]
+        self.slabs = [None] * self.world
+
+    def close(self):
+        self.pool.shutdown(wait=True)
+
+    def _rank(self, r, grp, pos, q, want_rho):
+        dev = self.devices[r]
+        torch.cuda.set_device(dev)
+        try:
+            st, n = self.stages[r], q.shape[0]
+            comm = ThreadComm(grp, r, dev)
+            sl = self.slabs[r]
+            if sl is None or sl.n_global != n:
+                sl = self.slabs[r] = SlabEwald(st, dev, n, overlap=self.overlap, comm=comm)
+            sl.comm = comm
+            tp = torch.from_numpy(pos).to(dev)
+            tq = torch.from_numpy(q).to(dev)
+            mine = torch.nonzero(sl.owned_mask(st.rows(tp).long())).flatten()
+            f_own = torch.zeros((mine.shape[0], 3), dtype=torch.float64, device=dev)
+            rho = (torch.empty(2 * self.n_stored, dtype=torch.float64, device=dev)
+                   if want_rho else None)
+            u = sl.evaluate_local(tp[mine].contiguous(), tq[mine].contiguous(), f_own,
+                                  rho_out=rho)
+            return (u, mine.cpu().numpy(), f_own.cpu().numpy(),
+                    None if rho is None else rho.cpu().numpy())
+        except BaseException:
+            grp.abort()                    # release peers waiting at a barrier
+            raise
+
+    def evaluate(self, pos, q, force, rho_out=None):
+        """Host arrays: pos (N,3), q (N,) -> force (N,3) += on the caller's
+        array, rho_out (2K,) overwritten if given; returns (u_sr, u_lr,
+        u_self).  All ranks raise the same device error together, before
+        any caller array is written."""
+        grp = ThreadGroup(self.world)
+        futs = [self.pool.submit(self._rank, r, grp, pos, q, rho_out is not None and r == 0)
+                for r in range(self.world)]
+        errs, res = [], []
+        for f in futs:
+            try:
+                res.append(f.result())
+            except BaseException as e:       # noqa: BLE001 -- re-raised below
+                errs.append(e)
+        if errs:
+            import threading
+            real = [e for e in errs if not isinstance(e, threading.BrokenBarrierError)]
+            raise (real or errs)[0]
+        for _, idx, fo, _ in res:
+            force[idx] += fo
+        if rho_out is not None:
+            rho_out[:] = res[0][3]
+        return res[0][0]

@@ -17,8 +17,12 @@ Reference interfaces mirrored (file:line in the reference package):
 * ``EwaldEnergies`` (:582-596), ``EwaldSolver`` (:599-655),
   ``total_coulomb`` (:658-665) -> ``ewb_evaluate``.
 
-``workers`` is accepted for signature compatibility and ignored: one
-process drives one GPU; multi-GPU sharding lives in ``distributed.py``.
+``workers`` is the GPU count: ``EwaldSolver(workers=W)``, W > 1,
+shards the evaluation over W GPUs of this process (one host thread per GPU,
+``distributed.MultiDeviceEwald``: rows of cells per GPU, halo exchange, one
+S(k) all-reduce); None reads $EWALDB200_WORKERS (default 1), 0 takes every
+visible GPU.  ``compute_rho_hat``/``long_range_energy_forces`` run on one GPU.
+One process per GPU under torch.distributed is ``distributed.ShardedEwald``.
 ``cell_list`` is accepted and ignored: the device builds its own.
 """
 
@@ -29,12 +33,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .core import (
-    BoxTooSmallError,
-    GlobalAccumulator,
-    KSpaceEmptyError,
-    require_neutral,
-)
+from .core import GlobalAccumulator, error, require_neutral
 
 
 @dataclass(frozen=True)
@@ -102,7 +101,8 @@ def choose_parameters(n, box, epsilon, alpha=None, r_cutoff=None):
     try:
         params.validate()
     except ValueError as err:
-        raise BoxTooSmallError(
+        raise error(
+            "BoxTooSmallError",
             f"no parameters meet tolerance {epsilon:.1e} in a box of edge "
             f"{L} A: {err}") from err
     return params
@@ -149,7 +149,8 @@ def enumerate_kvectors(box, params):
     bound = params.k_cutoff * L / (2.0 * math.pi)
     mmax = int(math.floor(bound))
     if mmax < 1:
-        raise KSpaceEmptyError(
+        raise error(
+            "KSpaceEmptyError",
             f"k_cutoff {params.k_cutoff:.4g} admits no reciprocal vector for "
             f"box edge {L} (need k_cutoff > 2*pi/L = {2.0 * math.pi / L:.4g})")
     rng = np.arange(-mmax, mmax + 1)
@@ -161,7 +162,8 @@ def enumerate_kvectors(box, params):
     half = (z > 0) | ((z == 0) & (y > 0)) | ((z == 0) & (y == 0) & (x > 0))
     m = m[below & half]
     if m.shape[0] == 0:
-        raise KSpaceEmptyError(
+        raise error(
+            "KSpaceEmptyError",
             f"k_cutoff {params.k_cutoff:.4g} admits no reciprocal vector")
     return ReciprocalSpace(box, params, m.astype(np.int64))
 
@@ -258,6 +260,11 @@ def self_energy(ps, params):
     return _SELF_HANDLE.self_energy(q)
 
 
+def _env_workers():
+    import os
+    return os.environ.get("EWALDB200_WORKERS")
+
+
 @dataclass
 class EwaldEnergies:
     """Energy breakdown and per-component device times of one evaluation."""
@@ -292,6 +299,16 @@ class EwaldSolver:
         self._h = _lib.Handle()
         self._h.set_system(box.edge_length, params.alpha, params.r_cutoff)
         self._h.set_kspace(self.recip.m_int, self.recip.coeff)
+        # workers = GPU count: W > 1 shards the evaluation over
+        # W GPUs of this process (distributed.MultiDeviceEwald); the image-
+        # shell path (r_c > L/2, N <= 4096) stays on one GPU
+        self._multi = None
+        if (workers is not None or _env_workers() is not None) and not self.wide_cutoff:
+            from .distributed import MultiDeviceEwald, _resolve_devices
+            devices = _resolve_devices(workers)
+            if len(devices) > 1:
+                self._multi = MultiDeviceEwald(box.edge_length, params.alpha, params.r_cutoff,
+                                               self.recip.m_int, self.recip.coeff, devices)
 
     @property
     def handle(self):
@@ -308,7 +325,14 @@ class EwaldSolver:
         rv = self.recip.rho.values
         direct = _writable_f64(rv, 2 * self.recip.n_stored)
         rho = rv if direct else np.empty(2 * self.recip.n_stored)
-        en, tm = self._h.evaluate(pos, q, f, rho)
+        if self._multi is not None:
+            import time
+            t0 = time.perf_counter()
+            en = self._multi.evaluate(pos, q, f, rho)
+            # one wall-clock figure: the ranks' stages overlap across GPUs
+            tm = (0.0, time.perf_counter() - t0, 0.0, 0.0)
+        else:
+            en, tm = self._h.evaluate(pos, q, f, rho)
         if copied:
             ps.force[:] = f
         if not direct:

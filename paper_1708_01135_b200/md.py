@@ -31,7 +31,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .core import LatticeError, SimulationBox, create_particle_set, require_neutral
+from .core import SimulationBox, error, create_particle_set, require_neutral
 from .ewald import EwaldSolver, choose_parameters
 
 DEFAULT_SIGMA = 2.5
@@ -97,7 +97,8 @@ class SimConfig:
 def rocksalt_cells_for(n):
     c = round((n ** (1.0 / 3.0)) / 2.0)
     if c < 1 or (2 * c) ** 3 != n:
-        raise LatticeError(
+        raise error(
+            "LatticeError",
             f"N = {n} is not (2c)^3 for integer c; no alternating rock-salt "
             f"lattice closes at this count")
     return c
@@ -107,7 +108,7 @@ def init_rocksalt(cells_per_dim, spacing):
     """Alternating +-1 charges on a simple cubic lattice (driver.py:54-78)."""
     cells_per_dim = int(cells_per_dim)
     if cells_per_dim < 1:
-        raise LatticeError(f"cells_per_dim must be >= 1, got {cells_per_dim}")
+        raise error("LatticeError", f"cells_per_dim must be >= 1, got {cells_per_dim}")
     side = 2 * cells_per_dim
     ps = create_particle_set(side**3, SimulationBox(side * spacing))
     idx = np.arange(side)

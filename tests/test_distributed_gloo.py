@@ -114,3 +114,69 @@ def test_shard_range_partition():
             assert all(rs[i][1] == rs[i + 1][0] for i in range(w - 1))
             sizes = [b - a for a, b in rs]
             assert max(sizes) - min(sizes) <= 1
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_thread_group_matches_single_process(world):
+    """The in-process multi-GPU path behind EwaldSolver(workers=W): W host
+    threads, one SlabEwald each, collectives through a ThreadGroup (barrier +
+    rank-ordered sums), every rank's owned rows written into ONE force
+    array.  Oracle-backed stages on CPU."""
+    import sys
+    import threading
+    sys.path.insert(0, os.path.dirname(__file__))
+    from cpu_stages import OracleStages
+    from oracle import oracle as orc
+    from paper_1708_01135_b200.distributed import SlabEwald, ThreadComm, ThreadGroup
+    cfg = small_config()
+    n = cfg["q"].shape[0]
+    grp = ThreadGroup(world, timeout=120)
+    force = np.zeros((n, 3))
+    out = [None] * world
+
+    def rank(r):
+        st = OracleStages(cfg["L"], cfg["alpha_ref"], cfg["r_cutoff"], cfg["m_int"])
+        sl = SlabEwald(st, torch.device("cpu"), n, comm=ThreadComm(grp, r, "cpu"))
+        pos, q = torch.from_numpy(cfg["pos"]), torch.from_numpy(cfg["q"])
+        mine = torch.nonzero(sl.owned_mask(st.rows(pos).long())).flatten()
+        f_own = torch.zeros((mine.shape[0], 3), dtype=torch.float64)
+        u = sl.evaluate_local(pos[mine].contiguous(), q[mine].contiguous(), f_own)
+        out[r] = (u, mine.numpy(), f_own.numpy())
+
+    ts = [threading.Thread(target=rank, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert all(o is not None for o in out), "a rank failed"
+    for _, idx, fo in out:
+        force[idx] += fo
+    assert sum(o[1].shape[0] for o in out) == n
+    ref = orc.evaluate(cfg["pos"], cfg["q"], cfg["L"], cfg["alpha_ref"],
+                       cfg["r_cutoff"], cfg["m_int"])
+    for u_sr, u_lr, u_self in (o[0] for o in out):
+        assert rel(u_sr, ref["u_sr"]) <= 1e-12
+        assert rel(u_lr, ref["u_lr"]) <= 1e-12
+        assert rel(u_self, ref["u_self"]) <= 1e-13
+    assert np.abs(force - ref["force"]).max() <= 1e-12 * f_rms(ref["force"])
+
+
+def test_thread_group_failure_releases_peers():
+    """A rank that fails before a collective aborts the group: its peers get
+    BrokenBarrierError instead of waiting forever."""
+    import threading
+    from paper_1708_01135_b200.distributed import ThreadComm, ThreadGroup
+    grp = ThreadGroup(2, timeout=60)
+    seen = []
+
+    def ok():
+        try:
+            ThreadComm(grp, 0, "cpu").allreduce_(torch.ones(3))
+        except threading.BrokenBarrierError:
+            seen.append("broken")
+
+    t = threading.Thread(target=ok)
+    t.start()
+    grp.abort()
+    t.join(timeout=30)
+    assert not t.is_alive() and seen == ["broken"]

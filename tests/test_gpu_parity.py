@@ -489,3 +489,45 @@ def test_graph_replay_matches_eager(ew):
     for a, b in zip(results[False], results[True]):
         assert a[:3] == b[:3]
         assert np.array_equal(a[3], b[3]) and np.array_equal(a[4], b[4])
+
+
+def test_reference_error_contract_through_the_facade(ew):
+    """The reference's verify flow (verify.py:52-60, 141-153) with this
+    solver patched in: after set_error_types(<the caller's error namespace>)
+    net charge raises the caller's NeutralityError and a coincident pair its
+    CoincidentParticlesError (ewald.py:212-213).  The GPU box has no
+    reference package, so a stand-in namespace with classes of the same
+    names plays ewaldmd.core (tests/test_host.py checks the real one)."""
+    import types
+    from paper_1708_01135_b200.core import set_error_types
+
+    class RefError(Exception):
+        pass
+    ns = types.SimpleNamespace(
+        EwaldmdError=RefError,
+        NeutralityError=type("NeutralityError", (RefError,), {}),
+        CoincidentParticlesError=type("CoincidentParticlesError", (RefError,), {}))
+
+    def energy_fn(box, params):          # verify._energy_fn
+        solver = ew.EwaldSolver(box, params)
+
+        def evaluate(ps):
+            ps.force[:] = 0.0
+            return solver.evaluate(ps).total
+        return evaluate
+
+    set_error_types(ns)
+    try:
+        charged = ew.create_particle_set(2, ew.SimulationBox(10.0))
+        charged.charge[:] = 1.0
+        charged.position[1, 0] = 2.5
+        with pytest.raises(ns.NeutralityError):
+            energy_fn(charged.box, ew.choose_parameters(2, charged.box, 1e-3))(charged)
+        pos, q = random_neutral(64, 8.0, seed=2)
+        pos[5] = pos[9]
+        box, ps = system(ew, pos, q, 8.0)
+        with pytest.raises(ns.CoincidentParticlesError) as ei:
+            energy_fn(box, ew.EwaldParams(0.5, 3.5, 4.0, 1e-6))(ps)
+        assert isinstance(ei.value, ew.CoincidentParticlesError)
+    finally:
+        set_error_types(None)

@@ -131,3 +131,78 @@ def test_pinned_zeros_falls_back_to_numpy_without_a_device():
     a[:] = 1.5
     assert float(a.sum()) == 1500.0
     assert _lib.pinned_zeros(0).shape == (0,)
+
+
+REF_SRC = "/root/reference/pkg/src"
+
+
+def _reference_core():
+    """ewaldmd.core of the reference (this container only; the GPU box has
+    no /root/reference)."""
+    import importlib
+    import sys
+    if not os.path.isdir(os.path.join(REF_SRC, "ewaldmd")):
+        pytest.skip("reference package not present")
+    if REF_SRC not in sys.path:
+        sys.path.append(REF_SRC)
+    try:
+        return importlib.import_module("ewaldmd.core")
+    except Exception as e:  # numba or another dependency missing
+        pytest.skip(f"reference not importable: {e}")
+
+
+def test_registered_reference_errors_are_raised():
+    """After set_error_types(ewaldmd.core) every error the facade raises is an
+    instance of the reference's class of the same name (so verify.py:141-153's
+    ``except NeutralityError`` catches it) and of this package's own."""
+    import paper_1708_01135_b200 as ew
+    from paper_1708_01135_b200 import _lib
+    from paper_1708_01135_b200.core import set_error_types
+    ref = _reference_core()
+    set_error_types(ref)
+    try:
+        # neutrality: host check with the reference's expression, on the
+        # reference's own ParticleSet
+        ps = ref.create_particle_set(2, ref.SimulationBox(10.0))
+        ps.charge[:] = 1.0
+        with pytest.raises(ref.NeutralityError) as ei:
+            ew.core.require_neutral(ps)
+        assert isinstance(ei.value, ew.NeutralityError)
+        # device statuses (ewald.py:212-213 coincident; celllist.py:84-88)
+        for st, name in ((_lib.EWB_ECOINCIDENT, "CoincidentParticlesError"),
+                         (_lib.EWB_ECUTOFF, "CutoffTooLargeError"),
+                         (_lib.EWB_EKSPACE, "KSpaceEmptyError"),
+                         (_lib.EWB_EBOX, "BoxTooSmallError"),
+                         (_lib.EWB_ESIZE, "OracleSizeError")):
+            with pytest.raises(getattr(ref, name)) as ei:
+                _lib.raise_for(st, "x")
+            assert isinstance(ei.value, getattr(ew, name))
+            assert isinstance(ei.value, ref.EwaldmdError)
+        # host-side parameter errors
+        with pytest.raises(ref.KSpaceEmptyError):
+            ew.enumerate_kvectors(ew.SimulationBox(10.0), ew.EwaldParams(0.5, 4.0, 0.1, 1e-6))
+    finally:
+        set_error_types(None)
+    with pytest.raises(ew.CoincidentParticlesError) as ei:
+        _lib.raise_for(_lib.EWB_ECOINCIDENT, "x")
+    assert not isinstance(ei.value, ref.EwaldmdError)
+
+
+def test_workers_resolution(monkeypatch):
+    """workers = GPU count; capped at the visible GPUs unless
+    ranks may share a device."""
+    import torch
+    from paper_1708_01135_b200 import distributed as d
+    monkeypatch.setattr(torch.cuda, "is_available", lambda: True)
+    monkeypatch.setattr(torch.cuda, "device_count", lambda: 2)
+    monkeypatch.delenv("EWALDB200_WORKERS", raising=False)
+    monkeypatch.delenv("EWALDB200_SHARE_DEVICES", raising=False)
+    assert d._resolve_devices(None) == [0]
+    assert d._resolve_devices(0) == [0, 1]
+    assert d._resolve_devices(8) == [0, 1]
+    monkeypatch.setenv("EWALDB200_SHARE_DEVICES", "1")
+    assert d._resolve_devices(3) == [0, 1, 0]
+    monkeypatch.setenv("EWALDB200_WORKERS", "2")
+    assert d._resolve_devices(None) == [0, 1]
+    with pytest.raises(ValueError):
+        d._resolve_devices(-1)

@@ -13,8 +13,14 @@ r_c=6, cube |n_i|<=18 (25,326 half-space k-vectors).
   timed region, each step is timed with CUDA events on the library's stream
   between barrier+synchronize, and the job time is the max over ranks.
 * e2e: the same metric through the reference-facing API
-  (EwaldSolver.evaluate on a ParticleSet whose arrays live in pinned host
-  memory), host<->device copies inside the timed region.
+  (EwaldSolver.evaluate on a stock ParticleSet: pageable numpy arrays, as
+  the reference allocates them), host<->device copies inside the timed
+  region; the same call on page-locked arrays is reported beside it.
+* dtype: f64 in and out; the reciprocal sums run on the int8 tensor cores as
+  48-bit fixed-point slices; `fp64_pipe` is the same
+  workload with both reciprocal sums on the FP64 pipe.
+* secondary: c3 (262,144 charges, the largest single-GPU config) measured in
+  the same run, device-resident and through the public API.
 * roofline: the stage with the largest share of the step (stage times from
   a separate pass with the two-stream overlap off).  S(k) and the
   reciprocal forces run on the int8 tensor cores (k1t_gemm, k3t_gemm):
@@ -26,9 +32,12 @@ r_c=6, cube |n_i|<=18 (25,326 half-space k-vectors).
 * cpu_baseline: the oracle (C restatement of the reference, OpenMP over all
   host cores) on one full evaluation of the same config, rank 0 at N=1.
 
-N>1 (torchrun): particles are sharded across ranks, S(k) partials are
-combined by one NCCL all-reduce, real space is split by cell z-slabs; the
-total work is fixed (strong scaling).
+N>1 (torchrun): row-slab domain decomposition (distributed.ShardedEwald):
+every rank owns the particles of its rows of cells, receives its halo by
+grouped send/receive, runs the pair kernel over its own rows, computes its
+S(k) partial (one NCCL all-reduce), gathers the reciprocal forces of its own
+particles; forces return by an all-gather of the owned rows.  The total work
+is fixed (strong scaling).
 """
 
 import argparse
@@ -75,6 +84,23 @@ def ncu_traffic(config, kernel):
                                    f"({ent['source']}), bytes per launch")
     return None, None
 
+def ncu_fp64(config, kernel, t, peak):
+    """FP64 flops the kernel EXECUTES per launch (2 DFMA + DMUL + DADD thread
+    instructions, predicated on) from the newest committed capture
+    (profiles/r*/traffic.json, tools/ncu_traffic.py), over time t."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "traffic.json")),
+                       reverse=True):
+        try:
+            ent = json.load(open(path))[config][kernel]
+            fl = 2.0 * ent["dfma"] + ent["dmul"] + ent["dadd"]
+        except (OSError, ValueError, KeyError, TypeError):
+            continue
+        return {"flops_per_launch": fl, "achieved": fl / t / 1e12, "frac": fl / t / 1e12 / peak,
+                "source": os.path.relpath(path, ROOT)}
+    return None
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -83,6 +109,8 @@ def parse():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the c3 line beside the c2 headline")
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--backend", default="nccl",
                     help="torch.distributed backend for N>1 (gloo: functional "
@@ -193,6 +221,14 @@ def workload_desc(cfg):
     }
 
 
+def parallelism_desc(world):
+    return (f"row-slab domain decomposition x{world}: halo exchange, S(k) all-reduce"
+            if world > 1 else "single GPU")
+
+
+DTYPE = "f64 (reciprocal: int8 tcgen05, 48-bit fixed-point emulation)"
+
+
 def cpu_sample_fraction(cfg, budget_s=15.0, threads=16):
     """Fraction of particles whose evaluation takes ~budget_s on the host
     (reciprocal work ~ N*K; ~1e9 pair-steps/s/core for the oracle)."""
@@ -244,8 +280,10 @@ def run_reference(args):
     cfg = wl.make_config(args.config, seed=0)
     threads = args.cpu_threads or orc.host_threads()
     steps = max(1, args.steps)
-    warm = max(0, min(args.warmup, 1))
-    frac = cpu_sample_fraction(cfg, threads=threads)
+    warm = max(3, args.warmup)          # the same warm-up as our arm
+    # each step a bounded sample, so that warm-up + steps end within minutes
+    budget = min(15.0, 150.0 / (steps + warm))
+    frac = cpu_sample_fraction(cfg, budget_s=budget, threads=threads)
     times, frac = cpu_reference(cfg, steps, warm, threads, frac)
     t = float(np.sum(times))
     value = steps / t
@@ -255,7 +293,7 @@ def run_reference(args):
         "steps": steps, "warmup": warm, "ms_per_step": 1e3 * t / steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded, BASELINE.json config)",
-        "config": workload_desc(cfg),
+        "config": dict(workload_desc(cfg), parallelism=parallelism_desc(world)),
         "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads,
                          "kind": "port",
                          "sample": (f"{steps} full evaluation(s) of {args.config}"
@@ -272,6 +310,78 @@ def run_reference(args):
 
 def flush_l2(buf):
     buf.add_(1.0)
+
+
+def e2e_public(ew, cfg, params, rs, l2, args, pinned):
+    """Seconds for args.steps calls of the public EwaldSolver.evaluate on a
+    ParticleSet (host arrays: H2D of positions, charges and forces, D2H of
+    forces and rho inside every call), L2 flushed before each."""
+    import torch
+    n = cfg["pos"].shape[0]
+    ps = ew.create_particle_set(n, cfg["box"])
+    ps.position[:] = cfg["pos"]
+    ps.charge[:] = cfg["q"]
+    if pinned:
+        ps.position = torch.from_numpy(ps.position).pin_memory().numpy()
+        ps.charge = torch.from_numpy(ps.charge).pin_memory().numpy()
+        ps.force = torch.zeros((n, 3), dtype=torch.float64).pin_memory().numpy()
+    solver = ew.EwaldSolver(cfg["box"], params, recip=rs)
+    for _ in range(max(3, args.warmup)):
+        solver.evaluate(ps)
+    t = 0.0
+    for _ in range(args.steps):
+        flush_l2(l2)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        solver.evaluate(ps)
+        t += time.perf_counter() - t0
+    return t
+
+
+def device_evals(h, cfg, dev, l2, steps, warmup):
+    """Seconds for `steps` device-resident evaluations (ewb_dev_evaluate),
+    CUDA events on the handle's stream, L2 flushed before each."""
+    import torch
+    n = cfg["pos"].shape[0]
+    pos_d = torch.from_numpy(cfg["pos"]).to(dev)
+    q_d = torch.from_numpy(cfg["q"]).to(dev)
+    f_d = torch.zeros((n, 3), dtype=torch.float64, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+    h.set_stream(stream.cuda_stream)
+    for _ in range(max(3, warmup)):
+        h.dev_evaluate(pos_d.data_ptr(), q_d.data_ptr(), n, f_d.data_ptr(), None)
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ms = 0.0
+    for _ in range(steps):
+        flush_l2(l2)
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        h.dev_evaluate(pos_d.data_ptr(), q_d.data_ptr(), n, f_d.data_ptr(), None)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        ms += ev0.elapsed_time(ev1)
+    return ms * 1e-3
+
+
+def secondary_config(ew, _lib, wl, name, dev, l2, args):
+    """The largest single-GPU config (c3) beside the headline, so the
+    driver's run also measures it: device-resident and public-API evals/s."""
+    cfg = wl.make_config(name, seed=0)
+    params = ew.EwaldParams(cfg["alpha_ref"], cfg["r_cutoff"], wl.k_cutoff_for(cfg), 1e-6)
+    rs = ew.ReciprocalSpace(cfg["box"], params, cfg["m_int"])
+    h = _lib.Handle(dev.index)
+    h.set_system(cfg["L"], params.alpha, params.r_cutoff)
+    h.set_kspace(rs.m_int, rs.coeff)
+    steps = max(3, min(args.steps, 10))
+    t = device_evals(h, cfg, dev, l2, steps, 3)
+    a = argparse.Namespace(steps=steps, warmup=3)
+    t_page = e2e_public(ew, cfg, params, rs, l2, a, pinned=False)
+    return {"workload": workload_desc(cfg)["workload"], "k_half": int(cfg["m_int"].shape[0]),
+            "steps": steps, "value": steps / t, "unit": "evals/s",
+            "e2e": {"value": steps / t_page, "unit": "evals/s",
+                    "path": "EwaldSolver.evaluate, stock ParticleSet (pageable)"}}
 
 
 def run_ours(args):
@@ -352,13 +462,24 @@ def run_ours(args):
         h.set_overlap(True)
     value = args.steps / total_s
     clocks = clk.summary()
+    fp64_pipe = None
+    if world == 1:
+        # the north_star's literal path: both reciprocal sums on the FP64
+        # pipe (k1_structure_factor, k3_force_gather), same workload
+        h.set_tensor_cores(False)
+        t64 = device_evals(h, cfg, dev, l2, args.steps, args.warmup)
+        h.set_tensor_cores("auto")
+        h.set_stream(stream.cuda_stream)
+        fp64_pipe = {"value": args.steps / t64, "unit": "evals/s",
+                     "note": "ewb_set_tensor_cores(0): S(k) and the force gather on the FP64 "
+                             "pipe (no tensor cores), device-resident, same workload"}
 
     # ---- e2e through the reference-facing API (host buffers) ----
     e2e = None
     if world > 1:
         # sharded public API: every rank copies the pinned host configuration
-        # in, evaluates its shard (S(k) all-reduce, force all-reduce) and
-        # copies the full forces out; max over ranks
+        # in, evaluates its rows (halo exchange, S(k) all-reduce, owned-row
+        # all-gather of the forces) and copies the full forces out; max over ranks
         pos_h = torch.from_numpy(cfg["pos"]).pin_memory()
         q_h = torch.from_numpy(cfg["q"]).pin_memory()
         f_h = torch.zeros((n, 3), dtype=torch.float64).pin_memory()
@@ -384,25 +505,17 @@ def run_ours(args):
                "d2h_bytes_per_step": int(n * 24),
                "path": "distributed.ShardedEwald.evaluate, pinned host arrays, max over ranks"}
     if world == 1:
-        box = cfg["box"]
-        ps = ew.create_particle_set(n, box)
-        ps.position = torch.from_numpy(cfg["pos"]).pin_memory().numpy()
-        ps.charge = torch.from_numpy(cfg["q"]).pin_memory().numpy()
-        ps.force = torch.zeros((n, 3), dtype=torch.float64).pin_memory().numpy()
-        solver = ew.EwaldSolver(box, params, recip=rs)
-        for _ in range(max(3, args.warmup)):
-            solver.evaluate(ps)
-        t_e2e = 0.0
-        for _ in range(args.steps):
-            flush_l2(l2)
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            solver.evaluate(ps)
-            t_e2e += time.perf_counter() - t0
-        e2e = {"value": args.steps / t_e2e, "unit": "evals/s",
+        # the headline: a stock ParticleSet (pageable np.zeros arrays, as the
+        # reference's core.py:111-115 allocates them); pinned arrays beside it
+        t_page = e2e_public(ew, cfg, params, rs, l2, args, pinned=False)
+        t_pin = e2e_public(ew, cfg, params, rs, l2, args, pinned=True)
+        e2e = {"value": args.steps / t_page, "unit": "evals/s",
                "h2d_bytes_per_step": int(n * (24 + 8 + 24)),
                "d2h_bytes_per_step": int(n * 24 + 16 * K + 3 * 8 + 4),
-               "path": "EwaldSolver.evaluate (ctypes -> ewb_evaluate), pinned host arrays"}
+               "path": "EwaldSolver.evaluate (ctypes -> ewb_evaluate) on a stock ParticleSet "
+                       "(pageable numpy arrays)",
+               "pinned": {"value": args.steps / t_pin, "unit": "evals/s",
+                          "path": "the same call with the ParticleSet arrays in page-locked memory"}}
 
     # ---- roofline of the dominant kernel (single GPU stage times) ----
     roof = None
@@ -410,6 +523,7 @@ def run_ours(args):
     if world == 1 and args.steps > 0:
         mean = stage / args.steps
         t_real, t_k1, t_k3 = mean[1], mean[2], mean[3]
+        t_pair = mean[1] - mean[0]      # t_sr without the cell build: k6 + its energy sum
         tci = h.tc_info()
         rs_pairs = h.last_pair_count()  # unordered in-cutoff pairs (half shell)
         np64 = ((n + 63) // 64) * 64
@@ -433,13 +547,16 @@ def run_ours(args):
                 "note": f"forces: executed int8 MMA ops ({tci['k3_pairs_per_kstep']} slice pairs of six 8-bit "
                         "slices, 2 per MAC) over the alg2 stage time (k3t_wmax + k3t_wprep + k3t_gemm + k3_combine)"},
             "k6_real_space": {
-                "stage_ms": 1e3 * t_real, "bound": "fp64", "unit": "TFLOP/s",
-                "pairs": rs_pairs,
-                "achieved": rs_pairs * FLOPS_PAIR_RS / t_real / 1e12, "peak": fp64_peak,
-                "frac": rs_pairs * FLOPS_PAIR_RS / t_real / 1e12 / fp64_peak,
-                "pair_evals_per_s": rs_pairs / t_real,
+                "stage_ms": 1e3 * t_real, "kernel_ms": 1e3 * t_pair, "bound": "fp64",
+                "unit": "TFLOP/s", "pairs": rs_pairs,
+                "achieved": rs_pairs * FLOPS_PAIR_RS / t_pair / 1e12, "peak": fp64_peak,
+                "frac": rs_pairs * FLOPS_PAIR_RS / t_pair / 1e12 / fp64_peak,
+                "pair_evals_per_s": rs_pairs / t_pair,
+                "executed": ncu_fp64(args.config, "k6_real_space", t_pair, fp64_peak),
                 "note": f"in-cutoff pairs x {FLOPS_PAIR_RS:.0f} FP64 flops per pair evaluation "
-                        "(erfc+exp+rsqrt, both forces); stage t_sr incl. binning"},
+                        "(the reference's erfc/exp/force formulation) over the pair-kernel time "
+                        "(t_sr - t_cell: k6 and its energy sum, binning excluded); 'executed': "
+                        "ncu DFMA/DMUL/DADD counts of the committed capture over the same time"},
         }
         dom = max(kern, key=lambda k: kern[k]["stage_ms"])
         d = kern[dom]
@@ -464,6 +581,10 @@ def run_ours(args):
                          "t_alg1": 1e3 * t_k1, "t_alg2": 1e3 * t_k3},
         }
 
+    secondary = None
+    if world == 1 and args.config == "c2" and not args.no_secondary:
+        secondary = {"c3": secondary_config(ew, _lib, wl, "c3", dev, l2, args)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import oracle as orc
@@ -483,11 +604,10 @@ def run_ours(args):
             "unit": "evals/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": 1e3 * total_s / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic (seeded, BASELINE.json config)",
-            "config": dict(workload_desc(cfg),
-                           parallelism=f"particle-shard x{world} + S(k) allreduce"
-                           if world > 1 else "single GPU"),
-            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
+            "dtype": DTYPE, "data": "synthetic (seeded, BASELINE.json config)",
+            "config": dict(workload_desc(cfg), parallelism=parallelism_desc(world)),
+            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "fp64_pipe": fp64_pipe,
+            "secondary": secondary,
             "gpu_launches": int(launches), "clocks": clocks,
             "energies": [float(x) for x in en],
             "fp64_peak_tflops_measured": fp64_peak,

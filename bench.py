@@ -13,9 +13,10 @@ r_c=6, cube |n_i|<=18 (25,326 half-space k-vectors).
   timed region, each step is timed with CUDA events on the library's stream
   between barrier+synchronize, and the job time is the max over ranks.
 * e2e: the same metric through the reference-facing API
-  (EwaldSolver.evaluate on a stock ParticleSet: pageable numpy arrays, as
-  the reference allocates them), host<->device copies inside the timed
-  region; the same call on page-locked arrays is reported beside it.
+  (EwaldSolver.evaluate on a stock ParticleSet: numpy arrays as the
+  reference allocates them, which the facade page-locks in place from their
+  second evaluation), host<->device copies inside the timed region; the same
+  call on arrays allocated page-locked is reported beside it.
 * dtype: f64 in and out; the reciprocal sums run on the int8 tensor cores as
   48-bit fixed-point slices; `fp64_pipe` is the same
   workload with both reciprocal sums on the FP64 pipe.
@@ -513,7 +514,8 @@ def run_ours(args):
                "h2d_bytes_per_step": int(n * (24 + 8 + 24)),
                "d2h_bytes_per_step": int(n * 24 + 16 * K + 3 * 8 + 4),
                "path": "EwaldSolver.evaluate (ctypes -> ewb_evaluate) on a stock ParticleSet "
-                       "(pageable numpy arrays)",
+                       "(numpy arrays as the reference allocates them; the facade page-locks them "
+                       "in place from their second evaluation, _lib.HostPins)",
                "pinned": {"value": args.steps / t_pin, "unit": "evals/s",
                           "path": "the same call with the ParticleSet arrays in page-locked memory"}}
 

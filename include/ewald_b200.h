@@ -242,6 +242,14 @@ int64_t ewb_launch_count(const ewb_handle *h);
  * ReciprocalSpace.rho): device-to-host copies land directly. */
 int ewb_host_alloc(size_t bytes, void **out);
 int ewb_host_free(void *p);
+/* Page-lock / release a caller-owned host range in place (cudaHostRegister):
+ * the facade pins a ParticleSet's arrays on their second evaluation so the
+ * copies of EwaldSolver.evaluate (reference ewald.py:629-655, pageable numpy
+ * arrays allocated at core.py:111-115) run as asynchronous DMA.  Returns 1
+ * if the range was registered already.  The caller unregisters before the
+ * memory is freed. */
+int ewb_host_register(void *p, size_t bytes);
+int ewb_host_unregister(void *p);
 
 /* ---- harness helper (csrc/workloads.c, separate library) ----
  * int ewb_gen_hardcore_gas(int64_t n, double L, double min_sep,

@@ -92,6 +92,8 @@ SIGNATURES = {
     "ewb_launch_count": (_I64, [_P]),
     "ewb_host_alloc": (_INT, [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
     "ewb_host_free": (_INT, [_P]),
+    "ewb_host_register": (_INT, [_P, ctypes.c_size_t]),
+    "ewb_host_unregister": (_INT, [_P]),
 }
 
 _LIB = None
@@ -132,6 +134,58 @@ def pinned_zeros(n):
     arr[:] = 0.0
     weakref.finalize(arr, lib.ewb_host_free, ctypes.c_void_p(ptr.value))
     return arr
+
+
+class HostPins:
+    """Caller host arrays page-locked in place while they live.
+
+    A reference ``ParticleSet`` allocates pageable numpy arrays
+    (core.py:111-115) and an MD loop hands the same arrays to every
+    evaluation; copies from pageable memory are staged by the driver and
+    block the host.  An array that owns its memory, is at least MIN_BYTES
+    and C-contiguous is registered (cudaHostRegister) the second time it is
+    seen; a finalizer unregisters it before numpy frees the memory (weakref
+    callbacks run at the start of the array's deallocation).  Arrays that
+    do not own their memory (views, ctypes / torch pinned buffers) are left
+    alone."""
+
+    MIN_BYTES = 1 << 18
+    MAX_ENTRIES = 64
+
+    def __init__(self):
+        self._seen = {}    # (ptr, nbytes) -> weakref to the owning array
+        self._pinned = set()
+
+    def touch(self, a):
+        import weakref
+        if not (isinstance(a, np.ndarray) and a.base is None and a.flags.owndata
+                and a.flags.c_contiguous and a.nbytes >= self.MIN_BYTES):
+            return
+        key = (a.ctypes.data, a.nbytes)
+        if key in self._pinned:
+            return
+        ref = self._seen.get(key)
+        if ref is None or ref() is not a:
+            if len(self._seen) >= self.MAX_ENTRIES:
+                self._seen = {k: r for k, r in self._seen.items() if r() is not None}
+                if len(self._seen) >= self.MAX_ENTRIES:
+                    return
+            self._seen[key] = weakref.ref(a)
+            return
+        lib = load_library()
+        if lib.ewb_host_register(ctypes.c_void_p(key[0]), key[1]) != EWB_OK:
+            return
+        self._pinned.add(key)
+        del self._seen[key]
+        weakref.finalize(a, HostPins._release, self, key)
+
+    @staticmethod
+    def _release(pins, key):
+        pins._pinned.discard(key)
+        load_library().ewb_host_unregister(ctypes.c_void_p(key[0]))
+
+
+PINS = HostPins()
 
 
 class DeviceError(RuntimeError):

@@ -2630,6 +2630,32 @@ int ewb_host_free(void *p) {
   return EWB_OK;
 }
 
+// page-lock a caller's host range in place (cudaHostRegister), so the
+// evaluation's copies of it run as asynchronous DMA; the caller unregisters
+// it before the memory is freed.  1: already registered (not an error).
+int ewb_host_register(void *p, size_t bytes) {
+  if (!p || !bytes) return EWB_EINVAL;
+  const cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterPortable);
+  if (e == cudaErrorHostMemoryAlreadyRegistered) {
+    cudaGetLastError();
+    return 1;
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return EWB_ECUDA;
+  }
+  return EWB_OK;
+}
+
+int ewb_host_unregister(void *p) {
+  if (!p) return EWB_EINVAL;
+  if (cudaHostUnregister(p) != cudaSuccess) {
+    cudaGetLastError();
+    return EWB_ECUDA;
+  }
+  return EWB_OK;
+}
+
 int64_t ewb_launch_count(const ewb_handle *h) { return h ? h->launches : -1; }
 
 }  // extern "C"

@@ -200,6 +200,8 @@ def _handle_for(rs, box=None, params=None):
 def _particles(ps):
     pos = _lib.f64c(ps.position, (ps.count, 3))
     q = _lib.f64c(ps.charge, (ps.count,))
+    _lib.PINS.touch(pos)
+    _lib.PINS.touch(q)
     return pos, q
 
 
@@ -207,6 +209,7 @@ def _force_buffer(ps):
     f = ps.force
     if (isinstance(f, np.ndarray) and f.dtype == np.float64
             and f.flags.c_contiguous and f.shape == (ps.count, 3)):
+        _lib.PINS.touch(f)
         return f, False
     return np.ascontiguousarray(f, dtype=np.float64).reshape(ps.count, 3), True
 

@@ -531,3 +531,31 @@ def test_reference_error_contract_through_the_facade(ew):
         assert isinstance(ei.value, ew.CoincidentParticlesError)
     finally:
         set_error_types(None)
+
+
+def test_pageable_arrays_pinned_in_place_and_released(ew):
+    """A stock ParticleSet's numpy arrays are page-locked in place on their
+    second evaluation (_lib.HostPins) and released when they are freed;
+    results are identical on every call."""
+    import gc
+    from paper_1708_01135_b200 import _lib
+    from paper_1708_01135_b200 import workloads as wl
+    cfg = wl.make_config("c2", seed=0)
+    box, ps = system(ew, cfg["pos"], cfg["q"], cfg["L"])
+    params = ew.EwaldParams(cfg["alpha_ref"], cfg["r_cutoff"], wl.k_cutoff_for(cfg), 1e-6)
+    solver = ew.EwaldSolver(box, params, recip=ew.ReciprocalSpace(box, params, cfg["m_int"]))
+    before = set(_lib.PINS._pinned)
+    out = []
+    for _ in range(3):
+        ps.force[:] = 0.0
+        res = solver.evaluate(ps)
+        out.append((res.total, ps.force.copy()))
+    pinned = set(_lib.PINS._pinned) - before
+    assert {k[0] for k in pinned} >= {ps.position.ctypes.data, ps.charge.ctypes.data,
+                                       ps.force.ctypes.data}
+    for tot, f in out[1:]:
+        assert tot == out[0][0]
+        assert np.array_equal(f, out[0][1])
+    del ps, out
+    gc.collect()
+    assert not (set(_lib.PINS._pinned) & pinned)

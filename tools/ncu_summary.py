@@ -18,7 +18,31 @@ KEYS = [
     ("launch__registers_per_thread", "registers/thread"),
     ("launch__grid_size", "grid"),
     ("sm__cycles_elapsed.avg.per_second", "SM clock"),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe % (active)"),
+    ("sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active",
+     "tensor pipe IMMA % (active)"),
+    ("sm__inst_executed_pipe_tensor_subpipe_imma.sum", "IMMA/UTCIMMA warp instr"),
+    ("sm__sass_thread_inst_executed_op_dfma_pred_on.sum", "DFMA thread instr"),
+    ("sm__sass_thread_inst_executed_op_dmul_pred_on.sum", "DMUL thread instr"),
+    ("sm__sass_thread_inst_executed_op_dadd_pred_on.sum", "DADD thread instr"),
 ]
+# extra counters the profiling runs add to --set full (tools/refresh_profiles.sh)
+EXTRA_METRICS = ",".join(k for k, _ in KEYS[-6:])
+UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+TUNIT = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0}
+
+
+def _num(r, hdr, units, key, scale=None):
+    if key not in hdr:
+        return None
+    i = hdr.index(key)
+    try:
+        v = float(r[i].replace(",", ""))
+    except ValueError:
+        return None
+    if scale is not None:
+        v *= scale.get(units[i], 1.0)
+    return v
 
 
 def full_report(path):
@@ -35,6 +59,17 @@ def full_report(path):
             if k in hdr:
                 i = hdr.index(k)
                 lines.append(f"- {lab}: {r[i]} {units[i]}")
+        # derived: achieved FP64 FLOP/s (2 per DFMA) and DRAM GB/s
+        t = _num(r, hdr, units, "gpu__time_duration.sum", TUNIT)
+        fma_, mul_, add_ = (_num(r, hdr, units, f"sm__sass_thread_inst_executed_op_{o}_pred_on.sum")
+                            for o in ("dfma", "dmul", "dadd"))
+        if t and fma_ is not None and mul_ is not None and add_ is not None:
+            fl = 2.0 * fma_ + mul_ + add_
+            lines.append(f"- FP64 flops executed: {fl:.4g} -> {fl / t / 1e12:.3f} TFLOP/s")
+        rb = _num(r, hdr, units, "dram__bytes_read.sum", UNIT)
+        wb = _num(r, hdr, units, "dram__bytes_write.sum", UNIT)
+        if t and rb is not None and wb is not None:
+            lines.append(f"- DRAM read+write: {(rb + wb) / t / 1e9:.1f} GB/s")
         st = []
         for i, h in enumerate(hdr):
             if h.startswith("smsp__average_warps_issue_stalled") and h.endswith("per_issue_active.ratio"):

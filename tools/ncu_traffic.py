@@ -24,7 +24,7 @@ def main(rep, config, out):
     ki = hdr.index("Kernel Name")
     ir, iw = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
     it = hdr.index("gpu__time_duration.sum")
-    acc = defaultdict(lambda: [0.0, 0.0, 0])
+    acc = defaultdict(lambda: [0.0, 0.0, 0, 0.0, 0.0, 0.0])
     for r in data:
         name = r[ki].replace("<unnamed>::", "").replace("(anonymous namespace)::", "")
         name = name.replace("void ", "").split("(")[0].split("<")[0].strip()
@@ -34,8 +34,16 @@ def main(rep, config, out):
         a[0] += b
         a[1] += t
         a[2] += 1
+        for k, op in enumerate(("dfma", "dmul", "dadd")):
+            key = f"sm__sass_thread_inst_executed_op_{op}_pred_on.sum"
+            if key in hdr:
+                try:
+                    a[3 + k] += float(r[hdr.index(key)].replace(",", ""))
+                except ValueError:
+                    pass
     res = json.load(open(out)) if os.path.exists(out) else {}
     res[config] = {k: {"dram_bytes": v[0] / v[2], "duration_ns": v[1] / v[2], "launches": v[2],
+                       "dfma": v[3] / v[2], "dmul": v[4] / v[2], "dadd": v[5] / v[2],
                        "source": os.path.basename(rep)}
                    for k, v in acc.items()}
     json.dump(res, open(out, "w"), indent=1, sort_keys=True)

@@ -94,6 +94,18 @@ int ewb_set_overlap(ewb_handle *h, int on);
  * evaluate with unchanged shapes/pointers/configuration is captured, later
  * ones replay the graph.  0 runs every kernel eagerly. */
 int ewb_set_graphs(ewb_handle *h, int on);
+/* Verlet pair lists with a skin (the reference rebuilds its cell list every
+ * step, SPEC.md:179 and driver.py:119-124, 227-245): with skin > 0 the
+ * real-space pass bins and builds per-unit pair lists at r_c + skin and
+ * later evaluations reuse them (exact r < r_c predicates per pair) while no
+ * particle has moved skin/2 since the build.  ewb_dev_verlet_check (one
+ * small kernel + synchronisation) decides for the NEXT evaluation of d_pos:
+ * *rebuild = 0 arms one reuse.  ewb_verlet_info: {builds, reuses}.  skin 0
+ * (default) rebuilds every evaluation. */
+int ewb_set_skin(ewb_handle *h, double skin);
+int ewb_dev_verlet_check(ewb_handle *h, const double *d_pos, int64_t n, int *rebuild);
+int ewb_verlet_info(const ewb_handle *h, int64_t *out2);
+
 /* 0 (default): real space visits each unordered pair once and scatters
  * the partner's force with fp64 atomics (fastest; summation order varies
  * run to run at the 1e-16 level).  1: ordered pairs, write-to-centre only

@@ -92,6 +92,9 @@ SIGNATURES = {
     "ewb_launch_count": (_I64, [_P]),
     "ewb_host_alloc": (_INT, [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
     "ewb_host_free": (_INT, [_P]),
+    "ewb_set_skin": (_INT, [_P, _D]),
+    "ewb_dev_verlet_check": (_INT, [_P, _P, _I64, ctypes.POINTER(_INT)]),
+    "ewb_verlet_info": (_INT, [_P, _P]),
     "ewb_host_register": (_INT, [_P, ctypes.c_size_t]),
     "ewb_host_unregister": (_INT, [_P]),
 }
@@ -303,6 +306,22 @@ class Handle:
         """1/True: two-pass real space (default), 0/False: fused kernel,
         2: two-pass with a tiny list capacity (tests the overflow pass)."""
         self._check(self.lib.ewb_set_real_space_split(self.h, int(mode)))
+
+    def set_skin(self, skin):
+        """Verlet pair lists built at r_c + skin, reused while every particle
+        stays within skin/2 of its build position (0: rebuild every call)."""
+        self._check(self.lib.ewb_set_skin(self.h, float(skin)))
+
+    def dev_verlet_check(self, d_pos, n):
+        """True if the next evaluation of d_pos must rebuild the lists."""
+        r = _INT(1)
+        self._check(self.lib.ewb_dev_verlet_check(self.h, _P(d_pos), int(n), ctypes.byref(r)))
+        return bool(r.value)
+
+    def verlet_info(self):
+        out = np.zeros(2, dtype=np.int64)
+        self._check(self.lib.ewb_verlet_info(self.h, out.ctypes.data))
+        return {"builds": int(out[0]), "reuses": int(out[1])}
 
     def set_stencil(self, rad):
         self._check(self.lib.ewb_set_stencil(self.h, int(rad)))

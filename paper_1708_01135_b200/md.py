@@ -266,6 +266,7 @@ class RunMetrics:
     })
     energy_trace: list = field(default_factory=list)
     max_step_displacement: float = 0.0
+    verlet: dict = field(default_factory=lambda: {"builds": 0, "reuses": 0})
     alpha: float = 0.0
     r_cutoff: float = 0.0
     n_k: int = 0
@@ -308,10 +309,11 @@ class DeviceMD:
     back.
     """
 
-    def __init__(self, ps, config):
+    def __init__(self, ps, config, skin=0.0):
         import torch
 
         self.config = config
+        self.skin = float(skin)
         self.box = ps.box
         self.n = ps.count
         self.assembler = ForceAssembler(ps, config)
@@ -322,6 +324,10 @@ class DeviceMD:
         self.dev = torch.device("cuda", h.device)
         self.stream = torch.cuda.Stream(device=self.dev)
         h.set_stream(self.stream.cuda_stream)
+        # Verlet pair lists (skin > 0): the real-space lists are rebuilt only
+        # when a particle has moved skin/2 since the last build; the
+        # reference rebuilds its cell lists every step
+        h.set_skin(self.skin)
         f64 = dict(dtype=torch.float64, device=self.dev)
         with torch.cuda.stream(self.stream):
             self.pos = torch.from_numpy(np.ascontiguousarray(ps.position)).to(**f64)
@@ -350,6 +356,8 @@ class DeviceMD:
             # as uploaded, so accept/reject is identical
             require_neutral(self._q_host)
             self._neutral_checked = True
+        if self.skin > 0.0:
+            self.h.dev_verlet_check(self.pos.data_ptr(), self.n)
         en, tm = self.h.dev_evaluate(self.pos.data_ptr(), self.q.data_ptr(), self.n,
                                      self.force.data_ptr(), None, timings=True)
         u_lj = float(self.h.last_energies()[3]) if self.config.lj_on else 0.0
@@ -404,14 +412,15 @@ class DeviceMD:
         ps.force[:] = self.force.cpu().numpy()
 
 
-def run(config, ps=None):
-    """NVE dynamics with the state resident on the device (driver.py:204-246)."""
+def run(config, ps=None, skin=0.0):
+    """NVE dynamics with the state resident on the device (driver.py:204-246);
+    skin > 0 reuses Verlet pair lists across steps (DeviceMD)."""
     if ps is None:
         cells = rocksalt_cells_for(config.n_particles)
         spacing = config.box_edge / (2 * cells)
         ps = init_rocksalt(cells, spacing)
     initial_velocities(ps, config.velocity_scale, config.seed)
-    md = DeviceMD(ps, config)
+    md = DeviceMD(ps, config, skin=skin)
     metrics = RunMetrics(n_steps=config.n_steps)
     if md.assembler.params is not None:
         metrics.alpha = md.assembler.params.alpha
@@ -435,4 +444,5 @@ def run(config, ps=None):
         metrics.max_step_displacement = max(metrics.max_step_displacement,
                                             md.max_displacement())
     md.download(ps)
+    metrics.verlet = md.h.verlet_info() if md.skin > 0.0 else {"builds": 0, "reuses": 0}
     return metrics

@@ -553,9 +553,11 @@ def test_pageable_arrays_pinned_in_place_and_released(ew):
     pinned = set(_lib.PINS._pinned) - before
     assert {k[0] for k in pinned} >= {ps.position.ctypes.data, ps.charge.ctypes.data,
                                        ps.force.ctypes.data}
+    # the half shell scatters partner forces with fp64 atomics: summation
+    # order (not the set of terms) varies from call to call
     for tot, f in out[1:]:
-        assert tot == out[0][0]
-        assert np.array_equal(f, out[0][1])
+        assert rel(tot, out[0][0]) <= 1e-13
+        assert np.abs(f - out[0][1]).max() <= 1e-13 * f_rms(out[0][1])
     del ps, out
     gc.collect()
     assert not (set(_lib.PINS._pinned) & pinned)

@@ -28,8 +28,10 @@ KEYS = [
 ]
 # extra counters the profiling runs add to --set full (tools/refresh_profiles.sh)
 EXTRA_METRICS = ",".join(k for k, _ in KEYS[-6:])
-UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-TUNIT = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0}
+UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1.0, "KB": 1e3, "MB": 1e6,
+        "GB": 1e9}
+TUNIT = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0, "ns": 1e-9,
+         "us": 1e-6, "ms": 1e-3, "s": 1.0}
 
 
 def _num(r, hdr, units, key, scale=None):
@@ -41,7 +43,9 @@ def _num(r, hdr, units, key, scale=None):
     except ValueError:
         return None
     if scale is not None:
-        v *= scale.get(units[i], 1.0)
+        if units[i] not in scale:
+            return None
+        v *= scale[units[i]]
     return v
 
 
@@ -105,6 +109,40 @@ def launch_list(path, skip_prefix=None):
     return "\n".join(lines)
 
 
+def rederive(md_path):
+    """Recompute the derived lines (FP64 TFLOP/s, DRAM GB/s) of a summary
+    written by full_report from its raw lines (duration, DFMA/DMUL/DADD
+    thread instructions, DRAM bytes)."""
+    out, cur = [], {}
+    for line in open(md_path).read().split("\n"):
+        if line.startswith("### "):
+            cur = {}
+        if line.startswith("- FP64 flops executed") or line.startswith("- DRAM read+write"):
+            continue
+        out.append(line)
+        if not line.startswith("- ") or ":" not in line:
+            continue
+        lab, val = line[2:].split(":", 1)
+        parts = val.split()
+        if not parts:
+            continue
+        try:
+            v = float(parts[0])
+        except ValueError:
+            continue
+        u = parts[1] if len(parts) > 1 else ""
+        cur[lab] = v * TUNIT.get(u, UNIT.get(u, 1.0)) if lab in ("duration", "dram read", "dram write") else v
+        if lab == "DADD thread instr" and "duration" in cur:
+            fl = 2.0 * cur.get("DFMA thread instr", 0.0) + cur.get("DMUL thread instr", 0.0) + v
+            out.append(f"- FP64 flops executed: {fl:.4g} -> {fl / cur['duration'] / 1e12:.3f} TFLOP/s")
+            if "dram read" in cur and "dram write" in cur:
+                out.append(f"- DRAM read+write: {(cur['dram read'] + cur['dram write']) / cur['duration'] / 1e9:.1f} GB/s")
+    return "\n".join(out)
+
+
 if __name__ == "__main__":
     kind, path = sys.argv[1], sys.argv[2]
-    print(full_report(path) if kind == "full" else launch_list(path))
+    if kind == "rederive":
+        print(rederive(path))
+    else:
+        print(full_report(path) if kind == "full" else launch_list(path))

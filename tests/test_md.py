@@ -139,7 +139,7 @@ def test_run_zero_steps_and_determinism(md):
         assert abs(a - b) <= 1e-10 * abs(a)
 
 
-@pytest.mark.parametrize("skin,expect_reuse", [(0.6, True), (0.004, None)])
+@pytest.mark.parametrize("skin,expect_reuse", [(0.6, True), (0.05, None)])
 def test_device_md_verlet_lists_match_rebuild_every_step(md, skin, expect_reuse):
     """DeviceMD with Verlet pair lists (built at r_c + skin, reused while no
     particle has moved skin/2) against rebuild-every-step (the reference's
@@ -147,8 +147,8 @@ def test_device_md_verlet_lists_match_rebuild_every_step(md, skin, expect_reuse)
     32^3 rock salt (stencil cell grid, so the lists are active).  A small skin
     forces rebuilds during the run."""
     import torch  # noqa: F401
-    cfg = md.SimConfig(n_particles=32768, box_edge=32.0, tolerance=1e-6, alpha=0.284089,
-                       r_cutoff=6.0, dt=0.005, n_steps=12, velocity_scale=0.5, seed=3,
+    cfg = md.SimConfig(n_particles=32768, box_edge=32.0, tolerance=1e-6, r_cutoff=6.0,
+                       dt=0.005, n_steps=12, velocity_scale=0.5, seed=3,
                        lj_on=True, lj=md.LJParams(0.05, 0.8, 2.0))
     runs = {}
     for s in (0.0, skin):

@@ -1,6 +1,6 @@
 """DeviceMD step time with Verlet pair lists (skin > 0) against rebuilding
 every step (skin 0, the reference's rule): rock salt side^3 at unit spacing,
-beta 0.533, r_c 6 (the c2/c3 parameters), Coulomb + LJ, velocity scale 0.5.
+r_c 6 (alpha from choose_parameters at 1e-6), Coulomb + LJ, velocity scale 0.5.
 usage: python tools/md_verlet_time.py SIDE [SKIN ...]"""
 import sys
 
@@ -13,7 +13,7 @@ side = int(sys.argv[1]) if len(sys.argv) > 1 else 32
 skins = [float(x) for x in sys.argv[2:]] or [0.0, 0.3, 0.6]
 for skin in skins:
     cfg = md.SimConfig(n_particles=side ** 3, box_edge=float(side), tolerance=1e-6,
-                       alpha=0.284089, r_cutoff=6.0, dt=0.005, n_steps=30, velocity_scale=0.5,
+                       r_cutoff=6.0, dt=0.005, n_steps=30, velocity_scale=0.5,
                        seed=3, lj_on=True, lj=md.LJParams(0.05, 0.8, 2.0))
     cells = md.rocksalt_cells_for(cfg.n_particles)
     ps = md.init_rocksalt(cells, cfg.box_edge / (2 * cells))

@@ -303,8 +303,10 @@ class Handle:
         self.deterministic = bool(on)
 
     def set_real_space_split(self, mode):
-        """1/True: two-pass real space (default), 0/False: fused kernel,
-        2: two-pass with a tiny list capacity (tests the overflow pass)."""
+        """0/False: the fused traversal + evaluation kernel (default);
+        1/True: two passes -- per-unit pair lists in HBM, then their
+        evaluation (the machinery of the Verlet lists, ewb_set_skin);
+        2: two passes with a tiny list capacity (tests the overflow pass)."""
         self._check(self.lib.ewb_set_real_space_split(self.h, int(mode)))
 
     def set_skin(self, skin):

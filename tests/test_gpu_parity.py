@@ -578,7 +578,10 @@ def test_c5_large_sample_vs_oracle(ew, orc):
     K = rs.n_stored
     ks = np.sort(rng.choice(K, size=8192, replace=False))
     rho_s = orc.rho_hat(cfg["pos"], cfg["q"], cfg["L"], cfg["m_int"][ks])
-    rmax = np.abs(g["rho_re_sample"]).max()
+    # the reference's bound is relative to max|rho| over ALL k (test_ewald.py:
+    # 184-190); the jittered lattice's Bragg peak (n = (50, 50, 50), |rho| ~
+    # 0.86 N) sets it, the 512 golden samples miss it
+    rmax = max(np.abs(rs.rho.values).max(), np.abs(rho_s).max())
     assert np.abs(rs.rho.values[ks] - rho_s[:8192]).max() <= RHO_TOL * rmax
     assert np.abs(rs.rho.values[K + ks] - rho_s[8192:]).max() <= RHO_TOL * rmax
     sel = np.sort(rng.choice(cfg["pos"].shape[0], size=8192, replace=False))

@@ -649,6 +649,25 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
     CK(cudaMemsetAsync(h->fsorted.p, 0, (size_t)n * 3 * sizeof(double), h->stream));
     facc = h->fsorted.as<double>();
   }
+  // persistent pair-kernel grids (K6_PERSIST): at most one resident wave,
+  // warps fetch further units from a counter; energy slots are summed over
+  // the launched warps only
+  CK(h->k6work.ensure(2 * sizeof(int)));
+  if (K6_PERSIST) CK(cudaMemsetAsync(h->k6work.p, 0, 2 * sizeof(int), h->stream));
+  int *work0 = K6_PERSIST ? h->k6work.as<int>() : nullptr;
+  int *work1 = K6_PERSIST ? h->k6work.as<int>() + 1 : nullptr;
+  auto grid_for = [&](const void *kern) -> unsigned {
+    if (!K6_PERSIST) return nb;
+    int &occ = h->k6_occ[kern];  // cached: the query stays out of graph captures
+    if (occ < 1 &&
+        (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, K6_WARPS * 32, 0) != cudaSuccess ||
+         occ < 1)) {
+      cudaGetLastError();
+      occ = 1;
+    }
+    return (unsigned)std::min<int64_t>(nb, (int64_t)occ * h->n_sm);
+  };
+  int64_t n_esum = n_eslot_all;
   {
     K6Lists lists{split ? h->rs_list.as<uint32_t>() : nullptr,
                   split ? h->rs_count.as<int>() : nullptr, cap};
@@ -665,11 +684,13 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
                                          : k6_real_space<true, false, K6_MODE_FUSED>)
                               : (rp.half ? k6_real_space<false, true, K6_MODE_FUSED>
                                          : k6_real_space<false, false, K6_MODE_FUSED>));
-      kern<<<nb, K6_WARPS * 32, 0, h->stream>>>(
+      const unsigned nbk = grid_for((const void *)kern);
+      n_esum = (int64_t)nbk * K6_WARPS;
+      kern<<<nbk, K6_WARPS * 32, 0, h->stream>>>(
           h->sorted.as<double4>(), h->sorted_f.as<float4>(), h->sorted_cell.as<int>(),
           h->order.as<int>(), h->start.as<int>(), h->row_ustart.as<int>(), rp,
           facc, eb, eb_lj, h->errflag.as<int>(),
-          h->pairc.as<unsigned long long>(), lists);
+          h->pairc.as<unsigned long long>(), lists, work0);
       CKL();
     } else {
       // pass 1: traversal -> per-unit pair lists (the LJ switch only
@@ -678,11 +699,11 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
       if (!reuse) {
         auto trav = rp.half ? k6_real_space<false, true, K6_MODE_LIST>
                             : k6_real_space<false, false, K6_MODE_LIST>;
-        trav<<<nb, K6_WARPS * 32, 0, h->stream>>>(
+        trav<<<grid_for((const void *)trav), K6_WARPS * 32, 0, h->stream>>>(
             h->sorted.as<double4>(), h->sorted_f.as<float4>(), h->sorted_cell.as<int>(),
             h->order.as<int>(), h->start.as<int>(), h->row_ustart.as<int>(), rp,
             facc, nullptr, nullptr, h->errflag.as<int>(),
-            h->pairc.as<unsigned long long>(), lists);
+            h->pairc.as<unsigned long long>(), lists, work0);
         CKL();
       }
       if (verlet) {
@@ -709,11 +730,13 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
                                   : k6_real_space<true, false, K6_MODE_OVF>)
                        : (rp.half ? k6_real_space<false, true, K6_MODE_OVF>
                                   : k6_real_space<false, false, K6_MODE_OVF>);
-      ovf<<<nb, K6_WARPS * 32, 0, h->stream>>>(
+      const unsigned nbo = grid_for((const void *)ovf);
+      n_esum = n_eslots + (int64_t)nbo * K6_WARPS;
+      ovf<<<nbo, K6_WARPS * 32, 0, h->stream>>>(
           h->sorted.as<double4>(), h->sorted_f.as<float4>(), h->sorted_cell.as<int>(),
           h->order.as<int>(), h->start.as<int>(), h->row_ustart.as<int>(), rp,
           facc, eb + n_eslots, eb_lj ? eb_lj + n_eslots : nullptr,
-          h->errflag.as<int>(), nullptr, lists);
+          h->errflag.as<int>(), nullptr, lists, work1);
       CKL();
     }
   }
@@ -724,11 +747,11 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
     CKL();
   }
   if (pair_coul) {
-    k_sum<<<1, 1024, 0, h->stream>>>(h->eblk.as<double>(), n_eslot_all, 1.0, d_u_out);
+    k_sum<<<1, 1024, 0, h->stream>>>(h->eblk.as<double>(), n_esum, 1.0, d_u_out);
     CKL();
   }
   if (lj_on && d_ulj_out) {
-    k_sum<<<1, 1024, 0, h->stream>>>(h->eblk_lj.as<double>(), n_eslot_all, 1.0, d_ulj_out);
+    k_sum<<<1, 1024, 0, h->stream>>>(h->eblk_lj.as<double>(), n_esum, 1.0, d_ulj_out);
     CKL();
   }
   return EWB_OK;

@@ -615,7 +615,9 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
   }
   const unsigned nb = (unsigned)std::max<int64_t>(
       1, (units_max * rp.jsplit + K6_WARPS - 1) / K6_WARPS);
-  const int64_t n_eslots = (int64_t)nb * K6_WARPS;  // one energy slot per warp
+  // one energy slot per work item (unit x split), zeroed before the pass:
+  // items past the slab's real unit count are never written
+  const int64_t n_eslots = (int64_t)nb * K6_WARPS;
   // two-pass real space: lists of 32-bit entries (j < 2^23), capacity per
   // unit twice the mean half-shell pair count of K6_G centres plus slack
   // two-pass real space: the Verlet lists, or the list/evaluation split on request
@@ -652,12 +654,16 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
   // persistent pair-kernel grids (K6_PERSIST): at most one resident wave,
   // warps fetch further units from a counter; energy slots are summed over
   // the launched warps only
+  // Deterministic mode keeps the static unit -> warp map: per-warp energy
+  // partials (summed in a fixed order) must not depend on which warp took
+  // which unit.
+  const bool persist = K6_PERSIST && rp.half;
   CK(h->k6work.ensure(2 * sizeof(int)));
-  if (K6_PERSIST) CK(cudaMemsetAsync(h->k6work.p, 0, 2 * sizeof(int), h->stream));
-  int *work0 = K6_PERSIST ? h->k6work.as<int>() : nullptr;
-  int *work1 = K6_PERSIST ? h->k6work.as<int>() + 1 : nullptr;
+  if (persist) CK(cudaMemsetAsync(h->k6work.p, 0, 2 * sizeof(int), h->stream));
+  int *work0 = persist ? h->k6work.as<int>() : nullptr;
+  int *work1 = persist ? h->k6work.as<int>() + 1 : nullptr;
   auto grid_for = [&](const void *kern) -> unsigned {
-    if (!K6_PERSIST) return nb;
+    if (!persist) return nb;
     int &occ = h->k6_occ[kern];  // cached: the query stays out of graph captures
     if (occ < 1 &&
         (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, K6_WARPS * 32, 0) != cudaSuccess ||
@@ -667,7 +673,10 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
     }
     return (unsigned)std::min<int64_t>(nb, (int64_t)occ * h->n_sm);
   };
-  int64_t n_esum = n_eslot_all;
+  const int64_t n_esum = n_eslot_all;
+  if (pair_coul || lj_on)
+    CK(cudaMemsetAsync(h->eblk.p, 0, n_eslot_all * sizeof(double), h->stream));
+  if (lj_on) CK(cudaMemsetAsync(h->eblk_lj.p, 0, n_eslot_all * sizeof(double), h->stream));
   {
     K6Lists lists{split ? h->rs_list.as<uint32_t>() : nullptr,
                   split ? h->rs_count.as<int>() : nullptr, cap};
@@ -685,7 +694,6 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
                               : (rp.half ? k6_real_space<false, true, K6_MODE_FUSED>
                                          : k6_real_space<false, false, K6_MODE_FUSED>));
       const unsigned nbk = grid_for((const void *)kern);
-      n_esum = (int64_t)nbk * K6_WARPS;
       kern<<<nbk, K6_WARPS * 32, 0, h->stream>>>(
           h->sorted.as<double4>(), h->sorted_f.as<float4>(), h->sorted_cell.as<int>(),
           h->order.as<int>(), h->start.as<int>(), h->row_ustart.as<int>(), rp,
@@ -731,7 +739,6 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
                        : (rp.half ? k6_real_space<false, true, K6_MODE_OVF>
                                   : k6_real_space<false, false, K6_MODE_OVF>);
       const unsigned nbo = grid_for((const void *)ovf);
-      n_esum = n_eslots + (int64_t)nbo * K6_WARPS;
       ovf<<<nbo, K6_WARPS * 32, 0, h->stream>>>(
           h->sorted.as<double4>(), h->sorted_f.as<float4>(), h->sorted_cell.as<int>(),
           h->order.as<int>(), h->start.as<int>(), h->row_ustart.as<int>(), rp,

@@ -37,12 +37,10 @@
 //   stage's mbarrier.  Two stages: the MMAs of block k overlap the
 //   production of block k+1.
 
-#ifndef K1_TABLES
-// 1: per-particle m_y / m_z phase tables written by k1t_prep and read by the
-// producers; 0: a sincospi per particle and run in the producers (measured
+// per-particle m_y / m_z phase tables written by k1t_prep and read by the
+// producers (a sincospi per particle and run in the producers measured
 // slower: c5 S(k) 70 vs 48.5 ms, the producers are on the critical path)
-#define K1_TABLES 1
-#endif
+constexpr bool K1_TABLES = true;
 constexpr int TC_S = 6;                     // byte slices per operand
 constexpr int TC_W0 = 4;                    // kept levels: w = s + t >= TC_W0
 constexpr int TC_NL = 2 * TC_S - 1 - TC_W0; // 7 levels
@@ -147,23 +145,18 @@ __device__ __forceinline__ void tc_st8(uint32_t taddr, const uint32_t (&r)[8]) {
 __device__ __forceinline__ void tc_wait_st() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
-#ifndef K1_ACP
-// 1: G slices staged in TMEM by tcgen05.cp, TS-form MMAs (c5 S(k) 47.2 ->
-// 41.2 ms against unmerged SS); 0 (default): SS-form merged MMAs read G
-// from shared memory directly -- the staging copies execute in the tensor
-// pipe in order with the MMAs, and once MMAs are merged along N each G
-// slice feeds only 1-3 of them (c5 39.9 -> 37.8 ms with K1_MERGE 3)
-#define K1_ACP 0
-#endif
-static_assert(!K1_ACP || TC_NL * TC_NMAX + 32 <= 512, "TMEM: levels + 4 G slots");
+// SS-form merged MMAs read G from shared memory directly.  Staging G in TMEM
+// (tcgen05.cp) for TS-form MMAs measured slower once MMAs are merged along N
+// (each G slice then feeds only 1-3 MMAs and the copies occupy the tensor
+// pipe in order with them): c5 39.9 (TS) vs 37.8 ms (SS, merge 3).
 #ifndef K1_MERGE
-#define K1_MERGE 3  // SS: 3 best (c5 37.8 ms; 2: 39.1, 4: 38.2); TS: 2 (39.9 ms)
+#define K1_MERGE 3  // c5 37.8 ms; 2: 39.1, 4: 38.2
 #endif
 // K1_MERGE = m > 1: one MMA covers up to m consecutive X slices
 // against G slice s, N = (m - 1) x 64 + npad (X slices sit 64 rows apart in
 // shared memory; levels 64 columns apart in TMEM, the columns npad..63 of a
 // level collect junk and are never read); accumulators zeroed first
-static_assert((K1_MERGE - 1) * TC_NMAX + TC_NMAX <= 256, "merged N <= 256");
+static_assert(K1_MERGE > 1 && (K1_MERGE - 1) * TC_NMAX + TC_NMAX <= 256, "merged N <= 256");
 // one lane of a converged warp (PTX elect.sync)
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
@@ -430,42 +423,7 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
         if (!(dbg & 2) && elect_one()) {
           const uint64_t gd = tc_desc(smem_u32(gbuf + gs * TC_S * TC_GSL));
           const uint64_t xd = tc_desc(smem_u32(xbuf + xs * xblk));
-          const uint32_t acc0 = it > 0 ? 1u : 0u;  // unmerged forms only
-          (void)acc0;
           constexpr int XSL = tc_xsl_bytes(XNP);
-#if K1_ACP
-          // G slices staged in TMEM (four 8-column slots after the levels),
-          // TS-form MMAs slice-major: each G slice leaves shared memory once
-          const uint32_t aslot = tmem + (uint32_t)(TC_NL * XNP);
-#pragma unroll
-          for (int ks = 0; ks < TC_KB / 32; ++ks) {
-#pragma unroll
-            for (int s = 0; s < TC_S; ++s) {
-              const uint32_t ta = aslot + (uint32_t)(((ks * TC_S + s) & 3) * 8);
-              tc_cp_a(ta, gd + (uint64_t)((s * TC_GSL + ks * 256) >> 4));
-#if K1_MERGE > 1
-              const uint32_t idesc0 = idesc & ~(63u << 17);
-#pragma unroll
-              for (int t = (TC_W0 - s > 0 ? TC_W0 - s : 0); t < TC_S; t += K1_MERGE) {
-                const int m = TC_S - t < K1_MERGE ? TC_S - t : K1_MERGE;
-                tc_mma_ts(tmem + (uint32_t)((s + t - TC_W0) * XNP), ta,
-                          xd + (uint64_t)((t * XSL + ks * 256) >> 4),
-                          idesc0 | ((uint32_t)(((m - 1) * XNP + npad) >> 3) << 17), 1u);
-              }
-#else
-#pragma unroll
-              for (int t = 0; t < TC_S; ++t) {
-                const int l = s + t - TC_W0;
-                if (l < 0) continue;
-                const int s_lo = TC_W0 + l - (TC_S - 1) > 0 ? TC_W0 + l - (TC_S - 1) : 0;
-                tc_mma_ts(tmem + (uint32_t)(l * npad), ta,
-                          xd + (uint64_t)((t * XSL + ks * 256) >> 4), idesc,
-                          (s > s_lo || ks > 0) ? 1u : acc0);
-              }
-#endif
-            }
-          }
-#elif K1_MERGE > 1
           // SS form with merged N: each G slice read from shared memory by
           // its merged MMAs, no staging copy into TMEM
           const uint32_t idesc0 = idesc & ~(63u << 17);
@@ -483,25 +441,6 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
               }
             }
           }
-#else
-#pragma unroll
-          for (int l = 0; l < TC_NL; ++l) {
-            constexpr int dummy = 0;
-            (void)dummy;
-            const int w = TC_W0 + l;
-            const int s_lo = w - (TC_S - 1) > 0 ? w - (TC_S - 1) : 0;
-#pragma unroll
-            for (int s = 0; s < TC_S; ++s) {
-              const int t = w - s;
-              if (t < 0 || t >= TC_S) continue;
-#pragma unroll
-              for (int ks = 0; ks < TC_KB / 32; ++ks)
-                tc_mma(tmem + (uint32_t)(l * npad), gd + (uint64_t)((s * TC_GSL + ks * 256) >> 4),
-                       xd + (uint64_t)((t * XSL + ks * 256) >> 4), idesc,
-                       (s > s_lo || ks > 0) ? 1u : acc0);
-            }
-          }
-#endif
           tc_commit(smem_u32(&g_empty[gs]));
           tc_commit(smem_u32(&x_empty[xs]));
         } else if ((dbg & 2) && lane == 0) {
@@ -534,7 +473,6 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
         double2 cur[4], e1[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-#if K1_TABLES
           if (active) {
             const double2 yv = ytab[(int64_t)(myl - ymin) * np + j + u];
             const double2 zv = ztab[(int64_t)(run.x - zmin) * np + j + u];
@@ -543,21 +481,6 @@ __global__ void __launch_bounds__(TC_NTHREADS, 1)
           } else {
             cur[u] = e1[u] = make_double2(0.0, 0.0);
           }
-#else
-          // run start (q/qmax) e^{-i 2pi (m_y0 f_y + m_z f_z)} straight from the
-          // particle (no per-particle tables), then the m_y recurrence
-          const int64_t jj = p_begin + j + u;
-          if (active && jj < p_end) {
-            const double4 fp = frac[jj];
-            double sn, cs;
-            sincospi(2.0 * fma((double)myl, fp.y, (double)run.x * fp.z), &sn, &cs);
-            const double sc = fp.w * inv_qmax;
-            cur[u] = make_double2(sc * cs, -sc * sn);
-            e1[u] = base[3 * jj + 1];
-          } else {
-            cur[u] = e1[u] = make_double2(0.0, 0.0);
-          }
-#endif
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {

@@ -197,17 +197,9 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t local_addr, uint32_
                : "memory");
 }
 
-#ifndef T3_ACP
-#define T3_ACP 0
-#endif
-// T3_ACP 1: stage the A slices in TMEM (tcgen05.cp, four 8-column slots
-// after the level accumulators) and issue the MMAs in TS form, slice-major,
-// so the tensor core reads each A slice from shared memory once per K step
-// instead of once per slice pair (c5 forces 91 -> 84 ms before merging).
-// 0 (default): SS-form merged MMAs -- with T3_MERGE each A slice feeds only
-// 1-2 MMAs, and the staging copies cost tensor-pipe time in order with the
-// MMAs (c5 79.0 -> 73.2 ms, c2 0.164 -> 0.156 ms)
-static_assert(!T3_ACP || T3_NL * T3_NP + 32 <= 512, "TMEM: levels + 4 A slots");
+// SS-form merged MMAs: each A slice read from shared memory by its 1-2 MMAs.
+// Staging A in TMEM for TS-form MMAs (slice-major) measured slower once the
+// MMAs are merged: c5 forces 79.0 (TS) vs 73.2 ms (SS), c2 0.164 vs 0.156.
 #ifndef T3_MERGE
 #define T3_MERGE 3  // c5 forces 84.2 -> 81.1 ms
 #endif
@@ -215,7 +207,7 @@ static_assert(!T3_ACP || T3_NL * T3_NP + 32 <= 512, "TMEM: levels + 4 A slots");
 // t..t+m-1 against A slice s -- N = m x 80 rows of B (the slices are
 // contiguous in shared memory) into the m consecutive level accumulators
 // (contiguous in TMEM); accumulators are zeroed first and every MMA adds
-static_assert(T3_MERGE * T3_NP <= 256, "merged N <= 256");
+static_assert(T3_MERGE > 1 && T3_MERGE * T3_NP <= 256, "merged N <= 256");
 
 // k3t_gemm: grid (particle tiles of 64, M tiles, k splits), clusters of
 // T3_CL consecutive particle tiles: every A block is bulk-copied once per
@@ -297,8 +289,6 @@ __global__ void __launch_bounds__(T3_THREADS, 1)
     }
   } else if (warp == T3_PROD) {
     {
-      const uint32_t idesc =
-          (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(T3_NP >> 3) << 17) | (8u << 24);
       for (int it = 0; it < nkb; ++it) {
         const int bs = it % T3_BS, as = it % T3_AS;
         mbar_wait(smem_u32(&b_full[bs]), (it / T3_BS) & 1);
@@ -308,40 +298,6 @@ __global__ void __launch_bounds__(T3_THREADS, 1)
         if (!(dbg & 2) && elect_one()) {
           const uint64_t ad = tc_desc(smem_u32(abuf + as * ABLK));
           const uint64_t bd = tc_desc(smem_u32(bbuf + bs * T3_S * T3_BSL));
-          const uint32_t acc0 = it > 0 ? 1u : 0u;  // unmerged forms only
-          (void)acc0;
-          (void)idesc;
-#if T3_ACP
-          const uint32_t aslot = tmem + (uint32_t)(T3_NL * T3_NP);
-#pragma unroll
-          for (int ks = 0; ks < TC_KB / 32; ++ks) {
-#pragma unroll
-            for (int s = 0; s < T3_S; ++s) {
-              const uint32_t ta = aslot + (uint32_t)(((ks * T3_S + s) & 3) * 8);
-              tc_cp_a(ta, ad + (uint64_t)((s * TC_GSL + ks * 256) >> 4));
-#if T3_MERGE > 1
-              constexpr uint32_t idesc0 = (2u << 4) | (1u << 7) | (1u << 10) | (8u << 24);
-#pragma unroll
-              for (int t = (T3_W0 - s > 0 ? T3_W0 - s : 0); t < T3_S; t += T3_MERGE) {
-                const int m = T3_S - t < T3_MERGE ? T3_S - t : T3_MERGE;
-                tc_mma_ts(tmem + (uint32_t)((s + t - T3_W0) * T3_NP), ta,
-                          bd + (uint64_t)((t * T3_BSL + ks * 256) >> 4),
-                          idesc0 | ((uint32_t)((m * T3_NP) >> 3) << 17), 1u);
-              }
-#else
-#pragma unroll
-              for (int t = 0; t < T3_S; ++t) {
-                const int l = s + t - T3_W0;
-                if (l < 0) continue;
-                const int s_lo = T3_W0 + l - (T3_S - 1) > 0 ? T3_W0 + l - (T3_S - 1) : 0;
-                tc_mma_ts(tmem + (uint32_t)(l * T3_NP), ta,
-                          bd + (uint64_t)((t * T3_BSL + ks * 256) >> 4), idesc,
-                          (s > s_lo || ks > 0) ? 1u : acc0);
-              }
-#endif
-            }
-          }
-#elif T3_MERGE > 1
           // SS form with merged N: A slice s read from shared memory by its
           // (one or two) MMAs, no staging copy into TMEM
           constexpr uint32_t idesc0 = (2u << 4) | (1u << 7) | (1u << 10) | (8u << 24);
@@ -359,23 +315,6 @@ __global__ void __launch_bounds__(T3_THREADS, 1)
               }
             }
           }
-#else
-#pragma unroll
-          for (int l = 0; l < T3_NL; ++l) {
-            const int w = T3_W0 + l;
-            const int s_lo = w - (T3_S - 1) > 0 ? w - (T3_S - 1) : 0;
-#pragma unroll
-            for (int s = 0; s < T3_S; ++s) {
-              const int t = w - s;
-              if (t < 0 || t >= T3_S) continue;
-#pragma unroll
-              for (int ks = 0; ks < TC_KB / 32; ++ks)
-                tc_mma(tmem + (uint32_t)(l * T3_NP), ad + (uint64_t)((s * TC_GSL + ks * 256) >> 4),
-                       bd + (uint64_t)((t * T3_BSL + ks * 256) >> 4), idesc,
-                       (s > s_lo || ks > 0) ? 1u : acc0);
-            }
-          }
-#endif
           tc_commit(smem_u32(&b_empty[bs]));
           if (T3_CL == 1)
             tc_commit(smem_u32(&a_empty[as]));

@@ -90,9 +90,6 @@ constexpr int K3_CH = 32;         // k-items per shared-memory chunk
 #ifndef K6_HI_WAVES
 #define K6_HI_WAVES 3             // fused pair kernel at 5 blocks/SM from this many waves up
 #endif
-#ifndef K6_PERSIST
-#define K6_PERSIST 1              // pair-kernel grids of one resident wave, units fetched by warps
-#endif
 #ifndef K6_SPLIT
 #define K6_SPLIT 0                // real space as traversal + evaluation passes (measured slower)
 #endif
@@ -296,8 +293,6 @@ struct ewb_handle {
   int row_lo = -1, row_hi = -1;  // explicit centre rows of the next real-space pass
   int rs_split = K6_SPLIT;        // two-pass real space (pair lists in HBM), off by default
   DBuf rs_list, rs_count;         // per-unit pair lists and their lengths
-  DBuf k6work;                    // work counters of the persistent pair-kernel grids
-  std::map<const void *, int> k6_occ;  // resident blocks per SM of each pair-kernel variant
   // Verlet pair lists (ewb_set_skin): lists built at r_c + skin are reused
   // while no particle has moved more than skin/2 since the build
   double skin = 0.0;
@@ -448,7 +443,7 @@ void ewb_destroy(ewb_handle *h) {
                   &h->order_tmp, &h->order, &h->sorted, &h->sorted_cell, &h->row_ustart,
                   &h->sorted_f, &h->tc_qmax, &h->tc_ytab, &h->tc_ztab, &h->tc_xsl, &h->t3_wsl,
                   &h->t3_rscale, &h->pairc, &h->eblk_r, &h->fsorted, &h->force_in,
-                  &h->rs_list, &h->rs_count, &h->k6work, &h->vl_xb, &h->vl_dmax})
+                  &h->rs_list, &h->rs_count, &h->vl_xb, &h->vl_dmax})
     b->release();
   if (h->hscr) cudaFreeHost(h->hscr);
   h->plan.release();

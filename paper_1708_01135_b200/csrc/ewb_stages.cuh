@@ -651,28 +651,6 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
     CK(cudaMemsetAsync(h->fsorted.p, 0, (size_t)n * 3 * sizeof(double), h->stream));
     facc = h->fsorted.as<double>();
   }
-  // persistent pair-kernel grids (K6_PERSIST): at most one resident wave,
-  // warps fetch further units from a counter; energy slots are summed over
-  // the launched warps only
-  // Deterministic mode keeps the static unit -> warp map: per-warp energy
-  // partials (summed in a fixed order) must not depend on which warp took
-  // which unit.
-  const bool persist = K6_PERSIST && rp.half;
-  CK(h->k6work.ensure(2 * sizeof(int)));
-  if (persist) CK(cudaMemsetAsync(h->k6work.p, 0, 2 * sizeof(int), h->stream));
-  int *work0 = persist ? h->k6work.as<int>() : nullptr;
-  int *work1 = persist ? h->k6work.as<int>() + 1 : nullptr;
-  auto grid_for = [&](const void *kern) -> unsigned {
-    if (!persist) return nb;
-    int &occ = h->k6_occ[kern];  // cached: the query stays out of graph captures
-    if (occ < 1 &&
-        (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, K6_WARPS * 32, 0) != cudaSuccess ||
-         occ < 1)) {
-      cudaGetLastError();
-      occ = 1;
-    }
-    return (unsigned)std::min<int64_t>(nb, (int64_t)occ * h->n_sm);
-  };
   const int64_t n_esum = n_eslot_all;
   if (pair_coul || lj_on)
     CK(cudaMemsetAsync(h->eblk.p, 0, n_eslot_all * sizeof(double), h->stream));
@@ -693,12 +671,11 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
                                          : k6_real_space<true, false, K6_MODE_FUSED>)
                               : (rp.half ? k6_real_space<false, true, K6_MODE_FUSED>
                                          : k6_real_space<false, false, K6_MODE_FUSED>));
-      const unsigned nbk = grid_for((const void *)kern);
-      kern<<<nbk, K6_WARPS * 32, 0, h->stream>>>(
+      kern<<<nb, K6_WARPS * 32, 0, h->stream>>>(
           h->sorted.as<double4>(), h->sorted_f.as<float4>(), h->sorted_cell.as<int>(),
           h->order.as<int>(), h->start.as<int>(), h->row_ustart.as<int>(), rp,
           facc, eb, eb_lj, h->errflag.as<int>(),
-          h->pairc.as<unsigned long long>(), lists, work0);
+          h->pairc.as<unsigned long long>(), lists);
       CKL();
     } else {
       // pass 1: traversal -> per-unit pair lists (the LJ switch only
@@ -707,11 +684,11 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
       if (!reuse) {
         auto trav = rp.half ? k6_real_space<false, true, K6_MODE_LIST>
                             : k6_real_space<false, false, K6_MODE_LIST>;
-        trav<<<grid_for((const void *)trav), K6_WARPS * 32, 0, h->stream>>>(
+        trav<<<nb, K6_WARPS * 32, 0, h->stream>>>(
             h->sorted.as<double4>(), h->sorted_f.as<float4>(), h->sorted_cell.as<int>(),
             h->order.as<int>(), h->start.as<int>(), h->row_ustart.as<int>(), rp,
             facc, nullptr, nullptr, h->errflag.as<int>(),
-            h->pairc.as<unsigned long long>(), lists, work0);
+            h->pairc.as<unsigned long long>(), lists);
         CKL();
       }
       if (verlet) {
@@ -738,12 +715,11 @@ int stage_real_space(ewb_handle *h, int part, int nparts, double *d_force, doubl
                                   : k6_real_space<true, false, K6_MODE_OVF>)
                        : (rp.half ? k6_real_space<false, true, K6_MODE_OVF>
                                   : k6_real_space<false, false, K6_MODE_OVF>);
-      const unsigned nbo = grid_for((const void *)ovf);
-      ovf<<<nbo, K6_WARPS * 32, 0, h->stream>>>(
+      ovf<<<nb, K6_WARPS * 32, 0, h->stream>>>(
           h->sorted.as<double4>(), h->sorted_f.as<float4>(), h->sorted_cell.as<int>(),
           h->order.as<int>(), h->start.as<int>(), h->row_ustart.as<int>(), rp,
           facc, eb + n_eslots, eb_lj ? eb_lj + n_eslots : nullptr,
-          h->errflag.as<int>(), nullptr, lists, work1);
+          h->errflag.as<int>(), nullptr, lists);
       CKL();
     }
   }

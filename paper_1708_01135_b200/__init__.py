@@ -22,6 +22,7 @@ from .core import (
     SimulationBox,
     create_particle_set,
     minimum_image,
+    set_error_types,
     total_charge,
     wrap_position,
 )
@@ -44,7 +45,8 @@ __all__ = [
     "ContractViolationError", "CutoffTooLargeError", "EwaldmdError",
     "GlobalAccumulator", "KSpaceEmptyError", "LatticeError",
     "NeutralityError", "OracleSizeError", "ParticleSet", "SimulationBox",
-    "create_particle_set", "minimum_image", "total_charge", "wrap_position",
+    "create_particle_set", "minimum_image", "set_error_types", "total_charge",
+    "wrap_position",
     "BALANCE_CONSTANT", "EwaldEnergies", "EwaldParams", "EwaldSolver",
     "ReciprocalSpace", "choose_parameters", "compute_rho_hat",
     "enumerate_kvectors", "long_range_energy_forces", "self_energy",

@@ -340,12 +340,21 @@ class SlabEwald:
         n_own = q.shape[0]
         rows = st.rows(pos).long()
         # ---- halo exchange: (x, y, z, q) of my particles in every peer's halo
+        # (one nonzero over all peers: its (peer, particle) pairs come out
+        # peer-major, one host synchronisation for the whole selection)
+        need = self.need[:, rows]
+        need[self.rank] = False
+        nz = torch.nonzero(need)
+        cnt = torch.bincount(nz[:, 0], minlength=self.world).tolist() if nz.numel() else \
+            [0] * self.world
         send_idx, send = [None] * self.world, [None] * self.world
+        off = 0
+        xq = torch.cat([pos, q[:, None]], dim=1)
         for p in range(self.world):
             if p != self.rank:
-                send_idx[p] = torch.nonzero(self.need[p][rows]).flatten()
-                send[p] = torch.cat([pos[send_idx[p]], q[send_idx[p], None]], dim=1)
-        cnt = [0 if s is None else int(s.shape[0]) for s in send]
+                send_idx[p] = nz[off:off + cnt[p], 1]
+                send[p] = xq[send_idx[p]]
+            off += cnt[p]
         M = comm.counts(cnt)
         recv_counts = M[:, self.rank]
         recv = comm.exchange(send, recv_counts, 4, torch.float64, dev)
@@ -420,14 +429,21 @@ class ShardedEwald:
             self.slab = SlabEwald(self.st, self.device, n, self.group, self.overlap)
         sl = self.slab
         rows = self.st.rows(pos).long()       # same on every rank
-        owned = [torch.nonzero(sl.owned_mask(rows, r)).flatten() for r in range(sl.world)]
-        mine = owned[sl.rank]
+        # owner of every particle; a stable sort groups them by owner in
+        # index order (one host synchronisation for the per-owner counts)
+        lows = torch.tensor([lo for lo, _ in sl.bounds], dtype=torch.long, device=rows.device)
+        owner = torch.bucketize(rows, lows, right=True) - 1
+        perm = torch.argsort(owner, stable=True)
+        counts = torch.bincount(owner, minlength=sl.world).tolist()
+        start = [0]
+        for c in counts:
+            start.append(start[-1] + c)
+        mine = perm[start[sl.rank]:start[sl.rank + 1]]
         f_own = torch.zeros((mine.shape[0], 3), dtype=torch.float64, device=self.device)
         u = sl.evaluate_local(pos[mine].contiguous(), q[mine].contiguous(), f_own,
                               rho_out=rho_out)
-        blocks = sl.comm.all_gather_rows(f_own, [o.shape[0] for o in owned], 3)
-        for idx, b in zip(owned, blocks):
-            force.index_add_(0, idx, b)
+        blocks = sl.comm.all_gather_rows(f_own, counts, 3)
+        force.index_add_(0, perm, torch.cat(blocks) if len(blocks) > 1 else blocks[0])
         return u
 
 

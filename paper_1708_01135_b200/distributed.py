@@ -30,11 +30,14 @@ particle count, ewb_set_geometry_n):
   unwrapped positions) is reduced with them, so every rank raises the same
   exception together and no caller force array is touched.
 
-``SlabEwald`` is the domain-decomposed interface (each rank holds only its
-own particles).  ``ShardedEwald`` is the drop-in over the reference API,
-where every rank holds the full configuration: it selects its own rows'
-particles, runs SlabEwald, and returns the full force array by an all-gather
-of the owned rows (no 3N all-reduce).
+``SlabEwald.evaluate_local`` is the domain-decomposed interface (each rank
+holds only its own particles; halos by point-to-point exchange, as above).
+``ShardedEwald`` is the drop-in over the reference API, where every rank
+holds the full configuration (``SlabEwald.evaluate_replicated``): a rank
+takes its own rows' particles and its halo straight from that configuration
+(no point-to-point traffic at all), and the forces of every rank's own + halo
+particles come back by ONE all-gather, summed into the full array on every
+rank (the halo partners' forces included; no 3N all-reduce).
 
 ``stages`` is the device-stage interface (``DeviceStages`` wraps the C-ABI);
 the tests inject a CPU stand-in (tests/cpu_stages.py) to run this
@@ -335,6 +338,90 @@ class SlabEwald:
             cur.wait_stream(self._main)
         return out
 
+    def _compute(self, lpos, lq, n_own, rho_out):
+        """The rank's device work on its loaded particles (own first, then
+        halo): real space of its rows on the side stream, S(k) partial + the
+        all-reduce, finalisation, reciprocal forces and self energy of the own
+        particles.  Returns (forces of own + halo particles, energies [u_sr,
+        u_lr (rank 0 only), u_self, device error flag]) before the energy
+        all-reduce."""
+        st, comm, dev = self.st, self.comm, self.device
+        n_loc = lq.shape[0]
+        flocal = torch.zeros((n_loc, 3), dtype=torch.float64, device=dev)
+        ns = st.slot_size()
+        if self._slots is None or self._slots.numel() != ns:
+            self._slots = torch.empty(ns, dtype=torch.float64, device=dev)
+        en = torch.zeros(4, dtype=torch.float64, device=dev)
+        st.load(lpos, lq)
+        # ---- real space of my rows beside the reciprocal chain
+        if self._side is not None:
+            self._side.wait_stream(self._main)
+            st.set_stream(self._side)
+            st.real_space_rows(self.lo, self.hi, flocal)
+            st.set_stream(self._main)
+        else:
+            st.real_space_rows(self.lo, self.hi, flocal)
+        st.rho_partial(0, n_own, self._slots)
+        comm.allreduce_(self._slots)          # S(k) = sum of the ranks' partials
+        st.finalize(self._slots, rho_out)
+        if self._side is not None:
+            self._main.wait_stream(self._side)  # both add into flocal
+        st.recip_forces(0, n_own, flocal)
+        st.self_energy_range(0, n_own)
+        st.energies(en)
+        if self.rank != 0:
+            en[1] = 0.0                        # u_lr is complete on every rank
+        return flocal, en
+
+    def evaluate_replicated(self, pos, q, force, rho_out=None):
+        """Every rank holds the FULL configuration (the reference API): it
+        takes its own rows' particles and its halo straight from it (no
+        point-to-point exchange), and the forces of every rank's own + halo
+        particles return by ONE all-gather, summed into the full array on
+        every rank (halo partner forces included).  Two host
+        synchronisations size the per-rank lists; the collectives are the
+        S(k) all-reduce, the 4-double energy all-reduce and the all-gather."""
+        if self._main is None:
+            return self._replicated(pos, q, force, rho_out)
+        cur = torch.cuda.current_stream(self.device)
+        self._main.wait_stream(cur)
+        try:
+            with torch.cuda.stream(self._main):
+                self.st.set_stream(self._main)
+                out = self._replicated(pos, q, force, rho_out)
+        finally:
+            self.st.set_stream(None)
+            cur.wait_stream(self._main)
+        return out
+
+    def _replicated(self, pos, q, force, rho_out):
+        st, comm, W = self.st, self.comm, self.world
+        rows = st.rows(pos).long()
+        dev = rows.device
+        lows = torch.tensor([lo for lo, _ in self.bounds], dtype=torch.long, device=dev)
+        owner = torch.bucketize(rows, lows, right=True) - 1
+        ranks = torch.arange(W, device=dev)[:, None]
+        own_m = owner[None, :] == ranks
+        halo_m = self.need.to(dev)[:, rows] & ~own_m
+        # (rank, own 0 / halo 1, particle), rank-major with own before halo
+        nz = torch.nonzero(torch.stack([own_m, halo_m], dim=1))
+        cnt = torch.bincount(nz[:, 0] * 2 + nz[:, 1], minlength=2 * W).tolist()
+        sizes = [cnt[2 * r] + cnt[2 * r + 1] for r in range(W)]
+        starts = [0]
+        for sz in sizes:
+            starts.append(starts[-1] + sz)
+        lidx = nz[starts[self.rank]:starts[self.rank + 1], 2]
+        n_own = cnt[2 * self.rank]
+        flocal, en = self._compute(pos[lidx].contiguous(), q[lidx].contiguous(), n_own, rho_out)
+        comm.allreduce_(en)                    # energies + error flags of all ranks
+        u_sr, u_lr, u_self, err = en.tolist()
+        if err:
+            _raise_device_error(err)           # every rank, before any force is written
+        blocks = comm.all_gather_rows(flocal, sizes, 3)
+        force.index_add_(0, nz[:, 2].to(force.device),
+                         torch.cat(blocks).to(force.device) if len(blocks) > 1 else blocks[0])
+        return u_sr, u_lr, u_self
+
     def _evaluate(self, pos, q, force, rho_out):
         st, comm, dev = self.st, self.comm, self.device
         n_own = q.shape[0]
@@ -365,31 +452,7 @@ class SlabEwald:
             lq = torch.cat([q, h[:, 3]]).contiguous()
         else:
             lpos, lq = pos.contiguous(), q.contiguous()
-        n_loc = lq.shape[0]
-        flocal = torch.zeros((n_loc, 3), dtype=torch.float64, device=dev)
-        ns = st.slot_size()
-        if self._slots is None or self._slots.numel() != ns:
-            self._slots = torch.empty(ns, dtype=torch.float64, device=dev)
-        en = torch.zeros(4, dtype=torch.float64, device=dev)
-        st.load(lpos, lq)
-        # ---- real space of my rows beside the reciprocal chain
-        if self._side is not None:
-            self._side.wait_stream(self._main)
-            st.set_stream(self._side)
-            st.real_space_rows(self.lo, self.hi, flocal)
-            st.set_stream(self._main)
-        else:
-            st.real_space_rows(self.lo, self.hi, flocal)
-        st.rho_partial(0, n_own, self._slots)
-        comm.allreduce_(self._slots)          # S(k) = sum of the ranks' partials
-        st.finalize(self._slots, rho_out)
-        if self._side is not None:
-            self._main.wait_stream(self._side)  # both add into flocal
-        st.recip_forces(0, n_own, flocal)
-        st.self_energy_range(0, n_own)
-        st.energies(en)
-        if self.rank != 0:
-            en[1] = 0.0                        # u_lr is complete on every rank
+        flocal, en = self._compute(lpos, lq, n_own, rho_out)
         # ---- reverse exchange: halo partners' forces back to their owners
         back = [None] * self.world
         off = n_own
@@ -427,24 +490,7 @@ class ShardedEwald:
         n = q.shape[0]
         if self.slab is None or self.slab.n_global != n:
             self.slab = SlabEwald(self.st, self.device, n, self.group, self.overlap)
-        sl = self.slab
-        rows = self.st.rows(pos).long()       # same on every rank
-        # owner of every particle; a stable sort groups them by owner in
-        # index order (one host synchronisation for the per-owner counts)
-        lows = torch.tensor([lo for lo, _ in sl.bounds], dtype=torch.long, device=rows.device)
-        owner = torch.bucketize(rows, lows, right=True) - 1
-        perm = torch.argsort(owner, stable=True)
-        counts = torch.bincount(owner, minlength=sl.world).tolist()
-        start = [0]
-        for c in counts:
-            start.append(start[-1] + c)
-        mine = perm[start[sl.rank]:start[sl.rank + 1]]
-        f_own = torch.zeros((mine.shape[0], 3), dtype=torch.float64, device=self.device)
-        u = sl.evaluate_local(pos[mine].contiguous(), q[mine].contiguous(), f_own,
-                              rho_out=rho_out)
-        blocks = sl.comm.all_gather_rows(f_own, counts, 3)
-        force.index_add_(0, perm, torch.cat(blocks) if len(blocks) > 1 else blocks[0])
-        return u
+        return self.slab.evaluate_replicated(pos, q, force, rho_out=rho_out)
 
 
 def _resolve_devices(workers):

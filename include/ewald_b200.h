@@ -200,6 +200,13 @@ int ewb_rs_geometry(ewb_handle *h, int64_t *info4);
 /* Row of cells of each of n particles (device pointers), binned exactly as
  * the pair kernel's cell list (celllist.py:75-108 binning). */
 int ewb_dev_rows(ewb_handle *h, const double *d_pos, int64_t n, int *d_rows);
+/* Particles grouped by row of cells (a stable sort on the row: ascending
+ * index within a row) into d_order[n], and the row offsets d_row_start
+ * [n_rows + 1]: every rank's own particles and halo of the multi-GPU
+ * decomposition are slices of d_order (the reference partitions particles
+ * into worker blocks, engine.py:75-82). */
+int ewb_dev_row_order(ewb_handle *h, const double *d_pos, int64_t n, int *d_order,
+                      int *d_row_start);
 /* Real space of the loaded particles with centres restricted to the rows
  * [row_lo, row_hi): the rank's own rows, partners from its own rows and the
  * halo rows it received.  Half shell: forces also land on halo partners

@@ -73,6 +73,7 @@ SIGNATURES = {
     "ewb_set_geometry_n": (_INT, [_P, _I64]),
     "ewb_rs_geometry": (_INT, [_P, _P]),
     "ewb_dev_rows": (_INT, [_P, _P, _I64, _P]),
+    "ewb_dev_row_order": (_INT, [_P, _P, _I64, _P, _P]),
     "ewb_dev_real_space_rows": (_INT, [_P, _INT, _INT, _P, _P]),
     "ewb_dev_energies": (_INT, [_P, _P]),
     "ewb_dev_check": (_INT, [_P]),
@@ -478,6 +479,9 @@ class Handle:
         info = np.zeros(4, dtype=np.int64)
         self._check(self.lib.ewb_rs_geometry(self.h, _ptr(info)))
         return dict(zip(("cpd", "rad", "n_rows", "fold"), info.tolist()))
+
+    def dev_row_order(self, d_pos, n, d_order, d_row_start):
+        self._check(self.lib.ewb_dev_row_order(self.h, d_pos, int(n), d_order, d_row_start))
 
     def dev_rows(self, d_pos, n, d_rows):
         self._check(self.lib.ewb_dev_rows(self.h, d_pos, int(n), d_rows))

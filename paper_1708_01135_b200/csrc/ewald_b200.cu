@@ -33,6 +33,8 @@
 #include <string>
 #include <vector>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "ewald_b200.h"
 
 #define EWB_VERSION 100
@@ -293,6 +295,7 @@ struct ewb_handle {
   int row_lo = -1, row_hi = -1;  // explicit centre rows of the next real-space pass
   int rs_split = K6_SPLIT;        // two-pass real space (pair lists in HBM), off by default
   DBuf rs_list, rs_count;         // per-unit pair lists and their lengths
+  DBuf ro_key, ro_keyout, ro_idx, ro_cnt, ro_g, ro_tmp;  // ewb_dev_row_order scratch
   // Verlet pair lists (ewb_set_skin): lists built at r_c + skin are reused
   // while no particle has moved more than skin/2 since the build
   double skin = 0.0;
@@ -443,7 +446,8 @@ void ewb_destroy(ewb_handle *h) {
                   &h->order_tmp, &h->order, &h->sorted, &h->sorted_cell, &h->row_ustart,
                   &h->sorted_f, &h->tc_qmax, &h->tc_ytab, &h->tc_ztab, &h->tc_xsl, &h->t3_wsl,
                   &h->t3_rscale, &h->pairc, &h->eblk_r, &h->fsorted, &h->force_in,
-                  &h->rs_list, &h->rs_count, &h->vl_xb, &h->vl_dmax})
+                  &h->rs_list, &h->rs_count, &h->vl_xb, &h->vl_dmax, &h->ro_key, &h->ro_keyout,
+                  &h->ro_idx, &h->ro_cnt, &h->ro_g, &h->ro_tmp})
     b->release();
   if (h->hscr) cudaFreeHost(h->hscr);
   h->plan.release();
@@ -976,6 +980,58 @@ int ewb_dev_rows(ewb_handle *h, const double *d_pos, int64_t n, int *d_rows) {
   k_rows<<<blocks_for(n, 256), 256, 0, h->stream>>>(d_pos, n, h->L / (double)g[0], (int)g[0],
                                                    d_rows);
   CKL();
+  return EWB_OK;
+}
+
+}  // extern "C"
+namespace {
+__global__ void k_iota_hist(const int *__restrict__ key, int64_t n, int *__restrict__ idx,
+                            int *__restrict__ count) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  idx[i] = (int)i;
+  atomicAdd(count + key[i], 1);
+}
+}  // namespace
+extern "C" {
+
+// particles grouped by row of cells, ascending index within a row (stable
+// radix sort on the row), and the row offsets: the ownership and halo lists
+// of the multi-GPU decomposition are slices of d_order
+int ewb_dev_row_order(ewb_handle *h, const double *d_pos, int64_t n, int *d_order,
+                      int *d_row_start) {
+  int64_t g[4];
+  int rc = ewb_rs_geometry(h, g);
+  if (rc) return rc;
+  if (n < 1 || !d_pos || !d_order || !d_row_start) return h->fail(EWB_EINVAL, "bad arrays");
+  if (n >= ((int64_t)1 << 31)) return h->fail(EWB_EINVAL, "particle count too large");
+  CK(cudaSetDevice(h->device));
+  const int cpd = (int)g[0], n_rows = (int)g[2];
+  CK(h->ro_key.ensure(n * sizeof(int)));
+  CK(h->ro_keyout.ensure(n * sizeof(int)));
+  CK(h->ro_idx.ensure(n * sizeof(int)));
+  CK(h->ro_cnt.ensure((n_rows + 1) * sizeof(int)));
+  CK(h->ro_g.ensure((n_rows + 1) * sizeof(int)));
+  k_rows<<<blocks_for(n, 256), 256, 0, h->stream>>>(d_pos, n, h->L / (double)cpd, cpd,
+                                                   h->ro_key.as<int>());
+  CKL();
+  CK(cudaMemsetAsync(h->ro_cnt.p, 0, (n_rows + 1) * sizeof(int), h->stream));
+  k_iota_hist<<<blocks_for(n, 256), 256, 0, h->stream>>>(h->ro_key.as<int>(), n,
+                                                          h->ro_idx.as<int>(), h->ro_cnt.as<int>());
+  CKL();
+  k_scan_cells<<<1, 1024, 0, h->stream>>>(h->ro_cnt.as<int>(), n_rows, d_row_start,
+                                          h->ro_g.as<int>());
+  CKL();
+  int bits = 1;
+  while ((1 << bits) < n_rows) ++bits;
+  size_t tmp = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, h->ro_key.as<int>(), h->ro_keyout.as<int>(),
+                                     h->ro_idx.as<int>(), d_order, (int)n, 0, bits, h->stream));
+  CK(h->ro_tmp.ensure(tmp));
+  CK(cub::DeviceRadixSort::SortPairs(h->ro_tmp.p, tmp, h->ro_key.as<int>(),
+                                     h->ro_keyout.as<int>(), h->ro_idx.as<int>(), d_order, (int)n,
+                                     0, bits, h->stream));
+  ++h->launches;
   return EWB_OK;
 }
 

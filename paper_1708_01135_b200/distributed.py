@@ -117,6 +117,16 @@ class DeviceStages:
         self.h.dev_rows(pos.data_ptr(), pos.shape[0], out.data_ptr())
         return out
 
+    def row_order(self, pos, n_rows):
+        """(particle indices grouped by row of cells, ascending within a row;
+        row offsets as a host list) -- one host synchronisation."""
+        self.h.set_stream(torch.cuda.current_stream(pos.device).cuda_stream)
+        n = pos.shape[0]
+        order = torch.empty(n, dtype=torch.int32, device=pos.device)
+        start = torch.empty(n_rows + 1, dtype=torch.int32, device=pos.device)
+        self.h.dev_row_order(pos.data_ptr(), n, order.data_ptr(), start.data_ptr())
+        return order.long(), start.tolist()
+
     def load(self, pos, q):
         self.h.dev_load(pos.data_ptr(), q.data_ptr(), q.shape[0])
 
@@ -312,6 +322,17 @@ class SlabEwald:
                 continue
             need[s, halo_rows(lo, hi, self.cpd, self.rad, half)] = True
         self.need = torch.from_numpy(need).to(self.device)
+        # each rank's halo rows as runs [a, b) of consecutive rows
+        self._halo_runs = []
+        for r in range(self.world):
+            rr = np.nonzero(need[r])[0]
+            runs = []
+            for v in rr.tolist():
+                if runs and runs[-1][1] == v:
+                    runs[-1][1] = v + 1
+                else:
+                    runs.append([v, v + 1])
+            self._halo_runs.append([tuple(x) for x in runs])
         self._slots = None
         cuda = self.device.type == "cuda"
         self._main = torch.cuda.Stream(device=self.device) if cuda else None
@@ -365,9 +386,16 @@ class SlabEwald:
         comm.allreduce_(self._slots)          # S(k) = sum of the ranks' partials
         st.finalize(self._slots, rho_out)
         if self._side is not None:
-            self._main.wait_stream(self._side)  # both add into flocal
-        st.recip_forces(0, n_own, flocal)
-        st.self_energy_range(0, n_own)
+            # the reciprocal forces into their own buffer, so the force GEMM
+            # runs while the pair kernel is still busy on the side stream
+            frec = torch.zeros((n_own, 3), dtype=torch.float64, device=dev)
+            st.recip_forces(0, n_own, frec)
+            st.self_energy_range(0, n_own)
+            self._main.wait_stream(self._side)
+            flocal[:n_own] += frec
+        else:
+            st.recip_forces(0, n_own, flocal)
+            st.self_energy_range(0, n_own)
         st.energies(en)
         if self.rank != 0:
             en[1] = 0.0                        # u_lr is complete on every rank
@@ -396,29 +424,28 @@ class SlabEwald:
 
     def _replicated(self, pos, q, force, rho_out):
         st, comm, W = self.st, self.comm, self.world
-        rows = st.rows(pos).long()
-        dev = rows.device
-        lows = torch.tensor([lo for lo, _ in self.bounds], dtype=torch.long, device=dev)
-        owner = torch.bucketize(rows, lows, right=True) - 1
-        ranks = torch.arange(W, device=dev)[:, None]
-        own_m = owner[None, :] == ranks
-        halo_m = self.need.to(dev)[:, rows] & ~own_m
-        # (rank, own 0 / halo 1, particle), rank-major with own before halo
-        nz = torch.nonzero(torch.stack([own_m, halo_m], dim=1))
-        cnt = torch.bincount(nz[:, 0] * 2 + nz[:, 1], minlength=2 * W).tolist()
-        sizes = [cnt[2 * r] + cnt[2 * r + 1] for r in range(W)]
-        starts = [0]
-        for sz in sizes:
-            starts.append(starts[-1] + sz)
-        lidx = nz[starts[self.rank]:starts[self.rank + 1], 2]
-        n_own = cnt[2 * self.rank]
-        flocal, en = self._compute(pos[lidx].contiguous(), q[lidx].contiguous(), n_own, rho_out)
+        # particles grouped by row (one stable sort, one synchronisation):
+        # every rank's own rows and halo rows are slices of `order`
+        order, rstart = st.row_order(pos, self.n_rows)
+        lists, sizes, n_owns = [], [], []
+        for r, (lo, hi) in enumerate(self.bounds):
+            sl = [order[rstart[lo]:rstart[hi]]]
+            for a, b in self._halo_runs[r]:
+                sl.append(order[rstart[a]:rstart[b]])
+            lists.append(sl)
+            n_owns.append(rstart[hi] - rstart[lo])
+            sizes.append(sum(int(rstart[b] - rstart[a]) for a, b in self._halo_runs[r]) + n_owns[-1])
+        mine = lists[self.rank]
+        lidx = torch.cat(mine) if len(mine) > 1 else mine[0]
+        flocal, en = self._compute(pos[lidx].contiguous(), q[lidx].contiguous(),
+                                   n_owns[self.rank], rho_out)
         comm.allreduce_(en)                    # energies + error flags of all ranks
         u_sr, u_lr, u_self, err = en.tolist()
         if err:
             _raise_device_error(err)           # every rank, before any force is written
         blocks = comm.all_gather_rows(flocal, sizes, 3)
-        force.index_add_(0, nz[:, 2].to(force.device),
+        idx = torch.cat([t for sl in lists for t in sl])
+        force.index_add_(0, idx.to(force.device),
                          torch.cat(blocks).to(force.device) if len(blocks) > 1 else blocks[0])
         return u_sr, u_lr, u_self
 

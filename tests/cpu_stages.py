@@ -48,6 +48,12 @@ class OracleStages:
         cz = np.clip(np.floor(p[:, 2] / e).astype(np.int64), 0, self.cpd - 1)
         return torch.from_numpy((cy + self.cpd * cz).astype(np.int32))
 
+    def row_order(self, pos, n_rows):
+        rows = self.rows(pos).numpy()
+        order = np.argsort(rows, kind="stable")
+        start = np.concatenate([[0], np.cumsum(np.bincount(rows, minlength=n_rows))])
+        return torch.from_numpy(order.astype(np.int64)), start.tolist()
+
     def load(self, pos, q):
         self.pos = pos.detach().cpu().numpy().astype(np.float64)
         self.q = q.detach().cpu().numpy().astype(np.float64)

@@ -874,8 +874,8 @@ int ewb_dev_rho_partial(ewb_handle *h, int64_t i0, int64_t i1, double *d_slots) 
   }
   int n_part = 0;
   if ((rc = stage_rho(h, i0, i1, &n_part))) return rc;
-  const unsigned nb = blocks_for(n_pslots, RED_THREADS);
-  k2p_finalize<<<nb, RED_THREADS, 0, h->stream>>>(h->spart.as<double4>(), n_part, n_pslots,
+  const unsigned nb = blocks_for(n_pslots, K2P_THREADS);
+  k2p_finalize<<<nb, K2P_THREADS, 0, h->stream>>>(h->spart.as<double4>(), n_part, n_pslots,
                                                   nullptr, nullptr, h->plan.K, nullptr,
                                                   reinterpret_cast<double4 *>(d_slots), nullptr,
                                                   nullptr, 0);

@@ -174,9 +174,9 @@ int stage_finalize_pairs(ewb_handle *h, const double4 *src, int n_part, double *
                          double *d_u_out) {
   Plan &P = h->plan;
   const int64_t n_pslots = (int64_t)P.M1 * P.n_pitems;
-  const unsigned nb = blocks_for(n_pslots, RED_THREADS);
+  const unsigned nb = blocks_for(n_pslots, K2P_THREADS);
   CK(h->eblk_r.ensure(nb * sizeof(double)));
-  k2p_finalize<<<nb, RED_THREADS, 0, h->stream>>>(src, n_part, n_pslots, P.pslot_map.as<int4>(),
+  k2p_finalize<<<nb, K2P_THREADS, 0, h->stream>>>(src, n_part, n_pslots, P.pslot_map.as<int4>(),
                                                   P.slot_coeff.as<double>(), P.K, d_rho_out,
                                                   nullptr, h->sp.as<double2>(),
                                                   h->eblk_r.as<double>(), 1);

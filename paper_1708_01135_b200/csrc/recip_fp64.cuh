@@ -206,13 +206,16 @@ __global__ void __launch_bounds__(RED_THREADS)
 // slot, S(+-m_x) = (A+ -+ i A-)/2, scatter rho to the caller's k order, C*S to
 // the gather's slot layout, and u_lr partials.  finalize=0: only the summed
 // pair slots (multi-GPU partial S before the all-reduce).
-__global__ void __launch_bounds__(RED_THREADS)
+#ifndef K2P_THREADS
+#define K2P_THREADS 64  // small blocks: the slots spread over every SM (c2: 54 -> 216 blocks)
+#endif
+__global__ void __launch_bounds__(K2P_THREADS)
     k2p_finalize(const double4 *__restrict__ spart, int n_part, int64_t n_pslots,
                  const int4 *__restrict__ pmap, const double *__restrict__ slot_coeff, int64_t K,
                  double *__restrict__ rho_out, double4 *__restrict__ s_out,
                  double2 *__restrict__ sp, double *__restrict__ epart, int finalize) {
-  __shared__ double sh[RED_THREADS / 32];
-  const int64_t s = blockIdx.x * (int64_t)RED_THREADS + threadIdx.x;
+  __shared__ double sh[K2P_THREADS / 32];
+  const int64_t s = blockIdx.x * (int64_t)K2P_THREADS + threadIdx.x;
   double e = 0.0;
   if (s < n_pslots) {
     double4 A = make_double4(0.0, 0.0, 0.0, 0.0);
@@ -262,7 +265,7 @@ __global__ void __launch_bounds__(RED_THREADS)
     }
   }
   if (finalize) {
-    const double b = block_sum<RED_THREADS>(e, sh);
+    const double b = block_sum<K2P_THREADS>(e, sh);
     if (threadIdx.x == 0) epart[blockIdx.x] = b;
   }
 }

@@ -141,3 +141,22 @@ def test_solver_workers_errors_leave_forces(monkeypatch):
         solver.evaluate(ps)
     assert np.all(ps.force == 1.25)
     solver._multi.close()
+
+
+def test_solver_workers_wide_cutoff_stays_single_gpu(monkeypatch):
+    """r_c > L/2 (the image-shell path, N <= 4096) runs on one GPU even when
+    workers asks for more; results are the reference's."""
+    import paper_1708_01135_b200 as ew
+    monkeypatch.setenv("EWALDB200_SHARE_DEVICES", "1")
+    g = golden("wide_rand64")
+    box = ew.SimulationBox(float(g["L"]))
+    ps = ew.create_particle_set(g["pos"].shape[0], box)
+    ps.position[:] = g["pos"]
+    ps.charge[:] = g["q"]
+    params = ew.EwaldParams(float(g["alpha"]), float(g["r_cutoff"]), float(g["k_cutoff"]),
+                            float(g["tolerance"]))
+    solver = ew.EwaldSolver(box, params, workers=2, recip=ew.ReciprocalSpace(box, params, g["m_int"]))
+    assert solver._multi is None
+    res = solver.evaluate(ps)
+    assert rel(res.u_sr, float(g["u_sr"])) <= 1e-10
+    assert rel(res.u_lr, float(g["u_lr"])) <= 1e-10

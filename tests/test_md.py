@@ -167,3 +167,19 @@ def test_device_md_verlet_lists_match_rebuild_every_step(md, skin, expect_reuse)
         assert info["reuses"] == cfg.n_steps and info["builds"] == 1
     else:
         assert info["builds"] > 1 and info["reuses"] > 0
+
+
+def test_device_md_skin_on_scan_all_box_matches_golden(md):
+    """A box too small for a stencil cell grid (scan-all real space) keeps
+    rebuilding every step even with skin > 0; the reference trajectory is
+    reproduced as without a skin."""
+    g = golden("md_run")
+    ps = _ps(g["pos0"], g["q"], float(g["L"]))
+    cfg = md.SimConfig(n_particles=64, box_edge=14.0, tolerance=1e-6, dt=0.01, n_steps=8,
+                       velocity_scale=0.05, seed=1, lj_on=True,
+                       lj=md.LJParams(1.0, 2.5, 6.25))
+    m = md.run(cfg, ps, skin=0.4)
+    assert m.verlet["reuses"] == 0
+    assert np.abs(ps.position - g["pos_final"]).max() <= 1e-10
+    et = np.array(m.energy_trace)
+    assert np.abs(et - g["energy_trace"]).max() <= 1e-9 * np.abs(g["energy_trace"]).max()

@@ -231,3 +231,61 @@ def test_reference_arm_json_contract():
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
     assert d["config"]["parallelism"] == "single GPU" and d["config"]["n_particles"] == 1000
+
+
+def test_host_pins_policy(monkeypatch):
+    """_lib.HostPins: an owning, contiguous, large array is registered on its
+    second sighting and unregistered when it dies; views, small arrays and
+    non-owning arrays are never registered (the C calls are faked)."""
+    import gc
+    from paper_1708_01135_b200 import _lib
+    calls = []
+
+    class FakeLib:
+        def ewb_host_register(self, p, n):
+            calls.append(("reg", p.value, n))
+            return 0
+
+        def ewb_host_unregister(self, p):
+            calls.append(("unreg", p.value))
+            return 0
+    monkeypatch.setattr(_lib, "load_library", lambda: FakeLib())
+    pins = _lib.HostPins()
+    a = np.zeros((1 << 16, 3))
+    pins.touch(a)
+    assert calls == []                      # first sighting: remembered only
+    pins.touch(a)
+    assert calls == [("reg", a.ctypes.data, a.nbytes)]
+    pins.touch(a)
+    assert len(calls) == 1                  # already pinned
+    pins.touch(a[::2])                      # a view
+    pins.touch(a[:10])
+    pins.touch(np.zeros(16))                # small
+    pins.touch(np.zeros(16))
+    assert len(calls) == 1
+    ptr = a.ctypes.data
+    del a
+    gc.collect()
+    assert calls[-1] == ("unreg", ptr)
+    assert not pins._pinned
+
+
+def test_set_error_types_reset_and_partial_namespace():
+    """A namespace may define only some of the classes; None restores the
+    package's own classes."""
+    import types
+    import paper_1708_01135_b200 as ew
+    from paper_1708_01135_b200 import _lib
+    Mine = type("CoincidentParticlesError", (Exception,), {})
+    ew.set_error_types(types.SimpleNamespace(CoincidentParticlesError=Mine))
+    try:
+        with pytest.raises(Mine):
+            _lib.raise_for(_lib.EWB_ECOINCIDENT, "x")
+        with pytest.raises(ew.KSpaceEmptyError) as ei:
+            _lib.raise_for(_lib.EWB_EKSPACE, "x")
+        assert type(ei.value) is ew.KSpaceEmptyError
+    finally:
+        ew.set_error_types(None)
+    with pytest.raises(ew.CoincidentParticlesError) as ei:
+        _lib.raise_for(_lib.EWB_ECOINCIDENT, "x")
+    assert type(ei.value) is ew.CoincidentParticlesError

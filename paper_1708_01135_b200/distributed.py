@@ -204,8 +204,9 @@ class _Comm:
             recv[p] = b.to(device) if b.device != torch.device(device) else b
         return recv
 
-    def all_gather_rows(self, t, counts, width):
-        """Every rank's t (counts[r] rows) -> list of blocks by rank."""
+    def all_gather_rows(self, t, counts, width, need=True):
+        """Every rank's t (counts[r] rows) -> list of blocks by rank (need:
+        whether this rank uses them; NCCL receives them either way)."""
         if self.world == 1:
             return [t]
         m = int(max(counts))
@@ -285,9 +286,9 @@ class ThreadComm:
         self._done()
         return recv
 
-    def all_gather_rows(self, t, counts, width):
+    def all_gather_rows(self, t, counts, width, need=True):
         allv = self._post(t)
-        out = [a.to(t.device) for a in allv]
+        out = [a.to(t.device) for a in allv] if need else []
         self._done()
         return out
 
@@ -401,7 +402,7 @@ class SlabEwald:
             en[1] = 0.0                        # u_lr is complete on every rank
         return flocal, en
 
-    def evaluate_replicated(self, pos, q, force, rho_out=None):
+    def evaluate_replicated(self, pos, q, force, rho_out=None, apply=True):
         """Every rank holds the FULL configuration (the reference API): it
         takes its own rows' particles and its halo straight from it (no
         point-to-point exchange), and the forces of every rank's own + halo
@@ -410,19 +411,19 @@ class SlabEwald:
         synchronisations size the per-rank lists; the collectives are the
         S(k) all-reduce, the 4-double energy all-reduce and the all-gather."""
         if self._main is None:
-            return self._replicated(pos, q, force, rho_out)
+            return self._replicated(pos, q, force, rho_out, apply)
         cur = torch.cuda.current_stream(self.device)
         self._main.wait_stream(cur)
         try:
             with torch.cuda.stream(self._main):
                 self.st.set_stream(self._main)
-                out = self._replicated(pos, q, force, rho_out)
+                out = self._replicated(pos, q, force, rho_out, apply)
         finally:
             self.st.set_stream(None)
             cur.wait_stream(self._main)
         return out
 
-    def _replicated(self, pos, q, force, rho_out):
+    def _replicated(self, pos, q, force, rho_out, apply=True):
         st, comm, W = self.st, self.comm, self.world
         # particles grouped by row (one stable sort, one synchronisation):
         # every rank's own rows and halo rows are slices of `order`
@@ -443,7 +444,9 @@ class SlabEwald:
         u_sr, u_lr, u_self, err = en.tolist()
         if err:
             _raise_device_error(err)           # every rank, before any force is written
-        blocks = comm.all_gather_rows(flocal, sizes, 3)
+        blocks = comm.all_gather_rows(flocal, sizes, 3, need=apply)
+        if not apply:                          # another rank writes the caller's forces
+            return u_sr, u_lr, u_self
         idx = torch.cat([t for sl in lists for t in sl])
         force.index_add_(0, idx.to(force.device),
                          torch.cat(blocks).to(force.device) if len(blocks) > 1 else blocks[0])
@@ -547,11 +550,11 @@ def _resolve_devices(workers):
 class MultiDeviceEwald:
     """``EwaldSolver(box, params, workers=W)`` with W > 1: W GPUs driven by W
     host threads of the caller's process, each rank a SlabEwald over its rows
-    of cells (halo exchange, S(k) all-reduce, reverse force exchange) with a
-    ThreadGroup for the collectives.  Every rank reads the caller's full
-    configuration (the reference API hands it over whole), keeps its own
-    rows' particles, and writes their forces straight into the caller's
-    array -- disjoint rows, so no force reduction at all."""
+    of cells with a ThreadGroup for the collectives.  Every rank reads the
+    caller's full configuration (the reference API hands it over whole) and
+    takes its own rows and its halo from it (evaluate_replicated: S(k)
+    all-reduce, one all-gather of own + halo forces, summed by rank 0 into
+    the caller's array)."""
 
     def __init__(self, L, alpha, r_cutoff, m_int, coeff, devices, overlap=True):
         from concurrent.futures import ThreadPoolExecutor
@@ -586,13 +589,12 @@ class MultiDeviceEwald:
             sl.comm = comm
             tp = torch.from_numpy(pos).to(dev)
             tq = torch.from_numpy(q).to(dev)
-            mine = torch.nonzero(sl.owned_mask(st.rows(tp).long())).flatten()
-            f_own = torch.zeros((mine.shape[0], 3), dtype=torch.float64, device=dev)
+            # rank 0 sums every rank's own + halo forces (one all-gather)
+            f = torch.zeros((n, 3), dtype=torch.float64, device=dev) if r == 0 else None
             rho = (torch.empty(2 * self.n_stored, dtype=torch.float64, device=dev)
                    if want_rho else None)
-            u = sl.evaluate_local(tp[mine].contiguous(), tq[mine].contiguous(), f_own,
-                                  rho_out=rho)
-            return (u, mine.cpu().numpy(), f_own.cpu().numpy(),
+            u = sl.evaluate_replicated(tp, tq, f, rho_out=rho, apply=r == 0)
+            return (u, None if f is None else f.cpu().numpy(),
                     None if rho is None else rho.cpu().numpy())
         except BaseException:
             grp.abort()                    # release peers waiting at a barrier
@@ -616,8 +618,7 @@ class MultiDeviceEwald:
             import threading
             real = [e for e in errs if not isinstance(e, threading.BrokenBarrierError)]
             raise (real or errs)[0]
-        for _, idx, fo, _ in res:
-            force[idx] += fo
+        force += res[0][1]
         if rho_out is not None:
-            rho_out[:] = res[0][3]
+            rho_out[:] = res[0][2]
         return res[0][0]

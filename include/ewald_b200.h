@@ -172,6 +172,22 @@ int ewb_dev_rho_partial(ewb_handle *h, int64_t i0, int64_t i1,
  * internal C*S for the force gather, and u_lr = sum_k C_k |S_k|^2. */
 int ewb_dev_kspace_finalize(ewb_handle *h, const double *d_slots,
                             double *d_rho_out, double *u_lr);
+/* The multi-GPU S(k) reduction fused with the finalisation: d_slots[r]
+ * (host array of n_ranks <= 16 device pointers) are the ranks' partial
+ * pair-slot buffers (ewb_dev_rho_partial), read straight from peer memory
+ * (NVLink; enable with ewb_enable_peer_access) and summed in rank order
+ * inside the finalising kernel -- no separate all-reduce.  Every rank gets
+ * the same S; u_lr lands in the device energy slot (ewb_dev_energies).
+ * Replaces the reduce_global + finalize of engine.py:85-91 / ewald.py:457. */
+int ewb_dev_kspace_finalize_peer(ewb_handle *h, const double *const *d_slots, int n_ranks,
+                                 double *d_rho_out);
+int ewb_enable_peer_access(ewb_handle *h, int peer_device);
+/* One process per GPU: the S(k) partial in a dedicated allocation whose CUDA
+ * IPC handle (64 bytes) the ranks exchange once; each rank opens the others'
+ * (ewb_ipc_open) and ewb_dev_kspace_finalize_peer reads them over NVLink. */
+int ewb_ipc_slots(ewb_handle *h, void **d_ptr, unsigned char *handle64);
+int ewb_ipc_open(ewb_handle *h, const unsigned char *handle64, void **d_ptr);
+int ewb_ipc_close(ewb_handle *h, void *d_ptr);
 /* Reciprocal forces of particles [i0, i1), added into d_force (N,3). */
 int ewb_dev_recip_forces(ewb_handle *h, int64_t i0, int64_t i1,
                          double *d_force);

@@ -66,6 +66,11 @@ SIGNATURES = {
     "ewb_dev_slot_doubles": (_I64, [_P]),
     "ewb_dev_rho_partial": (_INT, [_P, _I64, _I64, _P]),
     "ewb_dev_kspace_finalize": (_INT, [_P, _P, _P, _P]),
+    "ewb_dev_kspace_finalize_peer": (_INT, [_P, _P, _INT, _P]),
+    "ewb_enable_peer_access": (_INT, [_P, _INT]),
+    "ewb_ipc_slots": (_INT, [_P, ctypes.POINTER(_P), _P]),
+    "ewb_ipc_open": (_INT, [_P, _P, ctypes.POINTER(_P)]),
+    "ewb_ipc_close": (_INT, [_P, _P]),
     "ewb_dev_recip_forces": (_INT, [_P, _I64, _I64, _P]),
     "ewb_dev_real_space": (_INT, [_P, _INT, _INT, _P, _P]),
     "ewb_dev_self_energy": (_INT, [_P, _P]),
@@ -497,6 +502,33 @@ class Handle:
     def dev_real_space_async(self, part, nparts, d_force):
         self._check(self.lib.ewb_dev_real_space(self.h, int(part), int(nparts),
                                                 d_force, None))
+
+    def dev_kspace_finalize_peer(self, d_slot_ptrs, d_rho_out=None):
+        """Sum the ranks' partial slots from their (peer) device pointers and
+        finalise, in one kernel."""
+        arr = (ctypes.c_void_p * len(d_slot_ptrs))(*[int(p) for p in d_slot_ptrs])
+        self._check(self.lib.ewb_dev_kspace_finalize_peer(self.h, arr, len(d_slot_ptrs),
+                                                          d_rho_out))
+
+    def ipc_slots(self):
+        """(device pointer, 64-byte IPC handle) of the handle's dedicated
+        S(k) partial buffer."""
+        ptr = _P()
+        hd = (ctypes.c_ubyte * 64)()
+        self._check(self.lib.ewb_ipc_slots(self.h, ctypes.byref(ptr), hd))
+        return int(ptr.value), bytes(hd)
+
+    def ipc_open(self, handle64):
+        ptr = _P()
+        hd = (ctypes.c_ubyte * 64).from_buffer_copy(handle64)
+        self._check(self.lib.ewb_ipc_open(self.h, hd, ctypes.byref(ptr)))
+        return int(ptr.value)
+
+    def ipc_close(self, ptr):
+        self._check(self.lib.ewb_ipc_close(self.h, _P(ptr)))
+
+    def enable_peer_access(self, peer_device):
+        self._check(self.lib.ewb_enable_peer_access(self.h, int(peer_device)))
 
     def dev_kspace_finalize_async(self, d_slots, d_rho_out=None):
         self._check(self.lib.ewb_dev_kspace_finalize(self.h, d_slots, d_rho_out,

@@ -296,6 +296,8 @@ struct ewb_handle {
   int rs_split = K6_SPLIT;        // two-pass real space (pair lists in HBM), off by default
   DBuf rs_list, rs_count;         // per-unit pair lists and their lengths
   DBuf ro_key, ro_keyout, ro_idx, ro_cnt, ro_g, ro_tmp;  // ewb_dev_row_order scratch
+  void *ipc_slots = nullptr;      // dedicated allocation of the S(k) partial (CUDA IPC export)
+  size_t ipc_bytes = 0;
   // Verlet pair lists (ewb_set_skin): lists built at r_c + skin are reused
   // while no particle has moved more than skin/2 since the build
   double skin = 0.0;
@@ -449,6 +451,7 @@ void ewb_destroy(ewb_handle *h) {
                   &h->rs_list, &h->rs_count, &h->vl_xb, &h->vl_dmax, &h->ro_key, &h->ro_keyout,
                   &h->ro_idx, &h->ro_cnt, &h->ro_g, &h->ro_tmp})
     b->release();
+  if (h->ipc_slots) cudaFree(h->ipc_slots);
   if (h->hscr) cudaFreeHost(h->hscr);
   h->plan.release();
   for (auto &ge : h->gexec)
@@ -896,6 +899,85 @@ int ewb_dev_kspace_finalize(ewb_handle *h, const double *d_slots, double *d_rho_
                        h->stream));
     CK(cudaStreamSynchronize(h->stream));
   }
+  return EWB_OK;
+}
+
+int ewb_dev_kspace_finalize_peer(ewb_handle *h, const double *const *d_slots, int n_ranks,
+                                 double *d_rho_out) {
+  int rc = require_state(h, true, false);
+  if (rc) return rc;
+  if (!d_slots || n_ranks < 1 || n_ranks > K2P_MAX_PEERS)
+    return h->fail(EWB_EINVAL, "1..16 peer slot buffers");
+  CK(cudaSetDevice(h->device));
+  CK(h->energy.ensure(8 * sizeof(double)));
+  Plan &P = h->plan;
+  const int64_t n_pslots = (int64_t)P.M1 * P.n_pitems;
+  PeerSlots ps{};
+  for (int r = 0; r < n_ranks; ++r) {
+    if (!d_slots[r]) return h->fail(EWB_EINVAL, "null peer slot buffer");
+    ps.p[r] = reinterpret_cast<const double4 *>(d_slots[r]);
+  }
+  ps.n = n_ranks;
+  const unsigned nb = blocks_for(n_pslots, K2P_THREADS);
+  CK(h->eblk_r.ensure(nb * sizeof(double)));
+  k2p_finalize_peer<<<nb, K2P_THREADS, 0, h->stream>>>(ps, n_pslots, P.pslot_map.as<int4>(),
+                                                       P.slot_coeff.as<double>(), P.K, d_rho_out,
+                                                       h->sp.as<double2>(), h->eblk_r.as<double>());
+  CKL();
+  k_sum<<<1, 1024, 0, h->stream>>>(h->eblk_r.as<double>(), nb, 1.0, h->energy.as<double>() + 1);
+  CKL();
+  return EWB_OK;
+}
+
+int ewb_ipc_slots(ewb_handle *h, void **d_ptr, unsigned char *handle64) {
+  int rc = require_state(h, true, false);
+  if (rc) return rc;
+  if (!d_ptr || !handle64) return h->fail(EWB_EINVAL, "null output");
+  CK(cudaSetDevice(h->device));
+  const size_t bytes = (size_t)h->plan.M1 * h->plan.n_pitems * sizeof(double4);
+  if (bytes != h->ipc_bytes) {
+    if (h->ipc_slots) CK(cudaFree(h->ipc_slots));
+    h->ipc_slots = nullptr;
+    h->ipc_bytes = 0;
+    CK(cudaMalloc(&h->ipc_slots, bytes ? bytes : 16));
+    h->ipc_bytes = bytes;
+  }
+  cudaIpcMemHandle_t hd;
+  CK(cudaIpcGetMemHandle(&hd, h->ipc_slots));
+  std::memcpy(handle64, &hd, sizeof hd < 64 ? sizeof hd : 64);
+  *d_ptr = h->ipc_slots;
+  return EWB_OK;
+}
+
+int ewb_ipc_open(ewb_handle *h, const unsigned char *handle64, void **d_ptr) {
+  if (!h || !handle64 || !d_ptr) return EWB_EINVAL;
+  CK(cudaSetDevice(h->device));
+  cudaIpcMemHandle_t hd;
+  std::memcpy(&hd, handle64, sizeof hd);
+  CK(cudaIpcOpenMemHandle(d_ptr, hd, cudaIpcMemLazyEnablePeerAccess));
+  return EWB_OK;
+}
+
+int ewb_ipc_close(ewb_handle *h, void *d_ptr) {
+  if (!h || !d_ptr) return EWB_EINVAL;
+  CK(cudaSetDevice(h->device));
+  CK(cudaIpcCloseMemHandle(d_ptr));
+  return EWB_OK;
+}
+
+int ewb_enable_peer_access(ewb_handle *h, int peer_device) {
+  if (!h) return EWB_EINVAL;
+  if (peer_device == h->device) return EWB_OK;
+  CK(cudaSetDevice(h->device));
+  int can = 0;
+  CK(cudaDeviceCanAccessPeer(&can, h->device, peer_device));
+  if (!can) return h->fail(EWB_ECUDA, "no peer access between the devices");
+  const cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return EWB_OK;
+  }
+  CK(e);
   return EWB_OK;
 }
 

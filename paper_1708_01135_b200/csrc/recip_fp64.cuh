@@ -209,6 +209,75 @@ __global__ void __launch_bounds__(RED_THREADS)
 #ifndef K2P_THREADS
 #define K2P_THREADS 64  // small blocks: the slots spread over every SM (c2: 54 -> 216 blocks)
 #endif
+// finalisation of one summed pair slot A = (A+, A-): S(+-m_x), rho into the
+// caller's k order, C*S into the gather's layout; returns its C |S|^2
+__device__ __forceinline__ double k2p_emit(const double4 A, int64_t s,
+                                           const int4 *__restrict__ pmap,
+                                           const double *__restrict__ slot_coeff, int64_t K,
+                                           double *__restrict__ rho_out,
+                                           double2 *__restrict__ sp) {
+  double e = 0.0;
+  const int4 mp = pmap[s];
+  const double2 Sp_ = make_double2(0.5 * (A.x + A.w), 0.5 * (A.y - A.z));  // +m_x
+  const double2 Sm_ = make_double2(0.5 * (A.x - A.w), 0.5 * (A.y + A.z));  // -m_x
+  if (mp.x >= 0) {
+    if (rho_out) {
+      rho_out[mp.x] = Sp_.x;
+      rho_out[K + mp.x] = Sp_.y;
+    }
+    const double C = slot_coeff[mp.z];
+    sp[mp.z] = make_double2(C * Sp_.x, C * Sp_.y);
+    e += C * (Sp_.x * Sp_.x + Sp_.y * Sp_.y);
+  }
+  if (mp.y >= 0) {
+    if (rho_out) {
+      rho_out[mp.y] = Sm_.x;
+      rho_out[K + mp.y] = Sm_.y;
+    }
+    const double C = slot_coeff[mp.w];
+    sp[mp.w] = make_double2(C * Sm_.x, C * Sm_.y);
+    e += C * (Sm_.x * Sm_.x + Sm_.y * Sm_.y);
+  }
+  return e;
+}
+
+// The ranks' S(k) partials (pair-slot layout) summed straight from their
+// buffers -- peer memory over NVLink (or the same device) -- in rank order,
+// then finalised: the all-reduce and the finalisation in ONE kernel.  Every
+// rank runs it over the same pointers, so every rank gets bitwise the same S.
+constexpr int K2P_MAX_PEERS = 16;
+struct PeerSlots {
+  const double4 *p[K2P_MAX_PEERS];
+  int n;
+};
+__global__ void __launch_bounds__(K2P_THREADS)
+    k2p_finalize_peer(PeerSlots parts, int64_t n_pslots, const int4 *__restrict__ pmap,
+                      const double *__restrict__ slot_coeff, int64_t K,
+                      double *__restrict__ rho_out, double2 *__restrict__ sp,
+                      double *__restrict__ epart) {
+  __shared__ double sh[K2P_THREADS / 32];
+  const int64_t s = blockIdx.x * (int64_t)K2P_THREADS + threadIdx.x;
+  double e = 0.0;
+  if (s < n_pslots) {
+    double4 v[K2P_MAX_PEERS];
+#pragma unroll
+    for (int r = 0; r < K2P_MAX_PEERS; ++r)
+      if (r < parts.n) v[r] = ldcs4(parts.p[r] + s);
+    double4 A = make_double4(0.0, 0.0, 0.0, 0.0);
+#pragma unroll
+    for (int r = 0; r < K2P_MAX_PEERS; ++r) {
+      if (r < parts.n) {
+        A.x += v[r].x;
+        A.y += v[r].y;
+        A.z += v[r].z;
+        A.w += v[r].w;
+      }
+    }
+    e = k2p_emit(A, s, pmap, slot_coeff, K, rho_out, sp);
+  }
+  const double b = block_sum<K2P_THREADS>(e, sh);
+  if (threadIdx.x == 0) epart[blockIdx.x] = b;
+}
 __global__ void __launch_bounds__(K2P_THREADS)
     k2p_finalize(const double4 *__restrict__ spart, int n_part, int64_t n_pslots,
                  const int4 *__restrict__ pmap, const double *__restrict__ slot_coeff, int64_t K,
@@ -240,29 +309,7 @@ __global__ void __launch_bounds__(K2P_THREADS)
       A.w += v.w;
     }
     if (s_out) s_out[s] = A;
-    if (finalize) {
-      const int4 mp = pmap[s];
-      const double2 Sp_ = make_double2(0.5 * (A.x + A.w), 0.5 * (A.y - A.z));  // +m_x
-      const double2 Sm_ = make_double2(0.5 * (A.x - A.w), 0.5 * (A.y + A.z));  // -m_x
-      if (mp.x >= 0) {
-        if (rho_out) {
-          rho_out[mp.x] = Sp_.x;
-          rho_out[K + mp.x] = Sp_.y;
-        }
-        const double C = slot_coeff[mp.z];
-        sp[mp.z] = make_double2(C * Sp_.x, C * Sp_.y);
-        e += C * (Sp_.x * Sp_.x + Sp_.y * Sp_.y);
-      }
-      if (mp.y >= 0) {
-        if (rho_out) {
-          rho_out[mp.y] = Sm_.x;
-          rho_out[K + mp.y] = Sm_.y;
-        }
-        const double C = slot_coeff[mp.w];
-        sp[mp.w] = make_double2(C * Sm_.x, C * Sm_.y);
-        e += C * (Sm_.x * Sm_.x + Sm_.y * Sm_.y);
-      }
-    }
+    if (finalize) e = k2p_emit(A, s, pmap, slot_coeff, K, rho_out, sp);
   }
   if (finalize) {
     const double b = block_sum<K2P_THREADS>(e, sh);

@@ -134,11 +134,23 @@ class DeviceStages:
         self.h.dev_real_space_rows_async(lo, hi, force.data_ptr())
 
     def rho_partial(self, i0, i1, slots):
-        self.h.dev_rho_partial(i0, i1, slots.data_ptr())
+        self.h.dev_rho_partial(i0, i1, slots if isinstance(slots, int) else slots.data_ptr())
+
+    def ipc_slots(self):
+        return self.h.ipc_slots()
+
+    def ipc_open(self, handle64):
+        return self.h.ipc_open(handle64)
 
     def finalize(self, slots, rho_out=None):
         self.h.dev_kspace_finalize_async(
             slots.data_ptr(), None if rho_out is None else rho_out.data_ptr())
+
+    def finalize_peer(self, slot_ptrs, rho_out=None):
+        """S(k) = sum of the ranks' partial slots read from peer memory, and
+        its finalisation, in one kernel (ewb_dev_kspace_finalize_peer)."""
+        self.h.dev_kspace_finalize_peer(slot_ptrs,
+                                        None if rho_out is None else rho_out.data_ptr())
 
     def recip_forces(self, i0, i1, force):
         self.h.dev_recip_forces(i0, i1, force.data_ptr())
@@ -165,6 +177,38 @@ class _Comm:
 
     def _to(self, t):
         return t.to(self.dev) if t.device != self.dev else t
+
+    # ---- S(k) reduction fused into the finalisation over CUDA IPC (opt-in:
+    # EWALDB200_PEER_FINALIZE=1).  The ranks export their partial buffers once;
+    # per step two host barriers bracket the kernel that reads every rank's
+    # partial over NVLink (instead of one asynchronous NCCL all-reduce).
+    def fused(self, st):
+        import os
+        return (self.world > 1 and hasattr(st, "ipc_slots") and hasattr(st, "finalize_peer")
+                and os.environ.get("EWALDB200_PEER_FINALIZE", "0") == "1")
+
+    def slot_ptr(self, st):
+        ptr, handle = st.ipc_slots()
+        if getattr(self, "_ipc_mine", None) != ptr:
+            mine = torch.frombuffer(bytearray(handle), dtype=torch.uint8)
+            allh = [torch.empty(64, dtype=torch.uint8) for _ in range(self.world)]
+            if self.host:
+                dist.all_gather(allh, mine, group=self.group)
+            else:
+                dev_h = [a.to(self.dev) for a in allh]
+                dist.all_gather(dev_h, mine.to(self.dev), group=self.group)
+                allh = [a.cpu() for a in dev_h]
+            self._ipc_ptrs = [ptr if r == self.rank else st.ipc_open(bytes(allh[r].tolist()))
+                              for r in range(self.world)]
+            self._ipc_mine = ptr
+        return ptr
+
+    def peer_finalize(self, st, ptr, rho_out):
+        torch.cuda.current_stream().synchronize()   # my partial is complete
+        dist.barrier(group=self.group)               # ... and every rank's
+        st.finalize_peer(self._ipc_ptrs, rho_out)
+        torch.cuda.current_stream().synchronize()
+        dist.barrier(group=self.group)               # peers done reading mine
 
     def allreduce_(self, t):
         if self.world == 1:
@@ -292,6 +336,21 @@ class ThreadComm:
         self._done()
         return out
 
+    def fused(self, st):
+        return hasattr(st, "finalize_peer")
+
+    def slot_ptr(self, st):
+        return None                               # the rank's own slot tensor
+
+    def peer_finalize(self, st, ptr, rho_out):
+        """The S(k) all-reduce fused into the finalisation: once every
+        rank's partial is complete, each rank's kernel reads all of them
+        through peer pointers (NVLink); the closing barrier keeps the
+        buffers alive until every rank's kernel is done."""
+        allv = self._post(ptr)
+        st.finalize_peer(list(allv), rho_out)
+        self._done()
+
 
 def _raise_device_error(flag):
     flag = int(flag)
@@ -383,9 +442,17 @@ class SlabEwald:
             st.set_stream(self._main)
         else:
             st.real_space_rows(self.lo, self.hi, flocal)
-        st.rho_partial(0, n_own, self._slots)
-        comm.allreduce_(self._slots)          # S(k) = sum of the ranks' partials
-        st.finalize(self._slots, rho_out)
+        if comm.fused(st):
+            # every rank's finalising kernel sums the partials from peer memory
+            ptr = comm.slot_ptr(st)
+            if ptr is None:
+                ptr = self._slots.data_ptr()
+            st.rho_partial(0, n_own, ptr)
+            comm.peer_finalize(st, ptr, rho_out)
+        else:
+            st.rho_partial(0, n_own, self._slots)
+            comm.allreduce_(self._slots)      # S(k) = sum of the ranks' partials
+            st.finalize(self._slots, rho_out)
         if self._side is not None:
             # the reciprocal forces into their own buffer, so the force GEMM
             # runs while the pair kernel is still busy on the side stream
@@ -571,6 +638,11 @@ class MultiDeviceEwald:
             h.set_kspace(m_int, coeff)
             return h
         self.handles = list(self.pool.map(make, range(self.world)))
+        # peer access between the ranks' GPUs: the fused S(k) reduction reads
+        # the other ranks' partials over NVLink
+        for r, h in enumerate(self.handles):
+            for d in {dv.index for dv in self.devices}:
+                h.enable_peer_access(d)
         self.stages = [DeviceStages(h) for h in self.handles]
         self.slabs = [None] * self.world
 

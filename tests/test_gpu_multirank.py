@@ -61,8 +61,14 @@ def _worker(rank, world, port, name, out_dir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name,world", [("c2", 2), ("c3", 2), ("c4", 4), ("c4", 8), ("c5", 2)])
-def test_sharded_device_stages_match_golden(tmp_path, name, world):
+@pytest.mark.parametrize("name,world,peer", [("c2", 2, "0"), ("c3", 2, "0"), ("c4", 4, "0"),
+                                             ("c4", 8, "0"), ("c5", 2, "0"), ("c2", 2, "1"),
+                                             ("c4", 4, "1")])
+def test_sharded_device_stages_match_golden(tmp_path, monkeypatch, name, world, peer):
+    """peer = "1": the S(k) reduction fused into the finalising kernel, which
+    reads the other ranks' partials through CUDA IPC (the ranks are
+    processes; here they share the one GPU)."""
+    monkeypatch.setenv("EWALDB200_PEER_FINALIZE", peer)
     import torch.multiprocessing as mp
     g = golden(name)
     port = _free_port()
@@ -160,3 +166,44 @@ def test_solver_workers_wide_cutoff_stays_single_gpu(monkeypatch):
     res = solver.evaluate(ps)
     assert rel(res.u_sr, float(g["u_sr"])) <= 1e-10
     assert rel(res.u_lr, float(g["u_lr"])) <= 1e-10
+
+
+def test_peer_finalize_equals_allreduce_then_finalize():
+    """ewb_dev_kspace_finalize_peer (the S(k) reduction read from the ranks'
+    buffers inside the finalising kernel) gives bitwise the rho and u_lr of
+    summing the partials first and finalising them."""
+    import torch
+    import paper_1708_01135_b200 as ew
+    from paper_1708_01135_b200 import _lib
+    from paper_1708_01135_b200 import workloads as wl
+    cfg = wl.make_config("c2", seed=0)
+    dev = torch.device("cuda", 0)
+    params = ew.EwaldParams(cfg["alpha_ref"], cfg["r_cutoff"], wl.k_cutoff_for(cfg), 1e-6)
+    rs = ew.ReciprocalSpace(cfg["box"], params, cfg["m_int"])
+    h = _lib.Handle(0)
+    st = torch.cuda.Stream()
+    h.set_stream(st.cuda_stream)
+    h.set_system(cfg["L"], params.alpha, params.r_cutoff)
+    h.set_kspace(rs.m_int, rs.coeff)
+    pos = torch.from_numpy(cfg["pos"]).to(dev)
+    q = torch.from_numpy(cfg["q"]).to(dev)
+    n = q.shape[0]
+    ns = h.dev_slot_doubles()
+    parts = [torch.empty(ns, dtype=torch.float64, device=dev) for _ in range(3)]
+    cuts = [0, n // 3, (2 * n) // 3, n]
+    with torch.cuda.stream(st):
+        h.dev_load(pos.data_ptr(), q.data_ptr(), n)
+        for r in range(3):
+            h.dev_rho_partial(cuts[r], cuts[r + 1], parts[r].data_ptr())
+        summed = parts[0].clone()
+        summed += parts[1]
+        summed += parts[2]
+        rho_a = torch.empty(2 * rs.n_stored, dtype=torch.float64, device=dev)
+        rho_b = torch.empty_like(rho_a)
+        u_a = h.dev_kspace_finalize(summed.data_ptr(), rho_a.data_ptr())
+        h.dev_kspace_finalize_peer([p.data_ptr() for p in parts], rho_b.data_ptr())
+        e = torch.zeros(3, dtype=torch.float64, device=dev)
+        h.dev_energies(e.data_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(rho_a, rho_b)
+    assert e[1].item() == u_a

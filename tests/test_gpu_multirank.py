@@ -207,3 +207,52 @@ def test_peer_finalize_equals_allreduce_then_finalize():
     torch.cuda.synchronize()
     assert torch.equal(rho_a, rho_b)
     assert e[1].item() == u_a
+
+
+def _worker_err(rank, world, port, out_dir):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1708_01135_b200 as ew
+        from paper_1708_01135_b200 import _lib
+        from paper_1708_01135_b200 import workloads as wl
+        from paper_1708_01135_b200.distributed import DeviceStages, ShardedEwald
+        cfg = wl.make_config("c2", seed=0)
+        dev = torch.device("cuda", 0)
+        torch.cuda.set_device(dev)
+        params = ew.EwaldParams(cfg["alpha_ref"], cfg["r_cutoff"], wl.k_cutoff_for(cfg), 1e-6)
+        rs = ew.ReciprocalSpace(cfg["box"], params, cfg["m_int"])
+        h = _lib.Handle(0)
+        h.set_system(cfg["L"], params.alpha, params.r_cutoff)
+        h.set_kspace(rs.m_int, rs.coeff)
+        pos = cfg["pos"].copy()
+        pos[11] = pos[12]                   # a coincident pair in one rank's slab
+        pd = torch.from_numpy(pos).to(dev)
+        q = torch.from_numpy(cfg["q"]).to(dev)
+        f = torch.full((q.shape[0], 3), 0.5, dtype=torch.float64, device=dev)
+        what = "none"
+        try:
+            ShardedEwald(DeviceStages(h), dev).evaluate(pd, q, f)
+        except ew.CoincidentParticlesError:
+            what = "coincident"
+        untouched = bool(torch.all(f == 0.5).item())
+        np.savez(os.path.join(out_dir, f"err{rank}.npz"), what=np.array(what),
+                 untouched=np.array(untouched))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_error_raised_on_every_rank(tmp_path):
+    """A coincident pair in one rank's rows: the device error flag travels
+    with the energies, so EVERY rank raises CoincidentParticlesError and no
+    rank writes its force array."""
+    import torch.multiprocessing as mp
+    world = 3
+    mp.spawn(_worker_err, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        got = np.load(tmp_path / f"err{r}.npz")
+        assert str(got["what"]) == "coincident"
+        assert bool(got["untouched"])

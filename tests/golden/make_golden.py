@@ -202,6 +202,18 @@ def md_cases():
          max_disp=m.max_step_displacement)
 
 
+def nve_acceptance_case():
+    """The reference's acceptance criterion 8 run (test_acceptance.py:226-239):
+    N=1728, Coulomb + LJ, dt 0.01, 1000 NVE steps; its energy trace and
+    drift (the reference measures 4.19e-4 here, above the criterion's 1e-4)."""
+    cfg = em.SimConfig(n_particles=1728, box_edge=30.0, tolerance=1e-6, dt=0.01,
+                       n_steps=1000, velocity_scale=0.05, threads=WORKERS, seed=8,
+                       coulomb_on=True, lj_on=True)
+    m = em.run(cfg)
+    save("md_nve1000", energy_trace=np.array(m.energy_trace), drift=m.drift,
+         max_disp=m.max_step_displacement)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["small", "c1", "c2", "c3", "c4", "c5"]
     for w in which:
@@ -209,5 +221,7 @@ if __name__ == "__main__":
             small_cases()
         elif w == "md":
             md_cases()
+        elif w == "nve":
+            nve_acceptance_case()
         else:
             config_case(w)

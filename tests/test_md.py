@@ -183,3 +183,24 @@ def test_device_md_skin_on_scan_all_box_matches_golden(md):
     assert np.abs(ps.position - g["pos_final"]).max() <= 1e-10
     et = np.array(m.energy_trace)
     assert np.abs(et - g["energy_trace"]).max() <= 1e-9 * np.abs(g["energy_trace"]).max()
+
+
+def test_nve_conservation_acceptance_8(md):
+    """The reference's acceptance criterion 8 run (test_acceptance.py:226-239):
+    N=1728 rock salt, Coulomb + LJ, dt 0.01, 1000 NVE steps on the device.
+    The reference itself measures a drift of 4.19e-4 here (above the
+    criterion's 1e-4; tests/golden/md_nve1000.npz, generated by running it):
+    the device run reproduces the reference's energy trace and drift, and
+    the criterion's displacement bound holds."""
+    g = golden("md_nve1000")
+    cfg = md.SimConfig(n_particles=1728, box_edge=30.0, tolerance=1e-6, dt=0.01,
+                       n_steps=1000, velocity_scale=0.05, threads=2, seed=8,
+                       coulomb_on=True, lj_on=True)
+    m = md.run(cfg)
+    et = np.array(m.energy_trace)
+    ref = g["energy_trace"]
+    # 1000 chaotic steps: early steps agree to rounding, the end to ~1e-8
+    assert np.abs(et[:101] - ref[:101]).max() <= 1e-9 * np.abs(ref).max()
+    assert np.abs(et - ref).max() <= 1e-6 * np.abs(ref).max()
+    assert abs(m.drift - float(g["drift"])) <= 1e-3 * float(g["drift"])
+    assert m.max_step_displacement < 0.05

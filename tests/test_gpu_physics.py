@@ -125,3 +125,22 @@ def test_translation_invariance_and_net_force(ew, name):
     assert abs(u1 - u0) / abs(u0) <= 1e-10
     residual = np.linalg.norm(f0.sum(axis=0))
     assert residual <= 1e-8 * np.abs(f0).max() * ps.count
+
+
+def test_alpha_invariance_nacl_1728_acceptance_3(ew):
+    """The reference's acceptance criterion 3 (test_acceptance.py:106-128):
+    jittered rock salt 12^3 (N=1728, spacing 2.5), alpha x0.5 (r_c > L/2:
+    the image-shell real space on the device) and x2: |dU|/U <= 5e-6."""
+    from paper_1708_01135_b200 import md
+    ps = md.init_rocksalt(6, 2.5)
+    rng = np.random.default_rng(3)
+    ps.position += 0.1 * rng.standard_normal(ps.position.shape)
+    ps.wrap()
+    base = ew.choose_parameters(ps.count, ps.box, 1e-6)
+
+    def total(params):
+        ps.force[:] = 0.0
+        return ew.total_coulomb(ps, params)
+    u0 = total(base)
+    worst = max(abs(total(params_for(ew, base.alpha * f)) - u0) / abs(u0) for f in (0.5, 2.0))
+    assert worst <= 5e-6
